@@ -1,0 +1,626 @@
+/*
+ * pp_oracle.c — TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, single-threaded CPU implementation of what the hot path of
+ * arXiv 1907.13257 computes (as read in SURVEY.md §8(c), readings R1–R20,
+ * definitions O1–O12).  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no
+ * code, header, table or constant generator with the CUDA path in
+ * paper_1907_13257_b200/ and neither side imports the other.
+ *
+ * Arithmetic: unsigned 64-bit integers for times (picoseconds), unsigned
+ * __int128 for products.  No floating point anywhere in a compared result.
+ *
+ * Citations: "PAPER.md:L" are line numbers of /root/reference/PAPER.md with
+ * the section/equation they fall in; "SPEC.md:L" likewise for SPEC.md.
+ *
+ * Parity status per function (see DESIGN.md §Oracle pins):
+ *   or_prepare / or_pi         pinned (SPEC Kahn examples, brute-force tests)
+ *   or_schedule                pinned (K1–K7, brute-force longest path, invariants)
+ *   or_gen (GRAY)              pinned (Gray property: one digit changes per step,
+ *                              bijection onto [0,M)^K; M=2 equals i^(i>>1))
+ *   or_gen (RANDOM, PERTURB)   pinned (SplitMix64 published test vector of the
+ *                              finaliser; distribution/flip-rate properties)
+ *   or_round / or_search       pinned (K2, K3, K8, exhaustive == brute force)
+ *   or_ar                      pinned (K9 closed form)
+ *   or_epochs / or_cell        pinned (K10–K12 paper ratios)
+ *   or_crossover               pinned (K10–K14 paper statements)
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <stdio.h>
+
+typedef unsigned __int128 u128;
+
+#define OR_OK 0
+#define OR_E_INVALID (-1)
+#define OR_E_CYCLE (-2)
+#define OR_E_RANGE (-3)
+#define OR_E_TOO_LARGE (-4)
+#define OR_E_INFEASIBLE (-5)
+
+#define OR_INFEASIBLE_MAKESPAN UINT64_MAX
+
+/* ---------------------------------------------------------------- O1 inputs */
+/* PAPER.md:350 (§6): DFG vertices K with Δ(k) and M(k), edges E with D(e);
+ * links with bandwidth B(l); Table 2 PAPER.md:365–392.
+ * R1: every op has a forward time Δf and a backward time Δb; every edge has
+ * activation bytes D_f and gradient bytes D_b (default D_b = D_f).           */
+typedef struct {
+    int32_t K, E;
+    const int64_t *op_id;          /* external ids, NULL => 0..K-1 */
+    const uint64_t *fwd_ps;        /* Δf(k) */
+    const uint64_t *bwd_ps;        /* Δb(k) */
+    const uint64_t *mem_bytes;     /* M(k), NULL => 0 */
+    const uint64_t *param_bytes;   /* weight bytes, NULL => 0 */
+    const int32_t *edge_src, *edge_dst;
+    const uint64_t *edge_fwd_bytes;
+    const uint64_t *edge_bwd_bytes; /* NULL => = fwd */
+    uint64_t link_bw_Bps, link_lat_ps, dev_mem_cap_bytes; /* cap 0 = unlimited */
+} or_input;
+
+typedef struct {
+    int K, E;
+    int64_t *id;        /* external id, original index order */
+    int *pi;            /* pi[p]  = original index of the op at π position p */
+    int *pos;           /* pos[k] = π position of original op k            */
+    /* everything below is indexed by π position */
+    uint64_t *df, *db, *mem;
+    /* adjacency lists by π position: in-edges and out-edges */
+    int *in_cnt, **in_src;  uint64_t **in_cf;
+    int *out_cnt, **out_dst; uint64_t **out_cb;
+    uint64_t cap;
+    uint64_t t1;
+    uint64_t grad_bytes;
+} or_ctx;
+
+static void set_err(char *err, int errlen, const char *msg) {
+    if (err && errlen > 0) { strncpy(err, msg, (size_t)errlen - 1); err[errlen - 1] = 0; }
+}
+
+/* O3: c(e) = ⌈D(e)·10^12 / BW⌉ + L  (§6 Δ_e = Σ_l C_el·(D(e)/B(l)+L(l)),
+ * reduced to one logical hop by reading R4).                                  */
+uint64_t or_edge_cost(uint64_t bytes, uint64_t bw, uint64_t lat, int *overflow) {
+    u128 num = (u128)bytes * (u128)1000000000000ULL;
+    u128 q = num / bw;
+    if (num % bw) q += 1;
+    q += lat;
+    if (q >> 64) { if (overflow) *overflow = 1; return UINT64_MAX; }
+    return (uint64_t)q;
+}
+
+void or_free(or_ctx *c) {
+    if (!c) return;
+    for (int p = 0; p < c->K; p++) {
+        if (c->in_src) free(c->in_src[p]);
+        if (c->in_cf) free(c->in_cf[p]);
+        if (c->out_dst) free(c->out_dst[p]);
+        if (c->out_cb) free(c->out_cb[p]);
+    }
+    free(c->in_src); free(c->in_cf); free(c->out_dst); free(c->out_cb);
+    free(c->in_cnt); free(c->out_cnt);
+    free(c->id); free(c->pi); free(c->pos); free(c->df); free(c->db); free(c->mem);
+    free(c);
+}
+
+/* O2: π = Kahn's algorithm; among ready ops pop the smallest external id
+ * (reading R3).  Plain O(K^2) selection.                      */
+static int kahn(int K, int E, const int64_t *id, const int32_t *src, const int32_t *dst,
+                int *pi, char *err, int errlen) {
+    int *indeg = calloc((size_t)K, sizeof(int));
+    char *done = calloc((size_t)K, 1);
+    for (int e = 0; e < E; e++) indeg[dst[e]]++;
+    int n = 0;
+    while (n < K) {
+        int best = -1;
+        for (int k = 0; k < K; k++)
+            if (!done[k] && indeg[k] == 0 && (best < 0 || id[k] < id[best])) best = k;
+        if (best < 0) break;
+        done[best] = 1;
+        pi[n++] = best;
+        for (int e = 0; e < E; e++) if (src[e] == best) indeg[dst[e]]--;
+    }
+    if (n < K) {
+        /* report one cycle: walk backwards along unfinished
+         * predecessors from any unfinished op until an op repeats            */
+        int *seen = malloc(sizeof(int) * (size_t)K);
+        for (int k = 0; k < K; k++) seen[k] = -1;
+        int v = -1;
+        for (int k = 0; k < K; k++) if (!done[k]) { v = k; break; }
+        int step = 0;
+        while (seen[v] < 0) {
+            seen[v] = step++;
+            int u = -1;
+            for (int e = 0; e < E; e++) if (dst[e] == v && !done[src[e]]) { u = src[e]; break; }
+            v = u;
+        }
+        /* v is on the cycle: collect it */
+        char msg[512]; int off = snprintf(msg, sizeof msg, "cycle:");
+        int start = v, guard = 0;
+        do {
+            off += snprintf(msg + off, sizeof msg - (size_t)off, " %lld", (long long)id[v]);
+            int u = -1;
+            for (int e = 0; e < E; e++) if (dst[e] == v && !done[src[e]]) { u = src[e]; break; }
+            v = u; guard++;
+        } while (v != start && guard <= K && off < 480);
+        set_err(err, errlen, msg);
+        free(seen); free(indeg); free(done);
+        return OR_E_CYCLE;
+    }
+    free(indeg); free(done);
+    return OR_OK;
+}
+
+int or_prepare(const or_input *in, or_ctx **out, char *err, int errlen) {
+    *out = NULL;
+    int K = in->K, E = in->E;
+    if (K < 1 || E < 0 || !in->fwd_ps || !in->bwd_ps || (E > 0 && (!in->edge_src || !in->edge_dst || !in->edge_fwd_bytes))) {
+        set_err(err, errlen, "invalid sizes or null arrays"); return OR_E_INVALID;
+    }
+    if (in->link_bw_Bps == 0) { set_err(err, errlen, "link bandwidth must be > 0"); return OR_E_INVALID; }
+    int64_t *id = malloc(sizeof(int64_t) * (size_t)K);
+    for (int k = 0; k < K; k++) id[k] = in->op_id ? in->op_id[k] : k;
+    for (int k = 0; k < K; k++) {
+        if (id[k] < 0) { set_err(err, errlen, "negative op id"); free(id); return OR_E_INVALID; }
+        for (int j = 0; j < k; j++)
+            if (id[j] == id[k]) { set_err(err, errlen, "duplicate op id"); free(id); return OR_E_INVALID; }
+    }
+    for (int e = 0; e < E; e++) {
+        if (in->edge_src[e] < 0 || in->edge_src[e] >= K || in->edge_dst[e] < 0 || in->edge_dst[e] >= K) {
+            set_err(err, errlen, "dangling edge endpoint"); free(id); return OR_E_INVALID;
+        }
+        if (in->edge_src[e] == in->edge_dst[e]) { set_err(err, errlen, "self edge"); free(id); return OR_E_INVALID; }
+    }
+    int *pi = malloc(sizeof(int) * (size_t)K);
+    int rc = kahn(K, E, id, in->edge_src, in->edge_dst, pi, err, errlen);
+    if (rc) { free(id); free(pi); return rc; }
+
+    or_ctx *c = calloc(1, sizeof(or_ctx));
+    c->K = K; c->E = E; c->id = id; c->pi = pi;
+    c->pos = malloc(sizeof(int) * (size_t)K);
+    for (int p = 0; p < K; p++) c->pos[pi[p]] = p;
+    c->df = malloc(8 * (size_t)K); c->db = malloc(8 * (size_t)K); c->mem = malloc(8 * (size_t)K);
+    for (int p = 0; p < K; p++) {
+        int k = pi[p];
+        c->df[p] = in->fwd_ps[k];
+        c->db[p] = in->bwd_ps[k];
+        c->mem[p] = in->mem_bytes ? in->mem_bytes[k] : 0;
+    }
+    c->cap = in->dev_mem_cap_bytes;
+    c->in_cnt = calloc((size_t)K, sizeof(int)); c->out_cnt = calloc((size_t)K, sizeof(int));
+    c->in_src = calloc((size_t)K, sizeof(int *)); c->in_cf = calloc((size_t)K, sizeof(uint64_t *));
+    c->out_dst = calloc((size_t)K, sizeof(int *)); c->out_cb = calloc((size_t)K, sizeof(uint64_t *));
+    for (int e = 0; e < E; e++) { c->in_cnt[c->pos[in->edge_dst[e]]]++; c->out_cnt[c->pos[in->edge_src[e]]]++; }
+    for (int p = 0; p < K; p++) {
+        c->in_src[p] = malloc(sizeof(int) * (size_t)(c->in_cnt[p] + 1));
+        c->in_cf[p] = malloc(8 * (size_t)(c->in_cnt[p] + 1));
+        c->out_dst[p] = malloc(sizeof(int) * (size_t)(c->out_cnt[p] + 1));
+        c->out_cb[p] = malloc(8 * (size_t)(c->out_cnt[p] + 1));
+        c->in_cnt[p] = 0; c->out_cnt[p] = 0;
+    }
+    /* O3 edge costs, and the R3/range bound: Σ(Δf+Δb) + Σ(c_f+c_b) < 2^61 */
+    u128 bound = 0;
+    int ovf = 0;
+    for (int e = 0; e < E; e++) {
+        int u = c->pos[in->edge_src[e]], v = c->pos[in->edge_dst[e]];
+        uint64_t bf = in->edge_fwd_bytes[e];
+        uint64_t bb = in->edge_bwd_bytes ? in->edge_bwd_bytes[e] : bf;
+        uint64_t cf = or_edge_cost(bf, in->link_bw_Bps, in->link_lat_ps, &ovf);
+        uint64_t cb = or_edge_cost(bb, in->link_bw_Bps, in->link_lat_ps, &ovf);
+        c->in_src[v][c->in_cnt[v]] = u; c->in_cf[v][c->in_cnt[v]] = cf; c->in_cnt[v]++;
+        c->out_dst[u][c->out_cnt[u]] = v; c->out_cb[u][c->out_cnt[u]] = cb; c->out_cnt[u]++;
+        bound += (u128)cf + cb;
+    }
+    u128 t1 = 0;
+    for (int p = 0; p < K; p++) t1 += (u128)c->df[p] + c->db[p];
+    bound += t1;
+    if (ovf || (bound >> 61)) { set_err(err, errlen, "time bound >= 2^61 ps"); or_free(c); return OR_E_RANGE; }
+    c->t1 = (uint64_t)t1;
+    c->grad_bytes = 0;
+    if (in->param_bytes) for (int k = 0; k < K; k++) c->grad_bytes += in->param_bytes[k];
+    *out = c;
+    return OR_OK;
+}
+
+int or_num_ops(const or_ctx *c) { return c->K; }
+void or_get_pi(const or_ctx *c, int32_t *pi_out) { for (int p = 0; p < c->K; p++) pi_out[p] = c->pi[p]; }
+/* O4 / R8: T_1 = Σ_k (Δf(k)+Δb(k)), the all-on-one-device makespan (PAPER.md:501 assumption 1). */
+uint64_t or_t1(const or_ctx *c) { return c->t1; }
+uint64_t or_grad_bytes(const or_ctx *c) { return c->grad_bytes; }
+
+/* O4: the in-order list schedule of placement d (indexed by π position).
+ * Forward in π order, backward in reverse π order (R1, R2):
+ *   PAPER.md:443–453 dependency T(dst) ≥ T(src)+Δ(src)+Δ_e,
+ *   PAPER.md:465–476 one op at a time per device,
+ *   PAPER.md:497–503 back-to-back ops; comm overlaps compute.
+ * start_f / start_b (optional) receive each op's start times.               */
+uint64_t or_schedule_ex(const or_ctx *c, int M, const uint8_t *d,
+                        uint64_t *start_f, uint64_t *start_b) {
+    int K = c->K;
+    uint64_t *fin = calloc((size_t)K, 8), *finb = calloc((size_t)K, 8);
+    uint64_t free_t[256];
+    for (int m = 0; m < M; m++) free_t[m] = 0;
+    for (int p = 0; p < K; p++) {                       /* forward */
+        uint64_t r = 0;
+        for (int i = 0; i < c->in_cnt[p]; i++) {
+            int u = c->in_src[p][i];
+            uint64_t t = fin[u] + (d[u] != d[p] ? c->in_cf[p][i] : 0);
+            if (t > r) r = t;
+        }
+        uint64_t s = r > free_t[d[p]] ? r : free_t[d[p]];
+        if (start_f) start_f[p] = s;
+        fin[p] = s + c->df[p];
+        free_t[d[p]] = fin[p];
+    }
+    for (int p = K - 1; p >= 0; p--) {                  /* backward */
+        uint64_t r = (c->out_cnt[p] == 0) ? fin[p] : 0;  /* a sink waits for its own forward (R1) */
+        for (int i = 0; i < c->out_cnt[p]; i++) {
+            int w = c->out_dst[p][i];
+            uint64_t t = finb[w] + (d[w] != d[p] ? c->out_cb[p][i] : 0);
+            if (t > r) r = t;
+        }
+        uint64_t s = r > free_t[d[p]] ? r : free_t[d[p]];
+        if (start_b) start_b[p] = s;
+        finb[p] = s + c->db[p];
+        free_t[d[p]] = finb[p];
+    }
+    uint64_t mk = 0;
+    for (int m = 0; m < M; m++) if (free_t[m] > mk) mk = free_t[m];
+    free(fin); free(finb);
+    /* PAPER.md:478–487 memory capacity, reading R7: violation => infeasible */
+    if (c->cap > 0) {
+        for (int m = 0; m < M; m++) {
+            u128 used = 0;
+            for (int p = 0; p < K; p++) if (d[p] == m) used += c->mem[p];
+            if (used > c->cap) return OR_INFEASIBLE_MAKESPAN;
+        }
+    }
+    return mk;
+}
+
+uint64_t or_schedule(const or_ctx *c, int M, const uint8_t *d_pi) {
+    return or_schedule_ex(c, M, d_pi, NULL, NULL);
+}
+
+/* placement given in original (descriptor) op order */
+int or_makespan_orig(const or_ctx *c, int M, const uint8_t *d_orig, uint64_t *out) {
+    if (M < 1 || M > 8) return OR_E_INVALID;
+    uint8_t *d = malloc((size_t)c->K);
+    for (int p = 0; p < c->K; p++) {
+        d[p] = d_orig[c->pi[p]];
+        if (d[p] >= M) { free(d); return OR_E_INVALID; }
+    }
+    *out = or_schedule(c, M, d);
+    free(d);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------- O5 / O6 generators */
+#define OR_GEN_GRAY 0
+#define OR_GEN_RANDOM 1
+#define OR_GEN_PERTURB 2
+
+/* SplitMix64 finaliser (SURVEY §8(c) O6 [proposal]; the paper has no generator). */
+uint64_t or_mix(uint64_t z) {
+    z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ULL;
+    z ^= z >> 27; z *= 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return z;
+}
+
+static int ceil_log2(int M) { int b = 0; while ((1 << b) < M) b++; return b; }
+
+static uint64_t word_at(uint64_t seed, uint64_t i, uint64_t Wd, uint64_t t) {
+    return or_mix(seed + 0x9E3779B97F4A7C15ULL * (i * Wd + t + 1));
+}
+
+/* Writes placement d[0..K-1] (π positions) of candidate i.
+ * GRAY   : O5, reflected M-ary Gray code of i.
+ * RANDOM : O6, bits from SplitMix64 words; i = 0 is all zeros.
+ * PERTURB: O6, per-op flip of base with probability τ/256; i = 0 is the base. */
+void or_gen(int K, int M, int gen, uint64_t seed_r, uint32_t tau,
+            const uint8_t *base, uint64_t i, uint8_t *d) {
+    if (M == 1) { for (int j = 0; j < K; j++) d[j] = 0; return; }
+    if (gen == OR_GEN_GRAY) {
+        uint64_t *a = malloc(8 * (size_t)(K + 1));
+        uint64_t x = i;
+        for (int j = 0; j < K; j++) { a[j] = x % (uint64_t)M; x /= (uint64_t)M; }
+        a[K] = 0;
+        for (int j = 0; j < K; j++) {
+            uint64_t par;
+            if (M % 2 == 0) par = a[j + 1];
+            else { par = 0; for (int t = j + 1; t <= K; t++) par += a[t]; }
+            d[j] = (uint8_t)((par % 2 == 0) ? a[j] : (uint64_t)(M - 1) - a[j]);
+        }
+        free(a);
+        return;
+    }
+    int b = ceil_log2(M);
+    if (gen == OR_GEN_RANDOM) {
+        if (i == 0) { for (int j = 0; j < K; j++) d[j] = 0; return; }
+        uint64_t P = (uint64_t)(64 / b);
+        uint64_t Wd = ((uint64_t)K + P - 1) / P;
+        for (int j = 0; j < K; j++) {
+            uint64_t w = word_at(seed_r, i, Wd, (uint64_t)j / P);
+            uint64_t x = (w >> ((uint64_t)b * ((uint64_t)j % P))) & ((1ULL << b) - 1);
+            d[j] = (uint8_t)((x * (uint64_t)M) >> b);
+        }
+        return;
+    }
+    /* PERTURB */
+    if (i == 0) { for (int j = 0; j < K; j++) d[j] = base[j]; return; }
+    uint64_t s2 = seed_r ^ 0xD1B54A32D192ED03ULL;
+    uint64_t fb = 8 + (uint64_t)b;
+    uint64_t P = 64 / fb;
+    uint64_t Wd = ((uint64_t)K + P - 1) / P;
+    for (int j = 0; j < K; j++) {
+        uint64_t w = word_at(s2, i, Wd, (uint64_t)j / P);
+        uint64_t f = (w >> (fb * ((uint64_t)j % P))) & ((1ULL << fb) - 1);
+        uint64_t u = f & 0xFF, y = f >> 8;
+        if (u >= tau) d[j] = base[j];
+        else d[j] = (uint8_t)((base[j] + 1 + (y % (uint64_t)(M - 1))) % (uint64_t)M);
+    }
+}
+
+/* O7 (one round): lexicographic min of (makespan, i) over candidates
+ * i ∈ [begin, end) with seed_r and base (π order).                         */
+typedef struct { uint64_t makespan, index; } or_best;
+
+or_best or_round(const or_ctx *c, int M, int gen, uint64_t seed_r, uint32_t tau,
+                 const uint8_t *base, uint64_t begin, uint64_t end) {
+    or_best best = { UINT64_MAX, UINT64_MAX };
+    uint8_t *d = malloc((size_t)c->K);
+    for (uint64_t i = begin; i < end; i++) {
+        or_gen(c->K, M, gen, seed_r, tau, base, i, d);
+        uint64_t mk = or_schedule(c, M, d);
+        if (mk < best.makespan || (mk == best.makespan && i < best.index)) {
+            best.makespan = mk; best.index = i;
+        }
+    }
+    free(d);
+    return best;
+}
+
+typedef struct {
+    uint64_t best_makespan_ps, best_index, best_round, t1_ps, evaluated;
+} or_result;
+
+/* O7: full search.  PERTURB rounds: seed_r = seed + r; the base moves to the
+ * round winner iff its makespan is strictly below the base's.  The reported
+ * best is the first round that reached the final best makespan (R9 ties to
+ * the smallest candidate index).  placement_orig receives the winner in
+ * descriptor order.  base_orig (descriptor order) may be NULL (all zero).   */
+int or_search(const or_ctx *c, int M, int gen, uint64_t seed, uint64_t count,
+              uint32_t rounds, uint32_t tau, const uint8_t *base_orig,
+              or_result *res, uint8_t *placement_orig) {
+    int K = c->K;
+    if (M < 1 || M > 8 || count < 1 || rounds < 1 || gen < 0 || gen > 2 || tau > 256) return OR_E_INVALID;
+    if (gen != OR_GEN_PERTURB && rounds != 1) return OR_E_INVALID;
+    if (gen == OR_GEN_GRAY) {
+        u128 space = 1;
+        for (int j = 0; j < K && space <= ((u128)1 << 63); j++) space *= (u128)M;
+        if (space > ((u128)1 << 63)) return OR_E_TOO_LARGE;
+        if ((u128)count > space) return OR_E_INVALID;
+    }
+    uint8_t *base = calloc((size_t)K, 1), *d = malloc((size_t)K), *bestd = malloc((size_t)K);
+    if (base_orig) for (int p = 0; p < K; p++) {
+        base[p] = base_orig[c->pi[p]];
+        if (base[p] >= M) { free(base); free(d); free(bestd); return OR_E_INVALID; }
+    }
+    or_best overall = { UINT64_MAX, UINT64_MAX };
+    uint64_t best_round = 0;
+    for (uint32_t r = 0; r < rounds; r++) {
+        uint64_t seed_r = seed + r;
+        or_best w = or_round(c, M, gen, seed_r, tau, base, 0, count);
+        or_gen(K, M, gen, seed_r, tau, base, w.index, d);
+        if (r == 0 || w.makespan < overall.makespan) {
+            overall = w; best_round = r;
+            memcpy(bestd, d, (size_t)K);
+        }
+        /* base of the next round: candidate 0 is the base, so the winner's
+         * makespan is ≤ the base's; move iff strictly smaller              */
+        uint64_t base_mk = or_schedule(c, M, base);
+        if (w.makespan < base_mk) memcpy(base, d, (size_t)K);
+    }
+    res->best_makespan_ps = overall.makespan;
+    res->best_index = overall.index;
+    res->best_round = best_round;
+    res->t1_ps = c->t1;
+    res->evaluated = count * (uint64_t)rounds;
+    if (placement_orig) for (int p = 0; p < K; p++) placement_orig[c->pi[p]] = bestd[p];
+    free(base); free(d); free(bestd);
+    if (overall.makespan == OR_INFEASIBLE_MAKESPAN) return OR_E_INFEASIBLE;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------ O8–O11 projection */
+typedef struct {
+    uint64_t dataset_items;            /* D  (§3) */
+    uint32_t mini_batch;               /* B  (§3.1) */
+    uint32_t n_knots;
+    const uint64_t *knot_G, *knot_uepochs; /* E(G) curve, µ-epochs (Fig. 4) */
+    uint64_t grad_bytes;               /* S for the ring all-reduce */
+    uint64_t bw_intra_Bps, lat_intra_ps, bw_inter_Bps, lat_inter_ps;
+    uint32_t node_size;                /* 0 => 8 */
+    uint32_t ar_mode;                  /* 0 = EQ5 (paper Eq. 5), 1 = TIME */
+    uint64_t t1_ps;                    /* T_1 */
+} or_scenario;
+
+typedef struct { uint64_t C_lo, C_hi, step_ps, steps, uepochs; uint32_t feasible, _pad; } or_cell;
+
+static int bitlen128(u128 x) { int n = 0; while (x) { n++; x >>= 1; } return n; }
+
+/* O8: ring all-reduce of S bytes over n workers (PAPER.md:120 ring all-reduce;
+ * PAPER.md:171 slower inter-node links; reading R10):
+ *   AR(n,S) = 0 if n = 1, else ⌈2(n−1)·S·10^12 / (n·BW)⌉ + 2(n−1)·α,
+ *   tier = intra if the cell's device count ≤ node_size else inter;
+ *   a tier with BW = 0 is "AR off" (SE ≡ 1).                    */
+int or_ar(const or_scenario *s, uint64_t n, uint64_t n_devices, u128 *out) {
+    *out = 0;
+    if (n <= 1) return OR_OK;
+    uint64_t node = s->node_size ? s->node_size : 8;
+    uint64_t bw = (n_devices <= node) ? s->bw_intra_Bps : s->bw_inter_Bps;
+    uint64_t al = (n_devices <= node) ? s->lat_intra_ps : s->lat_inter_ps;
+    if (bw == 0) return OR_OK;
+    u128 num = (u128)2 * (n - 1);
+    if (bitlen128(num) + bitlen128(s->grad_bytes) + 40 > 127) return OR_E_RANGE;
+    num = num * s->grad_bytes * (u128)1000000000000ULL;
+    u128 den = (u128)n * bw;
+    u128 q = num / den + (num % den ? 1 : 0);
+    *out = q + (u128)2 * (n - 1) * al;
+    return OR_OK;
+}
+
+uint64_t or_ar64(const or_scenario *s, uint64_t n, uint64_t n_devices, int *rc) {
+    u128 a; *rc = or_ar(s, n, n_devices, &a);
+    if (*rc == OR_OK && (a >> 64)) *rc = OR_E_RANGE;
+    return (uint64_t)a;
+}
+
+/* O9: E(G) from the knots (Fig. 4 shape; reading R12): exact at knots,
+ * floor of the linear interpolation in G between knots, infeasible outside. */
+int or_epochs(const or_scenario *s, uint64_t G, uint64_t *E) {
+    uint32_t n = s->n_knots;
+    if (n == 0 || G < s->knot_G[0] || G > s->knot_G[n - 1]) return 0;
+    for (uint32_t i = 0; i < n; i++) if (s->knot_G[i] == G) { *E = s->knot_uepochs[i]; return 1; }
+    for (uint32_t i = 0; i + 1 < n; i++) {
+        uint64_t g0 = s->knot_G[i], g1 = s->knot_G[i + 1];
+        if (g0 < G && G < g1) {
+            u128 num = (u128)s->knot_uepochs[i] * (g1 - G) + (u128)s->knot_uepochs[i + 1] * (G - g0);
+            *E = (uint64_t)(num / (g1 - g0));
+            return 1;
+        }
+    }
+    return 0;
+}
+
+static int validate_scenario(const or_scenario *s) {
+    if (s->mini_batch == 0 || s->dataset_items == 0 || s->t1_ps == 0 || s->ar_mode > 1) return OR_E_INVALID;
+    if (s->n_knots == 0 || !s->knot_G || !s->knot_uepochs) return OR_E_INVALID;
+    for (uint32_t i = 0; i < s->n_knots; i++) {
+        if (s->knot_uepochs[i] == 0) return OR_E_INVALID;
+        if (i > 0 && s->knot_G[i] <= s->knot_G[i - 1]) return OR_E_INVALID;
+        if (i > 0) {
+            uint64_t em = s->knot_uepochs[i] > s->knot_uepochs[i - 1] ? s->knot_uepochs[i] : s->knot_uepochs[i - 1];
+            if (bitlen128(em) + bitlen128(s->knot_G[i] - s->knot_G[i - 1]) + 1 > 127) return OR_E_RANGE;
+        }
+    }
+    return OR_OK;
+}
+
+/* O10: one cell (M, N).  Eq. 1 C = T×S×E; S = ⌈D/G⌉
+ * (reading R14); G = W·B with W = N/M workers;
+ * EQ5 (Eq. 5, reading R11): T = ⌊(T_1 + AR(W))·T_M / T_1⌋;
+ * TIME: T = T_M + AR(W).  M ∤ N => infeasible (R15).                          */
+int or_cell_compute(const or_scenario *s, uint32_t M, uint64_t T_M, uint32_t N, or_cell *cell) {
+    memset(cell, 0, sizeof *cell);
+    if (M == 0 || N == 0) return OR_E_INVALID;
+    if (N % M != 0) return OR_OK;
+    uint64_t W = N / M;
+    u128 G = (u128)W * s->mini_batch;
+    uint64_t E;
+    if (G >> 64) return OR_OK;
+    if (!or_epochs(s, (uint64_t)G, &E)) return OR_OK;
+    u128 A;
+    int rc = or_ar(s, W, N, &A);
+    if (rc) return rc;
+    u128 T;
+    if (s->ar_mode == 0) {
+        u128 a = (u128)s->t1_ps + A;
+        if (bitlen128(a) + bitlen128(T_M) > 127) return OR_E_RANGE;
+        T = a * T_M / s->t1_ps;
+    } else {
+        T = (u128)T_M + A;
+    }
+    if (T >> 64) return OR_E_RANGE;
+    uint64_t steps = (uint64_t)((s->dataset_items + (uint64_t)G - 1) / (uint64_t)G);
+    if (bitlen128(T) + bitlen128(steps) + bitlen128(E) > 127) return OR_E_RANGE;
+    u128 C = T * steps * E;
+    cell->C_lo = (uint64_t)C; cell->C_hi = (uint64_t)(C >> 64);
+    cell->step_ps = (uint64_t)T; cell->steps = steps; cell->uepochs = E; cell->feasible = 1;
+    return OR_OK;
+}
+
+/* cells[m*N_max + (N-1)] */
+int or_project(const or_scenario *s, int nM, const uint32_t *Ms, const uint64_t *T_M,
+               uint32_t N_max, or_cell *cells) {
+    int rc = validate_scenario(s);
+    if (rc) return rc;
+    if (nM < 1 || nM > 8 || N_max < 1 || N_max > 65536) return OR_E_INVALID;
+    for (int m = 0; m < nM; m++) if (Ms[m] == 0 || T_M[m] == 0) return OR_E_INVALID;
+    for (int m = 0; m < nM; m++)
+        for (uint32_t N = 1; N <= N_max; N++) {
+            rc = or_cell_compute(s, Ms[m], T_M[m], N, &cells[(size_t)m * N_max + (N - 1)]);
+            if (rc) return rc;
+        }
+    return OR_OK;
+}
+
+typedef struct {
+    uint32_t n_star, m_at_n_star;
+    uint32_t n_star_M[8], persistent_M[8];
+    uint32_t n_star_vs_best_dp;
+} or_crossover_result;
+
+static u128 cellC(const or_cell *c) { return ((u128)c->C_hi << 64) | c->C_lo; }
+
+/* O11: crossover (Eq. 6, strict ">", reading R16; §5
+ * PAPER.md:310–317).  best_m (optional, length N_max) receives the M with the
+ * smallest C at each N (ties → smaller M), 0 if none.        */
+int or_crossover(const or_cell *cells, int nM, const uint32_t *Ms, uint32_t N_max,
+                 or_crossover_result *res, uint32_t *best_m) {
+    memset(res, 0, sizeof *res);
+    int m1 = -1;
+    for (int m = 0; m < nM; m++) if (Ms[m] == 1) m1 = m;
+    if (m1 < 0 || nM < 1 || nM > 8 || N_max < 1) return OR_E_INVALID;
+    const or_cell *dp = cells + (size_t)m1 * N_max;
+    for (int m = 0; m < nM; m++) {
+        if (Ms[m] == 1) continue;
+        const or_cell *hy = cells + (size_t)m * N_max;
+        uint32_t ns = 0;
+        for (uint32_t N = 1; N <= N_max && !ns; N++) {
+            const or_cell *a = &hy[N - 1], *b = &dp[N - 1];
+            if (a->feasible && b->feasible && cellC(a) < cellC(b)) ns = N;
+        }
+        res->n_star_M[m] = ns;
+        if (ns) {
+            uint32_t pers = 1;
+            for (uint32_t N = ns; N <= N_max; N++) {
+                const or_cell *a = &hy[N - 1], *b = &dp[N - 1];
+                if (a->feasible && b->feasible && !(cellC(a) < cellC(b))) pers = 0;
+            }
+            res->persistent_M[m] = pers;
+            if (res->n_star == 0 || ns < res->n_star) res->n_star = ns;
+        }
+    }
+    if (res->n_star) {
+        uint32_t N = res->n_star;
+        int bm = -1;
+        for (int m = 0; m < nM; m++) {
+            const or_cell *a = &cells[(size_t)m * N_max + (N - 1)];
+            if (!a->feasible) continue;
+            if (bm < 0 || cellC(a) < cellC(&cells[(size_t)bm * N_max + (N - 1)]) ||
+                (cellC(a) == cellC(&cells[(size_t)bm * N_max + (N - 1)]) && Ms[m] < Ms[bm])) bm = m;
+        }
+        res->m_at_n_star = Ms[bm];
+    }
+    /* n_star_vs_best_dp: min N with min_M C(M,N) < min_{N'≤N} C(1,N')
+     * ("speedup over the best performing scale of DP-only");
+     * N with no feasible DP cell at or below it are skipped.                 */
+    int have_dp = 0; u128 best_dp = 0;
+    for (uint32_t N = 1; N <= N_max; N++) {
+        if (dp[N - 1].feasible && (!have_dp || cellC(&dp[N - 1]) < best_dp)) { best_dp = cellC(&dp[N - 1]); have_dp = 1; }
+        int bm = -1;
+        for (int m = 0; m < nM; m++) {
+            const or_cell *a = &cells[(size_t)m * N_max + (N - 1)];
+            if (!a->feasible) continue;
+            if (bm < 0 || cellC(a) < cellC(&cells[(size_t)bm * N_max + (N - 1)]) ||
+                (cellC(a) == cellC(&cells[(size_t)bm * N_max + (N - 1)]) && Ms[m] < Ms[bm])) bm = m;
+        }
+        if (best_m) best_m[N - 1] = bm < 0 ? 0 : Ms[bm];
+        if (!res->n_star_vs_best_dp && have_dp && bm >= 0 &&
+            cellC(&cells[(size_t)bm * N_max + (N - 1)]) < best_dp) res->n_star_vs_best_dp = N;
+    }
+    return OR_OK;
+}

@@ -1,0 +1,134 @@
+"""Independent brute-force checker for the oracle (pin K16).
+
+It shares nothing with oracle/pp_oracle.c: a different formulation of the same
+quantity.  The step makespan of a placement is the LONGEST PATH of an
+augmented DAG over 2K nodes (forward node F_k, backward node B_k):
+
+  * node weight = Δf(k) for F_k, Δb(k) for B_k;
+  * data edge F_u → F_v for every DFG edge (u, v) with weight c_f(e) if u and v
+    sit on different devices (the dependency constraint with
+    Δ_e), and the reversed gradient edge B_v → B_u with c_b(e) (reading R1);
+  * F_k → B_k for every op (a backward op never precedes its own forward);
+  * device-order edges between consecutive ops of one device in the issue
+    sequence F_π0..F_πK−1, B_πK−1..B_π0 (reading R2: in-order per-device issue,
+    PAPER.md:465–476 non-overlap, PAPER.md:501 back-to-back).
+
+The longest path is evaluated by memoised recursion over predecessors, not by
+walking the issue sequence.  Exhaustive search enumerates placements with
+itertools.product; Gray order is the textbook recursive reflected M-ary Gray
+list (not the digit rule of O5).
+"""
+from __future__ import annotations
+
+import functools
+import heapq
+import itertools
+import sys
+
+
+def kahn_by_id(K, ids, src, dst):
+    indeg = [0] * K
+    succ = [[] for _ in range(K)]
+    for u, v in zip(src, dst):
+        indeg[v] += 1
+        succ[u].append(v)
+    heap = [(ids[k], k) for k in range(K) if indeg[k] == 0]
+    heapq.heapify(heap)
+    order = []
+    while heap:
+        _, k = heapq.heappop(heap)
+        order.append(k)
+        for v in succ[k]:
+            indeg[v] -= 1
+            if indeg[v] == 0:
+                heapq.heappush(heap, (ids[v], v))
+    if len(order) != K:
+        raise ValueError("cycle")
+    return order
+
+
+def _cost(nbytes, bw, lat):
+    return -(-nbytes * 10**12 // bw) + lat
+
+
+def longest_path_makespan(spec, M, placement):
+    K = len(spec["fwd_ps"])
+    ids = spec.get("op_id") or list(range(K))
+    src, dst = spec["edge_src"], spec["edge_dst"]
+    bf = spec["edge_fwd_bytes"]
+    bb = spec.get("edge_bwd_bytes") or bf
+    bw, lat = spec["link_bw_Bps"], spec["link_lat_ps"]
+    order = kahn_by_id(K, ids, src, dst)
+    seq = [("F", k) for k in order] + [("B", k) for k in reversed(order)]
+    preds = {n: [] for n in seq}
+    for e, (u, v) in enumerate(zip(src, dst)):
+        cut = placement[u] != placement[v]
+        preds[("F", v)].append((("F", u), _cost(bf[e], bw, lat) if cut else 0))
+        preds[("B", u)].append((("B", v), _cost(bb[e], bw, lat) if cut else 0))
+    for k in range(K):
+        preds[("B", k)].append((("F", k), 0))
+    last = {}
+    for n in seq:
+        dev = placement[n[1]]
+        if dev in last:
+            preds[n].append((last[dev], 0))
+        last[dev] = n
+    w = {("F", k): spec["fwd_ps"][k] for k in range(K)}
+    w.update({("B", k): spec["bwd_ps"][k] for k in range(K)})
+    sys.setrecursionlimit(max(10000, 8 * K + 100))
+
+    @functools.lru_cache(maxsize=None)
+    def finish(n):
+        s = 0
+        for p, c in preds[n]:
+            s = max(s, finish(p) + c)
+        return s + w[n]
+
+    mk = max(finish(n) for n in seq)
+    cap = spec.get("dev_mem_cap_bytes") or 0
+    if cap:
+        mem = spec.get("mem_bytes") or [0] * K
+        for m in range(M):
+            if sum(mem[k] for k in range(K) if placement[k] == m) > cap:
+                return (1 << 64) - 1
+    return mk
+
+
+def reflected_gray(M, K):
+    """Textbook recursive reflected M-ary Gray list; tuple index j = digit j
+    (digit 0 changes fastest)."""
+    L = [(a,) for a in range(M)]
+    for _ in range(1, K):
+        nxt = []
+        for a in range(M):
+            block = L if a % 2 == 0 else list(reversed(L))
+            nxt.extend(t + (a,) for t in block)
+        L = nxt
+    return L
+
+
+def exhaustive(spec, M):
+    """(best makespan, number of optimal placements, all optima) by brute force."""
+    K = len(spec["fwd_ps"])
+    best, opt = None, []
+    for pl in itertools.product(range(M), repeat=K):
+        mk = longest_path_makespan(spec, M, pl)
+        if best is None or mk < best:
+            best, opt = mk, [pl]
+        elif mk == best:
+            opt.append(pl)
+    return best, opt
+
+
+def gray_first_index(spec, M, best):
+    """Index, in Gray order over π positions, of the first optimal placement."""
+    K = len(spec["fwd_ps"])
+    ids = spec.get("op_id") or list(range(K))
+    order = kahn_by_id(K, ids, spec["edge_src"], spec["edge_dst"])
+    for i, g in enumerate(reflected_gray(M, K)):
+        pl = [0] * K
+        for j, k in enumerate(order):
+            pl[k] = g[j]
+        if longest_path_makespan(spec, M, pl) == best:
+            return i, pl
+    return None, None

@@ -1,0 +1,78 @@
+"""Pins of the oracle's candidate generators (O5 Gray, O6 RANDOM/PERTURB)."""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle as O
+from tests import brute
+
+
+def test_splitmix64_published_vector():
+    # SplitMix64 (Steele, Lea, Flood 2014; Vigna's reference splitmix64.c) with
+    # state 1234567: first outputs 6457827717110365317, 3203168211198807973,
+    # 9817491932198370423.  next() = mix(state += 0x9E3779B97F4A7C15).
+    g = 0x9E3779B97F4A7C15
+    want = [6457827717110365317, 3203168211198807973, 9817491932198370423]
+    assert [O.mix((1234567 + g * k) % 2**64) for k in (1, 2, 3)] == want
+
+
+@pytest.mark.parametrize("M,K", [(2, 1), (2, 5), (2, 9), (3, 4), (3, 5), (4, 4), (5, 3), (6, 3), (8, 3)])
+def test_gray_equals_textbook_reflected_code(M, K):
+    ref = brute.reflected_gray(M, K)
+    got = [tuple(int(x) for x in O.gen(K, M, O.GEN_GRAY, 0, 0, None, i)) for i in range(M**K)]
+    assert got == ref
+    assert len(set(got)) == M**K                                   # bijection onto [0,M)^K
+    for a, b in zip(got, got[1:]):                                 # one digit, by ±1
+        diff = [abs(x - y) for x, y in zip(a, b) if x != y]
+        assert diff == [1]
+
+
+def test_gray_binary_is_i_xor_i_shift():
+    K = 12
+    for i in range(4096):
+        g = i ^ (i >> 1)
+        assert [int(x) for x in O.gen(K, 2, O.GEN_GRAY, 0, 0, None, i)] == [(g >> j) & 1 for j in range(K)]
+
+
+@pytest.mark.parametrize("M", [2, 3, 4, 5, 8])
+def test_random_index0_and_distribution(M):
+    K = 200
+    assert not O.gen(K, M, O.GEN_RANDOM, 99, 0, None, 0).any()
+    counts = np.zeros(M)
+    rows = []
+    for i in range(1, 400):
+        d = O.gen(K, M, O.GEN_RANDOM, 99, 0, None, i)
+        assert d.max() < M
+        counts += np.bincount(d, minlength=M)
+        rows.append(d.copy())
+    freq = counts / counts.sum()
+    if M & (M - 1) == 0:          # (x·M) >> b is uniform for M a power of two
+        assert np.allclose(freq, 1 / M, atol=0.01)
+    else:
+        assert (freq > 0).all()
+    assert len({r.tobytes() for r in rows}) == len(rows)           # no repeats at K = 200
+    # seed changes the stream
+    assert not np.array_equal(O.gen(K, M, O.GEN_RANDOM, 98, 0, None, 5),
+                              O.gen(K, M, O.GEN_RANDOM, 99, 0, None, 5))
+
+
+@pytest.mark.parametrize("M", [2, 3, 4, 8])
+def test_perturb_rules(M):
+    K = 150
+    rng = np.random.default_rng(M)
+    base = rng.integers(0, M, K).astype(np.uint8)
+    assert np.array_equal(O.gen(K, M, O.GEN_PERTURB, 7, 255, base, 0), base)      # i = 0 is the base
+    for i in range(1, 30):
+        assert np.array_equal(O.gen(K, M, O.GEN_PERTURB, 7, 0, base, i), base)    # τ = 0: no flips
+        d = O.gen(K, M, O.GEN_PERTURB, 7, 256, base, i)                           # τ = 256: all flip
+        assert (d != base).all() and d.max() < M
+        if M == 2:
+            assert np.array_equal(d, 1 - base)
+    flips = sum(int((O.gen(K, M, O.GEN_PERTURB, 11, 32, base, i) != base).sum()) for i in range(1, 300))
+    assert abs(flips / (299 * K) - 32 / 256) < 0.01                               # rate τ/256
+
+
+def test_m1_is_all_zero():
+    for g in (O.GEN_GRAY, O.GEN_RANDOM, O.GEN_PERTURB):
+        assert not O.gen(20, 1, g, 5, 128, None, 3).any()
