@@ -1,0 +1,319 @@
+"""Benchmark of the hot path (BASELINE.json metric: placements evaluated/sec).
+
+One step = one pass of the whole path over one batch:
+on-device generation + forward/backward list schedule + argmin of
+`--count` candidate placements of the Inception-V3-shaped DFG on M devices
+(sharded over the ranks, NCCL min all-reduce of the packed key), the round
+update, then the end-to-end projection over N = 1..N_max and the crossover.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl pp|reference]
+
+N > 1 runs under torchrun (one rank per GPU, NCCL).  Rank 0 prints one JSON
+line.  `--impl reference` times the CPU oracle (the reference arm of this
+tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "placements evaluated/sec at 1/2/4/8 B200; crossover N bit-exact vs CPU oracle"
+UNIT = "placements/s"
+SEED = 13257
+
+
+def workload(args):
+    spec = synth.inception_v3()
+    return spec
+
+
+def alg_counts(spec):
+    """Algorithmic work per placement:
+    6 int32 ops per scheduled op (64-bit max with free + 64-bit add), 7 per
+    edge visit (device compare, conditional 64-bit add, 64-bit max); shared
+    memory: 8 B read per edge visit + 8 B written per scheduled op."""
+    K, E = len(spec["fwd_ps"]), len(spec["edge_src"])
+    ops = 6 * (2 * K) + 7 * (2 * E)
+    smem = 8 * (2 * E) + 8 * (2 * K)
+    return ops, smem
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device_index):
+        self.idx = device_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks(sm_count, clock_mhz):
+    """Roofline denominators for this ALU/shared-memory-bound path (DESIGN.md
+    §Roofline): INT32 issue = 4 SMSPs × 32 lanes = 128 thread-ops/clk/SM;
+    shared memory = 128 B/clk/SM; at the max SM clock from MEASURED_PEAKS.json."""
+    return {"int32_ops_per_s": sm_count * 128 * clock_mhz * 1e6,
+            "smem_bytes_per_s": sm_count * 128 * clock_mhz * 1e6}
+
+
+def measured_clock():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"]), "measured"
+    except Exception:
+        return 1965.0, "fallback (B200_PROFILING.md clocks.max.sm)"
+
+
+# ------------------------------------------------------------ oracle arm
+def cpu_oracle_sample(spec, M, n_target_s=12.0, count=None):
+    """The CPU oracle (oracle/) as it stands, single thread, on a bounded
+    prefix of the same candidate stream; returns (placements/s, n, seconds)."""
+    import oracle as O
+    od = O.Dfg.from_spec(spec)
+    if count is None:
+        t = time.perf_counter()
+        od.round(M, O.GEN_RANDOM, SEED, 0, None, 0, 20_000)
+        rate = 20_000 / (time.perf_counter() - t)
+        count = max(20_000, int(rate * n_target_s))
+    t = time.perf_counter()
+    r = od.search(M, O.GEN_RANDOM, SEED, count)
+    dt = time.perf_counter() - t
+    return count / dt, count, dt, od, r
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle as O
+    spec = workload(args)
+    ops, _ = alg_counts(spec)
+    n_step = args.ref_sample
+    times = []
+    for s in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        od = O.Dfg.from_spec(spec)
+        r = od.search(args.M, O.GEN_RANDOM, SEED, n_step)
+        sc = synth.sweep_scenario("inception_v3", od.t1, od.grad_bytes)
+        cells = O.Scenario.from_spec(sc).project([1, args.M], [od.t1, r.best_makespan_ps], args.nmax)
+        x = O.crossover(cells, [1, args.M], args.nmax)
+        dt = time.perf_counter() - t
+        if s >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = n_step * len(times) / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic", "gpu_launches": 0,
+            "config": config_dict(args, spec, per_step=n_step),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{n_step} RANDOM candidates of the Inception-V3-shaped DFG per step "
+                                       f"(prefix of the GPU step's {args.count}) + projection N=1..{args.nmax} + crossover"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "crossover_n_star": x.n_star}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args, spec, per_step=None):
+    return {"workload": f"inception_v3_shaped_M{args.M}_random_{args.count:.0e}".replace("+0", ""),
+            "dfg": "Inception-V3-shaped (synth.inception_v3, batch 64)", "K": len(spec["fwd_ps"]),
+            "E": len(spec["edge_src"]), "M": args.M, "generator": "RANDOM (SplitMix64)", "seed": SEED,
+            "candidates_per_step": per_step or args.count, "projection": f"M in {{1,{args.M}}}, N=1..{args.nmax}",
+            "l2": "flushed between timed steps (256 MiB write); inputs live on-chip"}
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_pp(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1907_13257_b200 as pp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = pp.Comm(rank, world, local)
+    stream = torch.cuda.current_stream()
+    spec = workload(args)
+    g = pp.Dfg(spec, device=local)
+    M = args.M
+    sc = synth.sweep_scenario("inception_v3", g.t1, g.grad_bytes)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        r = g.search_best(M, pp.GEN_RANDOM, SEED, args.count, comm=comm, stream=stream)
+        cells = pp.project_e2e(sc, [1, M], [g.t1, r.best_makespan_ps], args.nmax, device=local, stream=stream)
+        x = pp.crossover(cells, [1, M], args.nmax, best_m=False, stream=stream)
+        return r, x
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    # ---- device-timed steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = pp.kernel_launch_count()
+    pp.set_kernel_timing(True)
+    results = []
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.fill_(s & 0xFF)          # L2 flush outside the timed window
+            barrier()
+            ev[s][0].record(stream)
+            results.append(step())
+            ev[s][1].record(stream)
+            torch.cuda.synchronize()
+    launches = pp.kernel_launch_count() - launches0
+    kern_ms, kern_n = pp.get_kernel_timing()
+    pp.set_kernel_timing(False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = torch.tensor([sum(step_ms), kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot_ms, op=dist.ReduceOp.MAX)
+    tot_ms, kern_ms_max = float(tot_ms[0]), float(tot_ms[1])
+    value = args.count * args.steps / (tot_ms / 1e3)
+
+    # ---- e2e through the C ABI with host buffers (load + search + projection + results)
+    barrier()
+    e2e_ms = []
+    h2d = d2h = 0
+    for s in range(max(1, args.steps)):
+        flush.fill_(s & 0xFF)
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        g2 = pp.Dfg(spec, device=local)                        # H2D of the DFG image
+        r2 = g2.search_best(M, pp.GEN_RANDOM, SEED, args.count, comm=comm, stream=stream)
+        cells2 = pp.project_e2e(sc, [1, M], [g2.t1, r2.best_makespan_ps], args.nmax, device=local, stream=stream)
+        x2 = pp.crossover(cells2, [1, M], args.nmax, best_m=False, stream=stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(t0.elapsed_time(t1))
+        h2d = g2.image_bytes + ((g2.K + 15) // 16) * 16           # image + base upload
+        d2h = 24 + ((g2.K + 15) // 16) * 16 + 4 + 76             # result, placement, range flag, crossover
+        g2.close()
+    e2 = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2, op=dist.ReduceOp.MAX)
+    e2e_value = args.count * len(e2e_ms) / (float(e2[0]) / 1e3)
+
+    if rank == 0:
+        ops, smem_b = alg_counts(spec)
+        clock, clock_src = measured_clock()
+        pk = peaks(torch.cuda.get_device_properties(dev).multi_processor_count, clock)
+        per_launch = args.count // world if world else args.count
+        kern_avg_s = (kern_ms_max / max(1, kern_n)) / 1e3
+        achieved_ops = ops * per_launch / kern_avg_s
+        achieved_smem = smem_b * per_launch / kern_avg_s
+        r, x = results[-1]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": config_dict(args, spec),
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "alu", "achieved": achieved_ops / 1e12, "peak": pk["int32_ops_per_s"] / 1e12,
+                         "unit": "Tops/s (int32)", "frac": achieved_ops / pk["int32_ops_per_s"],
+                         "traffic": None, "kernel": "pp::search_kernel<M,RANDOM>",
+                         "kernel_ms_avg": kern_avg_s * 1e3, "kernel_share_of_step": kern_ms_max / tot_ms,
+                         "alg_ops_per_placement": ops, "alg_smem_bytes_per_placement": smem_b,
+                         "smem_frac": achieved_smem / pk["smem_bytes_per_s"],
+                         "peak_note": f"148 SMs x 128 int32 lanes/clk x {clock:.0f} MHz ({clock_src} max SM clock)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "clocks": clk.summary(),
+            "result": {"T1_ps": g.t1, "TM_ps": r.best_makespan_ps, "best_index": r.best_index,
+                       "su_mp": g.t1 / r.best_makespan_ps, "crossover_n_star": x.n_star,
+                       "n_star_vs_best_dp": x.n_star_vs_best_dp},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            rate, n, dt, od, orr = cpu_oracle_sample(spec, M)
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                    "sample": f"first {n} RANDOM candidates of the same stream, {dt:.1f} s, "
+                                              f"single thread (nproc={os.cpu_count()})"}
+        print(json.dumps(line), flush=True)
+    g.close()
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="pp", choices=["pp", "reference"])
+    ap.add_argument("--M", type=int, default=2)
+    ap.add_argument("--count", type=int, default=100_000_000)
+    ap.add_argument("--nmax", type=int, default=1024)
+    ap.add_argument("--ref-sample", type=int, default=200_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_pp(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,480 @@
+// capi.cpp — the extern "C" entry points of libpp.so (include/pp.h): argument
+// validation, launch configuration, the per-round search driver with the
+// NCCL exchange, and the projection/crossover launches.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "internal.h"
+
+namespace pp {
+
+static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+static bool g_timing = false;
+static double g_timing_ms = 0.0;
+static uint64_t g_timing_n = 0;
+
+void set_error(const std::string &msg) { g_err = msg; }
+void note_launch() { g_launches++; }
+
+int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp_dfg **out);
+
+#define PP_DECL_M(m)                                        \
+    KernelInfo kernel_for_m##m(int gen, bool mem, bool wa); \
+    UpdateFn update_for_m##m(int gen);
+PP_DECL_M(1) PP_DECL_M(2) PP_DECL_M(3) PP_DECL_M(4) PP_DECL_M(5) PP_DECL_M(6) PP_DECL_M(7) PP_DECL_M(8)
+
+KernelInfo kernel_for(int M, int gen, bool mem, bool wa) {
+    switch (M) {
+        case 1: return kernel_for_m1(gen, mem, wa);
+        case 2: return kernel_for_m2(gen, mem, wa);
+        case 3: return kernel_for_m3(gen, mem, wa);
+        case 4: return kernel_for_m4(gen, mem, wa);
+        case 5: return kernel_for_m5(gen, mem, wa);
+        case 6: return kernel_for_m6(gen, mem, wa);
+        case 7: return kernel_for_m7(gen, mem, wa);
+        default: return kernel_for_m8(gen, mem, wa);
+    }
+}
+UpdateFn update_for(int M, int gen) {
+    switch (M) {
+        case 1: return update_for_m1(gen);
+        case 2: return update_for_m2(gen);
+        case 3: return update_for_m3(gen);
+        case 4: return update_for_m4(gen);
+        case 5: return update_for_m5(gen);
+        case 6: return update_for_m6(gen);
+        case 7: return update_for_m7(gen);
+        default: return update_for_m8(gen);
+    }
+}
+
+struct ProjParams;
+struct CrossParams;
+int launch_pack_key(uint64_t *s, int rank, void *stream);
+int launch_contrib(uint64_t *s, int rank, void *stream);
+
+static int cuda_err(cudaError_t e, const char *what) {
+    set_error(std::string("CUDA: ") + what + ": " + cudaGetErrorString(e));
+    return PP_E_CUDA;
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        err = cudaSetDevice(dev);
+        ok = err == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// ------------------------------------------------------------ launch setup
+struct Launch {
+    KernelInfo k;
+    int threads = 0, grid = 0, smem = 0;
+    KParams p{};
+};
+
+// Chooses the CTA size (largest of 256/128/64/32 whose per-lane state fits),
+// the dynamic shared memory layout and a grid of (resident CTAs per SM) × SMs.
+static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin, uint64_t end, Launch &L) {
+    const bool mem = g->cap > 0;
+    L.k = kernel_for(M, gen, mem, write_all);
+    const uint32_t nslot = (uint32_t)g->W + 1;
+    int threads = 256;
+    size_t smem = 0;
+    uint32_t slots_off = 0, free_off = 0, base_off = 0;
+    for (; threads >= 32; threads >>= 1) {
+        size_t off = (g->image_bytes + 127) & ~size_t(127);
+        slots_off = (uint32_t)off;
+        off += (size_t)nslot * threads * 8;
+        free_off = (uint32_t)off;
+        if (M > 2) off += (size_t)M * threads * 8;
+        off = (off + 15) & ~size_t(15);
+        base_off = (uint32_t)off;
+        if (gen == GEN_PERTURB) off += g->base_bytes;
+        smem = off;
+        if (smem <= (size_t)kMaxSmemBytes) break;
+    }
+    if (threads < 32) {
+        set_error("per-lane schedule state does not fit in shared memory");
+        return PP_E_TOO_LARGE;
+    }
+    cudaError_t e = cudaFuncSetAttribute(L.k.func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.k.func, threads, smem);
+    if (e != cudaSuccess) return cuda_err(e, "occupancy");
+    if (occ < 1) occ = 1;
+    const uint64_t n = end - begin;
+    const uint64_t tiles = (n + 31) / 32;
+    const uint64_t wpb = threads / 32;
+    uint64_t want = (tiles + wpb - 1) / wpb;
+    uint64_t grid = std::min<uint64_t>((uint64_t)occ * g->sm_count, want);
+    grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, kMaxGrid));
+    L.threads = threads;
+    L.grid = (int)grid;
+    L.smem = (int)smem;
+    KParams &p = L.p;
+    p.g_image = g->d_image;
+    p.g_base = g->d_base;
+    p.begin = begin;
+    p.end = end;
+    p.cap = g->cap;
+    p.image_bytes = g->image_bytes;
+    p.base_bytes = g->base_bytes;
+    p.K = (uint32_t)g->K;
+    p.nslot = nslot;
+    p.off_edges = g->off_edges;
+    p.off_mem = g->off_mem;
+    p.off_orig = g->off_orig;
+    p.smem_slots_off = slots_off;
+    p.smem_free_off = free_off;
+    p.smem_base_off = base_off;
+    p.g_partials = g->d_partials;
+    p.g_ticket = g->d_ticket;
+    p.g_out = g->d_scalars + SC_LOCAL_MK;
+    return PP_OK;
+}
+
+static int run(Launch &L, void *stream) {
+    int e = L.k.launch(L.p, L.grid, L.threads, L.smem, stream);
+    g_launches++;
+    if (e != 0) return cuda_err((cudaError_t)e, "kernel launch");
+    return PP_OK;
+}
+
+static int check_gen_args(const pp_dfg *g, int M, int gen, uint32_t tau, uint64_t end) {
+    if (!g) { set_error("dfg is NULL"); return PP_E_INVALID; }
+    if (M < 1 || M > 8) { set_error("M must be in [1,8]"); return PP_E_INVALID; }
+    if (gen < 0 || gen > 2) { set_error("unknown generator"); return PP_E_INVALID; }
+    if (tau > 256) { set_error("flip_thresh must be in [0,256]"); return PP_E_INVALID; }
+    if (gen == GEN_GRAY) {
+        unsigned __int128 space = 1;
+        for (int j = 0; j < g->K && space <= ((unsigned __int128)1 << 63); j++) space *= (unsigned)M;
+        if (space > ((unsigned __int128)1 << 63)) { set_error("GRAY space M^K exceeds 2^63"); return PP_E_TOO_LARGE; }
+        if ((unsigned __int128)end > space) { set_error("GRAY range exceeds M^K"); return PP_E_INVALID; }
+    }
+    return PP_OK;
+}
+
+// ------------------------------------------------------------------ NCCL
+struct Nccl {
+    void *h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static Nccl *nccl() {
+    static Nccl n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+        n.CommInitRank = (decltype(n.CommInitRank))dlsym(h, "ncclCommInitRank");
+        n.AllReduce = (decltype(n.AllReduce))dlsym(h, "ncclAllReduce");
+        n.CommDestroy = (decltype(n.CommDestroy))dlsym(h, "ncclCommDestroy");
+        n.GetErrorString = (decltype(n.GetErrorString))dlsym(h, "ncclGetErrorString");
+        if (n.GetUniqueId && n.CommInitRank && n.AllReduce && n.CommDestroy && n.GetErrorString) n.h = h;
+    });
+    return n.h ? &n : nullptr;
+}
+
+static int nccl_err(ncclResult_t r, const char *what) {
+    Nccl *n = nccl();
+    set_error(std::string("NCCL: ") + what + ": " + (n ? n->GetErrorString(r) : "unavailable"));
+    return PP_E_NCCL;
+}
+
+}  // namespace pp
+
+struct pp_comm {
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1, device = 0;
+};
+
+using namespace pp;
+
+extern "C" {
+
+const char *pp_last_error(void) { return g_err.c_str(); }
+uint64_t pp_kernel_launch_count(void) { return g_launches.load(); }
+
+void pp_set_kernel_timing(int enable) {
+    g_timing = enable != 0;
+    g_timing_ms = 0.0;
+    g_timing_n = 0;
+}
+
+void pp_get_kernel_timing(double *total_ms, uint64_t *n) {
+    if (total_ms) *total_ms = g_timing_ms;
+    if (n) *n = g_timing_n;
+}
+
+int pp_load_dfg(const pp_dfg_desc *desc, const pp_link_desc *link, int cuda_device, pp_dfg **out) {
+    g_err.clear();
+    return load_dfg(desc, link, cuda_device, out);
+}
+
+int pp_dfg_get_info(const pp_dfg *g, pp_dfg_info *out) {
+    if (!g || !out) { set_error("NULL argument"); return PP_E_INVALID; }
+    out->num_ops = g->K;
+    out->num_edges = g->E;
+    out->num_slots = g->W;
+    out->image_bytes = (int32_t)g->image_bytes;
+    out->t1_ps = g->t1;
+    out->grad_bytes = g->grad_bytes;
+    return PP_OK;
+}
+
+int pp_dfg_get_pi(const pp_dfg *g, int32_t *pi_out) {
+    if (!g || !pi_out) { set_error("NULL argument"); return PP_E_INVALID; }
+    memcpy(pi_out, g->pi.data(), sizeof(int32_t) * g->K);
+    return PP_OK;
+}
+
+int pp_eval_placements(const pp_dfg *g, int M, const uint8_t *d_placements, uint64_t count,
+                       uint64_t *d_makespan, void *stream) {
+    if (!g || M < 1 || M > 8 || (count && (!d_placements || !d_makespan))) {
+        set_error("invalid arguments");
+        return PP_E_INVALID;
+    }
+    if (count == 0) return PP_OK;
+    DeviceGuard dg(g->device);
+    if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
+    Launch L;
+    int rc = setup(g, M, GEN_EXPLICIT, true, 0, count, L);
+    if (rc) return rc;
+    L.p.g_place = d_placements;
+    L.p.g_makespan = d_makespan;
+    return run(L, stream);
+}
+
+int pp_eval_generated(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t tau, const uint8_t *d_base_pi,
+                      uint64_t begin, uint64_t count, uint64_t *d_makespan, void *stream) {
+    int rc = check_gen_args(g, M, gen, tau, begin + count);
+    if (rc) return rc;
+    if (count == 0) return PP_OK;
+    if (!d_makespan || (gen == GEN_PERTURB && !d_base_pi)) { set_error("NULL device buffer"); return PP_E_INVALID; }
+    DeviceGuard dg(g->device);
+    if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
+    if (gen == GEN_PERTURB) {
+        cudaError_t e = cudaMemcpyAsync(g->d_base, d_base_pi, g->K, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+        if (e != cudaSuccess) return cuda_err(e, "base copy");
+    }
+    Launch L;
+    rc = setup(g, M, gen, true, begin, begin + count, L);
+    if (rc) return rc;
+    L.p.seed = seed_r;
+    L.p.tau = tau;
+    L.p.g_makespan = d_makespan;
+    return run(L, stream);
+}
+
+int pp_search_range(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t tau, const uint8_t *d_base_pi,
+                    uint64_t begin, uint64_t end, uint64_t *d_best, void *stream) {
+    int rc = check_gen_args(g, M, gen, tau, end);
+    if (rc) return rc;
+    if (end <= begin || !d_best || (gen == GEN_PERTURB && !d_base_pi)) {
+        set_error("invalid range or NULL buffer");
+        return PP_E_INVALID;
+    }
+    DeviceGuard dg(g->device);
+    if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
+    if (gen == GEN_PERTURB) {
+        cudaError_t e = cudaMemcpyAsync(g->d_base, d_base_pi, g->K, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+        if (e != cudaSuccess) return cuda_err(e, "base copy");
+    }
+    Launch L;
+    rc = setup(g, M, gen, false, begin, end, L);
+    if (rc) return rc;
+    L.p.seed = seed_r;
+    L.p.tau = tau;
+    L.p.g_out = d_best;
+    return run(L, stream);
+}
+
+void pp_rank_slice(uint64_t count, int rank, int world, uint64_t *begin, uint64_t *end) {
+    unsigned __int128 c = count;
+    *begin = (uint64_t)(c * (unsigned)rank / (unsigned)world);
+    *end = (uint64_t)(c * (unsigned)(rank + 1) / (unsigned)world);
+}
+
+uint64_t pp_pack_key(uint64_t makespan, int rank) {
+    const uint64_t cap = (1ull << 61) - 1;
+    return ((makespan < cap ? makespan : cap) << 3) | (uint64_t)(rank & 7);
+}
+uint64_t pp_key_makespan(uint64_t key) {
+    uint64_t m = key >> 3;
+    return m == ((1ull << 61) - 1) ? PP_INFEASIBLE_MAKESPAN : m;
+}
+int pp_key_rank(uint64_t key) { return (int)(key & 7); }
+
+int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *comm, void *stream,
+                   pp_search_result *out) {
+    g_err.clear();
+    if (!desc || !out) { set_error("NULL argument"); return PP_E_INVALID; }
+    int rc = check_gen_args(g, M, desc->gen, desc->flip_thresh, desc->count);
+    if (rc) return rc;
+    if (desc->count < 1 || desc->rounds < 1 || (desc->gen != GEN_PERTURB && desc->rounds != 1)) {
+        set_error("count must be >= 1; rounds must be >= 1 and > 1 only for PERTURB");
+        return PP_E_INVALID;
+    }
+    const int rank = comm ? comm->rank : 0, world = comm ? comm->world : 1;
+    if (world < 1 || world > 8) { set_error("1 to 8 ranks"); return PP_E_INVALID; }
+    Nccl *nc = comm ? nccl() : nullptr;
+    if (comm && !nc) { set_error("NCCL not loadable"); return PP_E_NCCL; }
+    DeviceGuard dg(g->device);
+    if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int K = g->K;
+    // base (π order)
+    std::vector<uint8_t> base(g->base_bytes, 0);
+    if (desc->base)
+        for (int p = 0; p < K; p++) {
+            base[p] = desc->base[g->pi[p]];
+            if (base[p] >= M) { set_error("base device out of range"); return PP_E_INVALID; }
+        }
+    cudaError_t e = cudaMemcpyAsync(g->d_base, base.data(), g->base_bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_err(e, "base upload");
+    uint64_t begin = 0, end = 0;
+    pp_rank_slice(desc->count, rank, world, &begin, &end);
+    UpdateFn upd = update_for(M, desc->gen);
+    Launch L;
+    const bool empty = end <= begin;
+    if (!empty) {
+        rc = setup(g, M, desc->gen, false, begin, end, L);
+        if (rc) return rc;
+        L.p.tau = desc->flip_thresh;
+    }
+    std::vector<cudaEvent_t> evs;
+    struct EvGuard {
+        std::vector<cudaEvent_t> &v;
+        ~EvGuard() {
+            for (cudaEvent_t x : v) cudaEventDestroy(x);
+        }
+    } evg{evs};
+    for (uint32_t r = 0; r < desc->rounds; r++) {
+        const uint64_t seed_r = desc->seed + r;
+        if (!empty) {
+            L.p.seed = seed_r;
+            if (g_timing) {
+                cudaEvent_t a, b;
+                cudaEventCreate(&a);
+                cudaEventCreate(&b);
+                evs.push_back(a);
+                evs.push_back(b);
+                cudaEventRecord(a, st);
+            }
+            if ((rc = run(L, stream))) return rc;
+            if (g_timing) cudaEventRecord(evs.back(), st);
+        } else {
+            uint64_t none[2] = {PP_INFEASIBLE_MAKESPAN, PP_INFEASIBLE_MAKESPAN};
+            e = cudaMemcpyAsync(g->d_scalars + SC_LOCAL_MK, none, sizeof none, cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) return cuda_err(e, "empty slice");
+            cudaStreamSynchronize(st);
+        }
+        if (comm) {
+            // key = (makespan << 3) | rank ; min over ranks picks the winning rank,
+            // then the winner's index travels in a second min all-reduce
+            if ((rc = launch_pack_key(g->d_scalars, rank, stream))) return cuda_err((cudaError_t)rc, "pack");
+            ncclResult_t nr = nc->AllReduce(g->d_scalars + SC_KEY_LOCAL, g->d_scalars + SC_KEY_GLOBAL, 1,
+                                            ncclUint64, ncclMin, comm->comm, st);
+            if (nr != ncclSuccess) return nccl_err(nr, "allreduce key");
+            if ((rc = launch_contrib(g->d_scalars, rank, stream))) return cuda_err((cudaError_t)rc, "contrib");
+            nr = nc->AllReduce(g->d_scalars + SC_IDX_LOCAL, g->d_scalars + SC_IDX_GLOBAL, 1, ncclUint64, ncclMin,
+                               comm->comm, st);
+            if (nr != ncclSuccess) return nccl_err(nr, "allreduce index");
+            g_launches += 2;
+        }
+        UParams u{g->d_base, g->d_winner, g->d_best_place, g->d_scalars, seed_r, (uint32_t)K, desc->flip_thresh,
+                  r, comm ? 1 : 0};
+        if ((rc = upd(u, stream))) return cuda_err((cudaError_t)rc, "round update");
+        g_launches++;
+    }
+    uint64_t best[3];
+    std::vector<uint8_t> place(g->base_bytes);
+    e = cudaMemcpyAsync(best, g->d_scalars + SC_BEST_MK, sizeof best, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(place.data(), g->d_best_place, g->base_bytes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_err(e, "search result");
+    for (size_t i = 0; i + 1 < evs.size(); i += 2) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, evs[i], evs[i + 1]) == cudaSuccess) {
+            g_timing_ms += ms;
+            g_timing_n++;
+        }
+    }
+    out->best_makespan_ps = best[0];
+    out->best_index = best[1];
+    out->best_round = best[2];
+    out->t1_ps = g->t1;
+    out->evaluated = desc->count * (uint64_t)desc->rounds;
+    if (out->placement)
+        for (int p = 0; p < K; p++) out->placement[g->pi[p]] = place[p];
+    if (best[0] == PP_INFEASIBLE_MAKESPAN) {
+        set_error("every candidate violates the device memory capacity");
+        return PP_E_INFEASIBLE;
+    }
+    return PP_OK;
+}
+
+int pp_comm_get_unique_id(uint8_t out_id[128]) {
+    Nccl *n = nccl();
+    if (!n) { set_error("NCCL not loadable"); return PP_E_NCCL; }
+    ncclUniqueId id;
+    ncclResult_t r = n->GetUniqueId(&id);
+    if (r != ncclSuccess) return nccl_err(r, "ncclGetUniqueId");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(out_id, &id, 128);
+    return PP_OK;
+}
+
+int pp_comm_init(const uint8_t id_bytes[128], int rank, int world, int cuda_device, pp_comm **out) {
+    if (!out || !id_bytes || world < 1 || world > 8 || rank < 0 || rank >= world) {
+        set_error("invalid comm arguments (1..8 ranks)");
+        return PP_E_INVALID;
+    }
+    Nccl *n = nccl();
+    if (!n) { set_error("NCCL not loadable"); return PP_E_NCCL; }
+    DeviceGuard dg(cuda_device);
+    if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
+    ncclUniqueId id;
+    memcpy(&id, id_bytes, 128);
+    pp_comm *c = new pp_comm();
+    ncclResult_t r = n->CommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) { delete c; return nccl_err(r, "ncclCommInitRank"); }
+    c->rank = rank;
+    c->world = world;
+    c->device = cuda_device;
+    *out = c;
+    return PP_OK;
+}
+
+void pp_comm_destroy(pp_comm *c) {
+    if (!c) return;
+    Nccl *n = nccl();
+    if (n && c->comm) n->CommDestroy(c->comm);
+    delete c;
+}
+
+}  // extern "C"

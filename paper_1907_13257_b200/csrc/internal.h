@@ -1,0 +1,129 @@
+// internal.h — shared declarations of libpp.so (not part of the C ABI).
+//
+// The shared-memory image (built by loader.cpp, read by search_kernel.cuh):
+//
+//   [OpRec  × 2K ]  one record per scheduled op, in issue order: steps
+//                   s = 0..K−1 are the forward ops of π positions p = s, steps
+//                   s = K..2K−1 the backward ops of p = 2K−1−s (reading R1/R2).
+//   [EdgeRec × NE]  the inputs of each step: forward step p lists its in-edges
+//                   (cost c_f), backward step p its out-edges (cost c_b) plus,
+//                   for a sink, a zero-cost "self" record that makes the
+//                   backward wait for its own forward (R1).
+//   [u64   × K  ]   M(k) by π position (only read when a memory cap is set)
+//   [u32   × K  ]   descriptor index of π position p (explicit placements)
+//
+// Times in the kernel are tagged: value = 8·t + device (t < 2^61), so one
+// slot read yields both a producer's finish time and its device; max over
+// tagged values has the max time in its upper bits (ties differ only in the
+// tag, which is cleared before use).  OpRec.cost8 / EdgeRec.c8 hold 8·cost.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/pp.h"
+
+namespace pp {
+
+struct OpRec {
+    uint64_t cost8;       // 8·Δf(p) or 8·Δb(p)
+    uint32_t edge_begin;  // first EdgeRec of this step
+    uint32_t nedge_slot;  // n_edges (bits 0..15) | out_slot (bits 16..31)
+};
+static_assert(sizeof(OpRec) == 16, "OpRec is 16 B");
+
+struct EdgeRec {
+    uint64_t c8;          // 8·c(e) (c = ⌈D·10^12/BW⌉ + L), 0 for a self record
+    uint32_t src_slot;    // slot holding the producer's tagged finish time
+    uint32_t pad;
+};
+static_assert(sizeof(EdgeRec) == 16, "EdgeRec is 16 B");
+
+enum GenKind : int { GEN_GRAY = 0, GEN_RANDOM = 1, GEN_PERTURB = 2, GEN_EXPLICIT = 3 };
+
+constexpr uint64_t kInfeasible = ~0ull;
+constexpr int kMaxImageBytes = 96 * 1024;
+constexpr int kMaxSmemBytes = 227 * 1024;
+
+// Kernel parameters (by value).
+struct KParams {
+    const uint8_t *g_image;      // device image (16-B aligned, padded)
+    const uint8_t *g_base;       // PERTURB base, π order, padded to 16 B (device)
+    const uint8_t *g_place;      // explicit placements [count][K] (device)
+    uint64_t *g_makespan;        // write-all output [end-begin]
+    uint64_t *g_partials;        // [grid][2] per-CTA argmin
+    unsigned *g_ticket;          // last-CTA counter (self-resetting)
+    uint64_t *g_out;             // {makespan, index}
+    uint64_t begin, end;         // candidate range
+    uint64_t seed;               // seed of this round (RANDOM/PERTURB)
+    uint64_t cap;                // memory cap (0 = none)
+    uint32_t image_bytes, base_bytes;
+    uint32_t K;
+    uint32_t nslot;              // W + 1 (dead slot last)
+    uint32_t off_edges, off_mem, off_orig;
+    uint32_t tau;
+    uint32_t smem_slots_off;     // byte offset of the per-lane state in smem
+    uint32_t smem_free_off;      // byte offset of per-lane free[M] (M ≥ 3)
+    uint32_t smem_base_off;      // byte offset of the base copy
+};
+
+// Device scalar slots of pp_dfg::d_scalars (u64).
+enum ScalarSlot : int {
+    SC_LOCAL_MK = 0, SC_LOCAL_IDX = 1,       // this GPU's argmin of the round
+    SC_KEY_LOCAL = 2, SC_KEY_GLOBAL = 3,     // packed key, before / after min all-reduce
+    SC_IDX_LOCAL = 4, SC_IDX_GLOBAL = 5,     // winner-index contribution / result
+    SC_BEST_MK = 6, SC_BEST_IDX = 7, SC_BEST_ROUND = 8,
+    SC_COUNT = 16
+};
+
+struct UParams {
+    uint8_t *base;        // PERTURB base, π order (device)
+    uint8_t *winner;      // scratch [K]
+    uint8_t *best_place;  // [K] best placement so far, π order
+    uint64_t *s;          // d_scalars
+    uint64_t seed;        // seed of this round
+    uint32_t K, tau, round;
+    int multi;            // 1: winner comes from the NCCL-reduced slots
+};
+typedef int (*UpdateFn)(const UParams &, void *stream);
+
+// Launch one search/eval kernel instantiation. Returns a cudaError_t value.
+// threads: CTA size; grid: number of CTAs; smem: dynamic shared bytes.
+typedef int (*LaunchFn)(const KParams &, int grid, int threads, int smem, void *stream);
+
+struct KernelInfo {
+    LaunchFn launch;
+    const void *func;            // for occupancy queries / attributes
+};
+
+// search_inst.cu (compiled once per M with -DPP_M): kernel_for_m<M>(...)
+KernelInfo kernel_for(int M, int gen, bool mem, bool write_all);
+UpdateFn update_for(int M, int gen);
+
+}  // namespace pp
+
+struct pp_dfg {
+    int device = 0;
+    int K = 0, E = 0, W = 0;
+    uint64_t t1 = 0, grad_bytes = 0, cap = 0;
+    std::vector<int32_t> pi;     // π position → descriptor index
+    std::vector<int32_t> pos;    // descriptor index → π position
+    std::vector<uint8_t> image;  // host copy of the image
+    uint32_t off_edges = 0, off_mem = 0, off_orig = 0, image_bytes = 0;
+    uint32_t base_bytes = 0;     // K rounded up to 16
+    // device memory
+    uint8_t *d_image = nullptr;
+    uint8_t *d_base = nullptr;        // [base_bytes] PERTURB base (π order)
+    uint8_t *d_winner = nullptr;      // [base_bytes] scratch placement
+    uint8_t *d_best_place = nullptr;  // [base_bytes]
+    uint64_t *d_partials = nullptr;   // [kMaxGrid][2]
+    unsigned *d_ticket = nullptr;
+    uint64_t *d_scalars = nullptr;    // see capi.cpp (round result, keys, best)
+    int sm_count = 0;
+};
+
+namespace pp {
+void set_error(const std::string &msg);
+void note_launch();
+constexpr int kMaxGrid = 148 * 32;
+}

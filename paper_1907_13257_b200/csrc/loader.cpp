@@ -1,0 +1,273 @@
+// loader.cpp — pp_load_dfg: validation, π, edge costs, forward+backward
+// schedule records, liveness slots, packed shared-memory image, upload.
+//
+// PAPER.md:350 (§6) defines the DFG (K, E, Δ(k), M(k), D(e))
+// the edge delay Δ_e = Σ_l C_el·(D(e)/B(l) + L(l)), here one NVSwitch hop (R4):
+// c(e) = ⌈D(e)·10^12 / BW⌉ + L in integer ps.  π is Kahn's algorithm with the
+// smallest external id first (R3).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <queue>
+#include <unordered_set>
+
+#include "internal.h"
+
+namespace pp {
+
+typedef unsigned __int128 u128;
+
+static int fail(int code, const std::string &msg) {
+    set_error(msg);
+    return code;
+}
+
+// Kahn with a min-heap keyed by external id.  On a cycle, names one cycle.
+static int topo_order(int K, const std::vector<int64_t> &id, const std::vector<int32_t> &src,
+                      const std::vector<int32_t> &dst, std::vector<int32_t> &pi) {
+    std::vector<int> indeg(K, 0);
+    std::vector<std::vector<int>> succ(K), pred(K);
+    for (size_t e = 0; e < src.size(); e++) {
+        indeg[dst[e]]++;
+        succ[src[e]].push_back(dst[e]);
+        pred[dst[e]].push_back(src[e]);
+    }
+    typedef std::pair<int64_t, int> Item;
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
+    for (int k = 0; k < K; k++)
+        if (indeg[k] == 0) heap.push(Item(id[k], k));
+    std::vector<char> done(K, 0);
+    pi.clear();
+    while (!heap.empty()) {
+        int k = heap.top().second;
+        heap.pop();
+        done[k] = 1;
+        pi.push_back(k);
+        for (int v : succ[k])
+            if (--indeg[v] == 0) heap.push(Item(id[v], v));
+    }
+    if ((int)pi.size() == K) return PP_OK;
+    // every unfinished op has an unfinished predecessor: walk back until repeat
+    int v = 0;
+    while (done[v]) v++;
+    std::vector<int> seen(K, -1);
+    for (int step = 0; seen[v] < 0; step++) {
+        seen[v] = step;
+        for (int u : pred[v])
+            if (!done[u]) { v = u; break; }
+    }
+    std::string msg = "cycle:";
+    int start = v;
+    do {
+        msg += " " + std::to_string(id[v]);
+        for (int u : pred[v])
+            if (!done[u]) { v = u; break; }
+    } while (v != start);
+    return fail(PP_E_CYCLE, msg);
+}
+
+int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp_dfg **out) {
+    if (!out) return fail(PP_E_INVALID, "out is NULL");
+    *out = nullptr;
+    if (!d || !link) return fail(PP_E_INVALID, "desc or link is NULL");
+    const int K = d->num_ops, E = d->num_edges;
+    if (K < 1 || E < 0 || !d->fwd_ps || !d->bwd_ps ||
+        (E > 0 && (!d->edge_src || !d->edge_dst || !d->edge_fwd_bytes)))
+        return fail(PP_E_INVALID, "invalid sizes or null arrays");
+    if (link->link_bw_Bps == 0) return fail(PP_E_INVALID, "link bandwidth must be > 0");
+    if (K > 65535) return fail(PP_E_TOO_LARGE, "more than 65535 ops");
+
+    std::vector<int64_t> id(K);
+    std::unordered_set<int64_t> ids;
+    for (int k = 0; k < K; k++) {
+        id[k] = d->op_id ? d->op_id[k] : k;
+        if (id[k] < 0) return fail(PP_E_INVALID, "negative op id");
+        if (!ids.insert(id[k]).second) return fail(PP_E_INVALID, "duplicate op id " + std::to_string(id[k]));
+    }
+    std::vector<int32_t> src(E), dst(E);
+    for (int e = 0; e < E; e++) {
+        src[e] = d->edge_src[e];
+        dst[e] = d->edge_dst[e];
+        if (src[e] < 0 || src[e] >= K || dst[e] < 0 || dst[e] >= K)
+            return fail(PP_E_INVALID, "dangling edge endpoint at edge " + std::to_string(e));
+        if (src[e] == dst[e]) return fail(PP_E_INVALID, "self edge at edge " + std::to_string(e));
+    }
+    std::vector<int32_t> pi;
+    int rc = topo_order(K, id, src, dst, pi);
+    if (rc) return rc;
+    std::vector<int32_t> pos(K);
+    for (int p = 0; p < K; p++) pos[pi[p]] = p;
+
+    // edge costs and the 2^61 time bound (times are tagged as 8·t + device)
+    std::vector<uint64_t> cf(E), cb(E);
+    u128 bound = 0;
+    for (int k = 0; k < K; k++) bound += (u128)d->fwd_ps[k] + d->bwd_ps[k];
+    const u128 t1 = bound;
+    for (int e = 0; e < E; e++) {
+        uint64_t bf = d->edge_fwd_bytes[e];
+        uint64_t bb = d->edge_bwd_bytes ? d->edge_bwd_bytes[e] : bf;
+        u128 qf = ((u128)bf * 1000000000000ull + link->link_bw_Bps - 1) / link->link_bw_Bps + link->link_lat_ps;
+        u128 qb = ((u128)bb * 1000000000000ull + link->link_bw_Bps - 1) / link->link_bw_Bps + link->link_lat_ps;
+        bound += qf + qb;
+        if ((qf >> 64) || (qb >> 64) || (bound >> 61)) return fail(PP_E_RANGE, "time bound >= 2^61 ps");
+        cf[e] = (uint64_t)qf;
+        cb[e] = (uint64_t)qb;
+    }
+    if (bound >> 61) return fail(PP_E_RANGE, "time bound >= 2^61 ps");
+
+    // adjacency by π position
+    std::vector<std::vector<int>> in_e(K), out_e(K);
+    for (int e = 0; e < E; e++) {
+        in_e[pos[dst[e]]].push_back(e);
+        out_e[pos[src[e]]].push_back(e);
+    }
+
+    // ---- liveness: value F(p) produced at step p, B(p) at step 2K−1−p
+    const int S = 2 * K;
+    std::vector<int> last_f(K, -1), last_b(K, -1);
+    for (int e = 0; e < E; e++) {
+        int u = pos[src[e]], v = pos[dst[e]];
+        last_f[u] = std::max(last_f[u], v);             // forward consumer at step v
+        last_b[v] = std::max(last_b[v], S - 1 - u);     // backward of u reads B(v)
+    }
+    for (int p = 0; p < K; p++)
+        if (out_e[p].empty()) last_f[p] = std::max(last_f[p], S - 1 - p);   // sink self record
+    // linear-scan allocation in step order; reads happen before the write
+    std::vector<int> slot_f(K, -1), slot_b(K, -1);
+    std::vector<std::vector<int>> expire(S);   // slots freed after step s
+    std::vector<int> free_slots;               // min-heap of free slot ids
+    int nslots = 0;
+    auto take = [&]() {
+        if (free_slots.empty()) return nslots++;
+        std::pop_heap(free_slots.begin(), free_slots.end(), std::greater<int>());
+        int s = free_slots.back();
+        free_slots.pop_back();
+        return s;
+    };
+    for (int s = 0; s < S; s++) {
+        for (int sl : expire[s]) {
+            free_slots.push_back(sl);
+            std::push_heap(free_slots.begin(), free_slots.end(), std::greater<int>());
+        }
+        bool fwd = s < K;
+        int p = fwd ? s : S - 1 - s;
+        int last = fwd ? last_f[p] : last_b[p];
+        if (last < 0) continue;   // dead value: written to the dead slot
+        int sl = take();
+        (fwd ? slot_f : slot_b)[p] = sl;
+        expire[last].push_back(sl);   // freed before the write of step `last`... see below
+    }
+    // NOTE: a slot freed "at" step `last` becomes available for the output of
+    // step `last` itself (the kernel reads all inputs of a step before it
+    // writes the output), which is what pushing into expire[last] and
+    // draining expire[s] at the top of step s achieves.
+    const int W = nslots;
+    const int dead = W;
+    if (W + 1 > 65535) return fail(PP_E_TOO_LARGE, "too many live slots");
+
+    // ---- records
+    std::vector<OpRec> ops(S);
+    std::vector<EdgeRec> er;
+    for (int s = 0; s < S; s++) {
+        bool fwd = s < K;
+        int p = fwd ? s : S - 1 - s;
+        int k = pi[p];
+        OpRec &o = ops[s];
+        o.cost8 = 8ull * (fwd ? d->fwd_ps[k] : d->bwd_ps[k]);
+        o.edge_begin = (uint32_t)er.size();
+        if (fwd) {
+            for (int e : in_e[p]) er.push_back(EdgeRec{8ull * cf[e], (uint32_t)slot_f[pos[src[e]]], 0});
+        } else {
+            for (int e : out_e[p]) er.push_back(EdgeRec{8ull * cb[e], (uint32_t)slot_b[pos[dst[e]]], 0});
+            if (out_e[p].empty()) er.push_back(EdgeRec{0, (uint32_t)slot_f[p], 0});
+        }
+        uint32_t ne = (uint32_t)er.size() - o.edge_begin;
+        if (ne > 65535) return fail(PP_E_TOO_LARGE, "op with more than 65535 edges");
+        int out_slot = fwd ? slot_f[p] : slot_b[p];
+        if (out_slot < 0) out_slot = dead;
+        o.nedge_slot = ne | ((uint32_t)out_slot << 16);
+    }
+    size_t off_edges = sizeof(OpRec) * S;
+    size_t off_mem = off_edges + sizeof(EdgeRec) * er.size();
+    size_t off_orig = off_mem + 8ull * K;
+    size_t bytes = off_orig + 4ull * K;
+    bytes = (bytes + 15) & ~size_t(15);
+    if (bytes > (size_t)kMaxImageBytes) return fail(PP_E_TOO_LARGE, "DFG image exceeds 96 KB of shared memory");
+
+    pp_dfg *g = new pp_dfg();
+    g->device = cuda_device;
+    g->K = K;
+    g->E = E;
+    g->W = W;
+    g->t1 = (uint64_t)t1;
+    g->cap = link->dev_mem_cap_bytes;
+    g->grad_bytes = 0;
+    if (d->param_bytes)
+        for (int k = 0; k < K; k++) g->grad_bytes += d->param_bytes[k];
+    g->pi = pi;
+    g->pos = pos;
+    g->image.assign(bytes, 0);
+    memcpy(g->image.data(), ops.data(), sizeof(OpRec) * S);
+    if (!er.empty()) memcpy(g->image.data() + off_edges, er.data(), sizeof(EdgeRec) * er.size());
+    for (int p = 0; p < K; p++) {
+        uint64_t m = d->mem_bytes ? d->mem_bytes[pi[p]] : 0;
+        memcpy(g->image.data() + off_mem + 8ull * p, &m, 8);
+        uint32_t o = (uint32_t)pi[p];
+        memcpy(g->image.data() + off_orig + 4ull * p, &o, 4);
+    }
+    g->off_edges = (uint32_t)off_edges;
+    g->off_mem = (uint32_t)off_mem;
+    g->off_orig = (uint32_t)off_orig;
+    g->image_bytes = (uint32_t)bytes;
+    g->base_bytes = (uint32_t)((K + 15) & ~15);
+
+    // ---- device side
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaError_t ce = cudaSetDevice(cuda_device);
+    auto cuda_fail = [&](cudaError_t err) {
+        set_error(std::string("CUDA: ") + cudaGetErrorString(err));
+        cudaSetDevice(prev);
+        return PP_E_CUDA;
+    };
+    if (ce != cudaSuccess) { delete g; return cuda_fail(ce); }
+    cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
+    size_t scal = 64;   // u64 scalars
+    if ((ce = cudaMalloc(&g->d_image, bytes)) != cudaSuccess ||
+        (ce = cudaMalloc(&g->d_base, 3 * g->base_bytes)) != cudaSuccess ||
+        (ce = cudaMalloc(&g->d_partials, sizeof(uint64_t) * 2 * kMaxGrid)) != cudaSuccess ||
+        (ce = cudaMalloc(&g->d_ticket, sizeof(unsigned) * 4)) != cudaSuccess ||
+        (ce = cudaMalloc(&g->d_scalars, sizeof(uint64_t) * scal)) != cudaSuccess) {
+        pp_free_dfg(g);
+        return cuda_fail(ce);
+    }
+    g->d_winner = g->d_base + g->base_bytes;
+    g->d_best_place = g->d_base + 2 * g->base_bytes;
+    if ((ce = cudaMemcpy(g->d_image, g->image.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (ce = cudaMemset(g->d_base, 0, 3 * g->base_bytes)) != cudaSuccess ||
+        (ce = cudaMemset(g->d_ticket, 0, sizeof(unsigned) * 4)) != cudaSuccess ||
+        (ce = cudaMemset(g->d_scalars, 0, sizeof(uint64_t) * scal)) != cudaSuccess) {
+        pp_free_dfg(g);
+        return cuda_fail(ce);
+    }
+    cudaSetDevice(prev);
+    *out = g;
+    return PP_OK;
+}
+
+}  // namespace pp
+
+extern "C" void pp_free_dfg(pp_dfg *g) {
+    if (!g) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(g->device);
+    if (g->d_image) cudaFree(g->d_image);
+    if (g->d_base) cudaFree(g->d_base);
+    if (g->d_partials) cudaFree(g->d_partials);
+    if (g->d_ticket) cudaFree(g->d_ticket);
+    if (g->d_scalars) cudaFree(g->d_scalars);
+    cudaSetDevice(prev);
+    delete g;
+}

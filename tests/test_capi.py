@@ -1,0 +1,96 @@
+"""The C-ABI library loads and exports every symbol include/pp.h declares;
+host-only protocol helpers; loader validation runs on the host before any CUDA
+call, so its error codes are checked here against the oracle (no GPU)."""
+import os
+import re
+
+import pytest
+
+import oracle as O
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def pp():
+    from paper_1907_13257_b200 import _build
+    _build.build()
+    import paper_1907_13257_b200 as pp
+    pp.lib()
+    return pp
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "pp.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return set(re.findall(r"\b(pp_[a-z0-9_]+)\s*\(", src))
+
+
+def test_every_declared_symbol_is_exported(pp):
+    declared = _declared_functions()
+    assert len(declared) >= 19
+    L = pp.lib()
+    for name in declared:
+        assert hasattr(L, name), name
+    assert declared == set(pp.pp.SIGNATURES), declared ^ set(pp.pp.SIGNATURES)
+
+
+def test_struct_sizes(pp):
+    import ctypes as C
+    assert C.sizeof(pp.pp.Cell) == 48
+    assert C.sizeof(pp.pp.SearchDesc) == 40
+    assert C.sizeof(pp.pp.CrossoverC) == 76
+
+
+def test_rank_slices_partition(pp):
+    for count in (1, 7, 8, 1000, 10**8, 2**63 + 5):
+        for world in range(1, 9):
+            prev = 0
+            for r in range(world):
+                b, e = pp.rank_slice(count, r, world)
+                assert b == prev and e >= b
+                prev = e
+            assert prev == count
+
+
+def test_key_order_is_lexicographic(pp):
+    # min key picks the smaller makespan, ties to the lower rank (lower global index)
+    assert pp.pack_key(5, 7) < pp.pack_key(6, 0)
+    assert pp.pack_key(5, 1) < pp.pack_key(5, 2)
+    assert pp.key_makespan(pp.pack_key(123456789, 3)) == 123456789
+    assert pp.key_rank(pp.pack_key(123456789, 3)) == 3
+    assert pp.key_makespan(pp.pack_key(pp.INFEASIBLE, 4)) == pp.INFEASIBLE
+    assert pp.pack_key(2**61 - 2, 0) < pp.pack_key(pp.INFEASIBLE, 0)
+
+
+@pytest.mark.parametrize("bad,code", [
+    (dict(edge_src=[0, 0, 1, 3], edge_dst=[1, 2, 3, 1]), -2),
+    (dict(edge_dst=[1, 2, 3, 9]), -1),
+    (dict(edge_src=[0, 0, 1, 2], edge_dst=[1, 2, 3, 2]), -1),
+    (dict(op_id=[1, 2, 2, 3]), -1),
+    (dict(op_id=[1, -2, 4, 3]), -1),
+    (dict(fwd_ps=[2**60, 2**60, 8, 2]), -3),
+    (dict(link_bw_Bps=0), -1),
+])
+def test_loader_validation_matches_oracle(pp, bad, code):
+    spec = dict(synth.diamond(), **bad)
+    with pytest.raises(pp.PPError) as e:
+        pp.Dfg(spec)
+    assert e.value.code == code
+    with pytest.raises(O.OracleError) as e2:
+        O.Dfg.from_spec(spec)
+    assert e2.value.code == code
+    if code == -2:
+        # both name the same cycle's ids
+        ids = lambda s: sorted(int(x) for x in s.split("cycle:")[1].split())
+        assert ids(str(e.value)) == ids(str(e2.value)) == [1, 3]
+
+
+def test_no_cpu_fallback(pp):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(pp.PPError) as e:
+        pp.Dfg(synth.toy12())
+    assert e.value.code == -6

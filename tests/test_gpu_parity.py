@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+bit for bit (integer ps; every compared value is an exact
+integer, so the tolerance is zero)."""
+import random
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1907_13257_b200 as pp  # noqa: E402
+
+PAPER = ["toy12", "gnmt", "biglstm", "inception_v3"]
+
+
+def _oracle_candidates(od, M, gen, seed_r, tau, base_pi, idx):
+    return np.array([od.makespan_pi(M, O.gen(od.K, M, gen, seed_r, tau, base_pi, int(i))) for i in idx],
+                    dtype=np.uint64)
+
+
+@pytest.fixture(scope="module")
+def dfgs():
+    out = {}
+    for name in PAPER:
+        spec = getattr(synth, name)()
+        out[name] = (spec, pp.Dfg(spec), O.Dfg.from_spec(spec))
+    return out
+
+
+def test_pi_and_t1_match(dfgs):
+    for name, (spec, g, od) in dfgs.items():
+        assert list(g.pi) == list(od.pi)
+        assert g.t1 == od.t1
+        assert g.grad_bytes == od.grad_bytes
+
+
+def test_toy12_exhaustive_gray(dfgs):
+    spec, g, od = dfgs["toy12"]
+    r = g.search_best(2, pp.GEN_GRAY, 0, 4096)
+    o = od.search(2, O.GEN_GRAY, 0, 4096)
+    assert (r.best_makespan_ps, r.best_index, r.best_round, r.evaluated) == \
+           (o.best_makespan_ps, o.best_index, o.best_round, o.evaluated)
+    assert np.array_equal(r.placement, o.placement)
+    assert (r.best_makespan_ps, r.best_index) == (920_000_000, 288)
+    # every one of the 4096 makespans
+    got = pp.u64(g.eval_generated(2, pp.GEN_GRAY, 0, 0, None, 0, 4096))
+    want = _oracle_candidates(od, 2, O.GEN_GRAY, 0, 0, None, range(4096))
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 4, 5, 8])
+def test_eval_placements_paper_dfgs(dfgs, M):
+    rng = np.random.default_rng(M)
+    for name, (spec, g, od) in dfgs.items():
+        count = 1000 + 37   # several CTAs and a ragged tail
+        pl = rng.integers(0, M, size=(count, g.K), dtype=np.uint8)
+        pl[0] = 0
+        got = pp.u64(g.eval_placements(M, torch.as_tensor(pl, device="cuda")))
+        want = np.array([od.makespan(M, row) for row in pl], dtype=np.uint64)
+        assert np.array_equal(got, want), name
+        assert got[0] == od.t1
+
+
+@pytest.mark.parametrize("gen", [O.GEN_RANDOM, O.GEN_PERTURB])
+@pytest.mark.parametrize("M", [2, 3, 4, 8])
+def test_eval_generated_paper_dfgs(dfgs, gen, M):
+    rng = np.random.default_rng(10 * M + gen)
+    for name, (spec, g, od) in dfgs.items():
+        base = rng.integers(0, M, size=g.K, dtype=np.uint8)
+        seed = int(rng.integers(0, 2**63))
+        tau = 24
+        begin, count = (0, 700) if name != "toy12" else (0, 4096)
+        got = pp.u64(g.eval_generated(M, gen, seed, tau, base, begin, count))
+        want = _oracle_candidates(od, M, gen, seed, tau, base, range(begin, begin + count))
+        assert np.array_equal(got, want), name
+        # far into the index space (ragged tail at an odd offset)
+        begin = 10**9 + 13
+        got = pp.u64(g.eval_generated(M, gen, seed, tau, base, begin, 77))
+        want = _oracle_candidates(od, M, gen, seed, tau, base, range(begin, begin + 77))
+        assert np.array_equal(got, want), name
+
+
+@pytest.mark.parametrize("M", [2, 3, 4, 5, 6, 7, 8])
+def test_gray_small_exhaustive_all_M(M):
+    K = {2: 10, 3: 6, 4: 5, 5: 4, 6: 4, 7: 4, 8: 3}[M]
+    spec = synth.random_dag(300 + M, K, avg_deg=1.7, max_cost=100, max_bytes=100)
+    g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
+    n = M**K
+    got = pp.u64(g.eval_generated(M, pp.GEN_GRAY, 0, 0, None, 0, n))
+    want = _oracle_candidates(od, M, O.GEN_GRAY, 0, 0, None, range(n))
+    assert np.array_equal(got, want)
+    r = g.search_best(M, pp.GEN_GRAY, 0, n)
+    o = od.search(M, O.GEN_GRAY, 0, n)
+    assert (r.best_makespan_ps, r.best_index) == (o.best_makespan_ps, o.best_index)
+    assert np.array_equal(r.placement, o.placement)
+
+
+def test_search_random_inception_prefix(dfgs):
+    spec, g, od = dfgs["inception_v3"]
+    for M in (2, 4):
+        r = g.search_best(M, pp.GEN_RANDOM, 13257, 200_003)
+        o = od.search(M, O.GEN_RANDOM, 13257, 200_003)
+        assert (r.best_makespan_ps, r.best_index, r.best_round) == (o.best_makespan_ps, o.best_index, o.best_round)
+        assert np.array_equal(r.placement, o.placement)
+
+
+@pytest.mark.parametrize("name,M", [("gnmt", 2), ("gnmt", 4), ("biglstm", 2), ("inception_v3", 4), ("toy12", 3)])
+def test_search_perturb_rounds(dfgs, name, M):
+    spec, g, od = dfgs[name]
+    count, rounds = (20_000, 4) if name != "toy12" else (500, 6)
+    rng = np.random.default_rng(5)
+    base = rng.integers(0, M, size=g.K, dtype=np.uint8)
+    r = g.search_best(M, pp.GEN_PERTURB, 99, count, rounds=rounds, tau=8, base=base)
+    o = od.search(M, O.GEN_PERTURB, 99, count, rounds=rounds, tau=8, base=base)
+    assert (r.best_makespan_ps, r.best_index, r.best_round, r.evaluated) == \
+           (o.best_makespan_ps, o.best_index, o.best_round, o.evaluated)
+    assert np.array_equal(r.placement, o.placement)
+    assert od.makespan(M, r.placement) == r.best_makespan_ps
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_random_dags(seed):
+    rng = random.Random(seed)
+    K = rng.choice([1, 2, 7, 33, 100, 257, 600, 1024])
+    deg = rng.choice([0.5, 1.5, 3.0]) if K < 600 else 1.0
+    spec = synth.random_dag(seed, K, avg_deg=deg, max_in=rng.choice([2, 4, 9]),
+                            max_cost=rng.choice([10, 10**6]), max_bytes=rng.choice([0, 100, 10**7]),
+                            lat_max=rng.choice([0, 1000]))
+    if rng.random() < 0.3:
+        spec["mem_bytes"] = [rng.randint(0, 100) for _ in range(K)]
+        spec["dev_mem_cap_bytes"] = rng.randint(1, 60 * K)
+    g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
+    M = rng.choice([1, 2, 3, 4, 5, 8])
+    for gen in (O.GEN_RANDOM, O.GEN_PERTURB):
+        base = np.array([rng.randrange(M) for _ in range(K)], dtype=np.uint8)
+        s = rng.getrandbits(64)
+        begin = rng.choice([0, 5, 10**12])
+        got = pp.u64(g.eval_generated(M, gen, s, 40, base, begin, 333))
+        want = _oracle_candidates(od, M, gen, s, 40, base, range(begin, begin + 333))
+        assert np.array_equal(got, want)
+
+
+def test_memory_cap_infeasible():
+    spec = synth.random_dag(7, 20)
+    spec["mem_bytes"] = [10] * 20
+    spec["dev_mem_cap_bytes"] = 150          # needs ≥ 2 devices (200 B total)
+    g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
+    got = pp.u64(g.eval_generated(2, pp.GEN_RANDOM, 1, 0, None, 0, 500))
+    want = _oracle_candidates(od, 2, O.GEN_RANDOM, 1, 0, None, range(500))
+    assert np.array_equal(got, want)
+    assert got[0] == pp.INFEASIBLE            # index 0 = all on device 0
+    r = g.search_best(2, pp.GEN_RANDOM, 1, 500)
+    assert r.best_makespan_ps == od.search(2, O.GEN_RANDOM, 1, 500).best_makespan_ps
+    spec["dev_mem_cap_bytes"] = 5            # nothing fits
+    g2 = pp.Dfg(spec)
+    with pytest.raises(pp.PPError) as e:
+        g2.search_best(2, pp.GEN_RANDOM, 1, 100)
+    assert e.value.code == -5
+
+
+def test_rank_slices_equal_full_search(dfgs):
+    """Fake multi-rank on one GPU: slice the candidates exactly as the NCCL
+    path does, reduce the packed keys on the host; GPU-count invariance."""
+    spec, g, od = dfgs["gnmt"]
+    count = 50_001
+    full = g.search_best(2, pp.GEN_RANDOM, 3, count)
+    for world in (1, 2, 3, 4, 8):
+        keys, idx = [], []
+        for r in range(world):
+            b, e = pp.rank_slice(count, r, world)
+            out = pp.u64(g.search_range(2, pp.GEN_RANDOM, 3, 0, None, b, e))
+            keys.append(pp.pack_key(int(out[0]), r))
+            idx.append(int(out[1]))
+        k = min(keys)
+        assert pp.key_makespan(k) == full.best_makespan_ps
+        assert idx[pp.key_rank(k)] == full.best_index
+
+
+def test_edge_cases():
+    # single op, no edges; M = 1; empty eval
+    spec = synth.independent(1, 5, 7)
+    g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
+    assert g.search_best(1, pp.GEN_GRAY, 0, 1).best_makespan_ps == 12
+    r = g.search_best(4, pp.GEN_GRAY, 0, 4)
+    assert r.best_makespan_ps == 12 and r.best_index == 0
+    out = g.eval_placements(2, torch.zeros((0, 1), dtype=torch.uint8, device="cuda"))
+    assert out.numel() == 0
+    # independent ops: SU = M exactly (closed form, K7)
+    spec = synth.independent(8, 4, 5)
+    g = pp.Dfg(spec)
+    assert g.search_best(4, pp.GEN_GRAY, 0, 4**8).best_makespan_ps == 2 * 9
+    # chain: SU = 1 (K6)
+    spec = synth.chain(9, 3, 6, 50)
+    g = pp.Dfg(spec)
+    assert g.search_best(3, pp.GEN_GRAY, 0, 3**9).best_makespan_ps == g.t1
+
+
+def test_large_image_reduces_cta():
+    # K + E near the 96 KB image cap, large W
+    spec = synth.random_dag(77, 1100, avg_deg=0.9, max_in=3)
+    g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
+    assert g.image_bytes > 60_000
+    for M in (2, 8):
+        got = pp.u64(g.eval_generated(M, pp.GEN_RANDOM, 4, 0, None, 0, 100))
+        want = _oracle_candidates(od, M, O.GEN_RANDOM, 4, 0, None, range(100))
+        assert np.array_equal(got, want)
+
+
+def test_error_codes_match_oracle():
+    base = synth.diamond()
+    for bad, code in [(dict(base, edge_src=[0, 0, 1, 3], edge_dst=[1, 2, 3, 1]), -2),
+                      (dict(base, edge_dst=[1, 2, 3, 9]), -1),
+                      (dict(base, op_id=[1, 2, 2, 3]), -1),
+                      (dict(base, fwd_ps=[2**60, 2**60, 8, 2]), -3)]:
+        with pytest.raises(pp.PPError) as e:
+            pp.Dfg(bad)
+        assert e.value.code == code
+        with pytest.raises(O.OracleError) as e2:
+            O.Dfg.from_spec(bad)
+        assert e2.value.code == code
+    g = pp.Dfg(synth.toy12())
+    with pytest.raises(pp.PPError) as e:
+        g.search_best(2, pp.GEN_GRAY, 0, 4097)
+    assert e.value.code == -1
+    g = pp.Dfg(synth.inception_v3())
+    with pytest.raises(pp.PPError) as e:
+        g.search_best(2, pp.GEN_GRAY, 0, 10)
+    assert e.value.code == -4
