@@ -1,10 +1,11 @@
 """Benchmark of the hot path (BASELINE.json metric: placements evaluated/sec).
 
-One step = one pass of the whole path over one batch:
-on-device generation + forward/backward list schedule + argmin of
-`--count` candidate placements of the Inception-V3-shaped DFG on M devices
-(sharded over the ranks, NCCL min all-reduce of the packed key), the round
-update, then the end-to-end projection over N = 1..N_max and the crossover.
+One step = one pass of the whole path over one batch: a
+placement search of the Inception-V3-shaped DFG on M devices (BASELINE
+config 4: PERTURB, `--rounds` × `--count` candidates; on-device generation +
+forward/backward list schedule + argmin, sharded over the ranks with an NCCL
+min all-reduce of the packed key per round, the round/base update), then the
+end-to-end projection over N = 1..N_max and the crossover.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl pp|reference]
 
@@ -114,20 +115,20 @@ def measured_clock():
 
 
 # ------------------------------------------------------------ oracle arm
-def cpu_oracle_sample(spec, M, n_target_s=12.0, count=None):
+def cpu_oracle_sample(spec, M, gen_name, tau, n_target_s=12.0):
     """The CPU oracle (oracle/) as it stands, single thread, on a bounded
-    prefix of the same candidate stream; returns (placements/s, n, seconds)."""
+    prefix of round 0 of the same candidate stream (placements/s, n, s)."""
     import oracle as O
+    gen = O.GEN_PERTURB if gen_name == "perturb" else O.GEN_RANDOM
     od = O.Dfg.from_spec(spec)
-    if count is None:
-        t = time.perf_counter()
-        od.round(M, O.GEN_RANDOM, SEED, 0, None, 0, 20_000)
-        rate = 20_000 / (time.perf_counter() - t)
-        count = max(20_000, int(rate * n_target_s))
     t = time.perf_counter()
-    r = od.search(M, O.GEN_RANDOM, SEED, count)
+    od.round(M, gen, SEED, tau, None, 0, 20_000)
+    rate = 20_000 / (time.perf_counter() - t)
+    count = max(20_000, int(rate * n_target_s))
+    t = time.perf_counter()
+    od.round(M, gen, SEED, tau, None, 0, count)
     dt = time.perf_counter() - t
-    return count / dt, count, dt, od, r
+    return count / dt, count, dt
 
 
 def run_reference(args):
@@ -137,12 +138,15 @@ def run_reference(args):
     import oracle as O
     spec = workload(args)
     ops, _ = alg_counts(spec)
-    n_step = args.ref_sample
+    gen = O.GEN_PERTURB if args.gen == "perturb" else O.GEN_RANDOM
+    rounds = args.rounds if args.gen == "perturb" else 1
+    per_round = max(1, args.ref_sample // rounds)
+    n_step = per_round * rounds
     times = []
     for s in range(args.warmup + args.steps):
         t = time.perf_counter()
         od = O.Dfg.from_spec(spec)
-        r = od.search(args.M, O.GEN_RANDOM, SEED, n_step)
+        r = od.search(args.M, gen, SEED, per_round, rounds=rounds, tau=args.tau)
         sc = synth.sweep_scenario("inception_v3", od.t1, od.grad_bytes)
         cells = O.Scenario.from_spec(sc).project([1, args.M], [od.t1, r.best_makespan_ps], args.nmax)
         x = O.crossover(cells, [1, args.M], args.nmax)
@@ -157,8 +161,9 @@ def run_reference(args):
             "data": "synthetic", "gpu_launches": 0,
             "config": config_dict(args, spec, per_step=n_step),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{n_step} RANDOM candidates of the Inception-V3-shaped DFG per step "
-                                       f"(prefix of the GPU step's {args.count}) + projection N=1..{args.nmax} + crossover"},
+                             "sample": f"{rounds} rounds x {per_round} {args.gen.upper()} candidates of the "
+                                       f"Inception-V3-shaped DFG per step (the GPU step runs {rounds} x {args.count}) "
+                                       f"+ projection N=1..{args.nmax} + crossover"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "crossover_n_star": x.n_star}
     print(json.dumps(line), flush=True)
@@ -166,10 +171,13 @@ def run_reference(args):
 
 
 def config_dict(args, spec, per_step=None):
-    return {"workload": f"inception_v3_shaped_M{args.M}_random_{args.count:.0e}".replace("+0", ""),
+    gen = (f"PERTURB tau={args.tau}/256, {args.rounds} rounds x {args.count:.0e}" if args.gen == "perturb"
+           else f"RANDOM {args.count:.0e}").replace("+0", "")
+    return {"workload": f"inception_v3_shaped_M{args.M}_{args.gen}_{args.count * args.rounds:.0e}".replace("+0", ""),
             "dfg": "Inception-V3-shaped (synth.inception_v3, batch 64)", "K": len(spec["fwd_ps"]),
-            "E": len(spec["edge_src"]), "M": args.M, "generator": "RANDOM (SplitMix64)", "seed": SEED,
-            "candidates_per_step": per_step or args.count, "projection": f"M in {{1,{args.M}}}, N=1..{args.nmax}",
+            "E": len(spec["edge_src"]), "M": args.M, "generator": gen + " (SplitMix64)", "seed": SEED,
+            "candidates_per_step": per_step or args.count * args.rounds,
+            "projection": f"M in {{1,{args.M}}}, N=1..{args.nmax}, EQ5, ring AR on",
             "l2": "flushed between timed steps (256 MiB write); inputs live on-chip"}
 
 
@@ -189,6 +197,8 @@ def run_pp(args):
         dist.init_process_group("nccl", device_id=dev)
         comm = pp.Comm(rank, world, local)
     stream = torch.cuda.current_stream()
+    GEN = pp.GEN_PERTURB if args.gen == "perturb" else pp.GEN_RANDOM
+    per_step = args.count * args.rounds
     spec = workload(args)
     g = pp.Dfg(spec, device=local)
     M = args.M
@@ -201,7 +211,7 @@ def run_pp(args):
         torch.cuda.synchronize()
 
     def step():
-        r = g.search_best(M, pp.GEN_RANDOM, SEED, args.count, comm=comm, stream=stream)
+        r = g.search_best(M, GEN, SEED, args.count, rounds=args.rounds, tau=args.tau, comm=comm, stream=stream)
         cells = pp.project_e2e(sc, [1, M], [g.t1, r.best_makespan_ps], args.nmax, device=local, stream=stream)
         x = pp.crossover(cells, [1, M], args.nmax, best_m=False, stream=stream)
         return r, x
@@ -230,7 +240,7 @@ def run_pp(args):
     if world > 1:
         dist.all_reduce(tot_ms, op=dist.ReduceOp.MAX)
     tot_ms, kern_ms_max = float(tot_ms[0]), float(tot_ms[1])
-    value = args.count * args.steps / (tot_ms / 1e3)
+    value = per_step * args.steps / (tot_ms / 1e3)
 
     # ---- e2e through the C ABI with host buffers (load + search + projection + results)
     barrier()
@@ -242,7 +252,7 @@ def run_pp(args):
         t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         g2 = pp.Dfg(spec, device=local)                        # H2D of the DFG image
-        r2 = g2.search_best(M, pp.GEN_RANDOM, SEED, args.count, comm=comm, stream=stream)
+        r2 = g2.search_best(M, GEN, SEED, args.count, rounds=args.rounds, tau=args.tau, comm=comm, stream=stream)
         cells2 = pp.project_e2e(sc, [1, M], [g2.t1, r2.best_makespan_ps], args.nmax, device=local, stream=stream)
         x2 = pp.crossover(cells2, [1, M], args.nmax, best_m=False, stream=stream)
         t1.record(stream)
@@ -254,13 +264,13 @@ def run_pp(args):
     e2 = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2, op=dist.ReduceOp.MAX)
-    e2e_value = args.count * len(e2e_ms) / (float(e2[0]) / 1e3)
+    e2e_value = per_step * len(e2e_ms) / (float(e2[0]) / 1e3)
 
     if rank == 0:
         ops, smem_b = alg_counts(spec)
         clock, clock_src = measured_clock()
         pk = peaks(torch.cuda.get_device_properties(dev).multi_processor_count, clock)
-        per_launch = args.count // world if world else args.count
+        per_launch = args.count / world
         kern_avg_s = (kern_ms_max / max(1, kern_n)) / 1e3
         achieved_ops = ops * per_launch / kern_avg_s
         achieved_smem = smem_b * per_launch / kern_avg_s
@@ -273,7 +283,7 @@ def run_pp(args):
             "gpu_launches": int(launches),
             "roofline": {"bound": "alu", "achieved": achieved_ops / 1e12, "peak": pk["int32_ops_per_s"] / 1e12,
                          "unit": "Tops/s (int32)", "frac": achieved_ops / pk["int32_ops_per_s"],
-                         "traffic": None, "kernel": "pp::search_kernel<M,RANDOM>",
+                         "traffic": None, "kernel": f"pp::search_kernel<{M},{args.gen.upper()}>",
                          "kernel_ms_avg": kern_avg_s * 1e3, "kernel_share_of_step": kern_ms_max / tot_ms,
                          "alg_ops_per_placement": ops, "alg_smem_bytes_per_placement": smem_b,
                          "smem_frac": achieved_smem / pk["smem_bytes_per_s"],
@@ -285,10 +295,10 @@ def run_pp(args):
                        "n_star_vs_best_dp": x.n_star_vs_best_dp},
         }
         if world == 1 and not args.no_cpu_baseline:
-            rate, n, dt, od, orr = cpu_oracle_sample(spec, M)
+            rate, n, dt = cpu_oracle_sample(spec, M, args.gen, args.tau)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
-                                    "sample": f"first {n} RANDOM candidates of the same stream, {dt:.1f} s, "
-                                              f"single thread (nproc={os.cpu_count()})"}
+                                    "sample": f"first {n} {args.gen.upper()} candidates of round 0 of the same "
+                                              f"stream, {dt:.1f} s, single thread (nproc={os.cpu_count()})"}
         print(json.dumps(line), flush=True)
     g.close()
     if comm is not None:
@@ -305,11 +315,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="pp", choices=["pp", "reference"])
     ap.add_argument("--M", type=int, default=2)
-    ap.add_argument("--count", type=int, default=100_000_000)
+    ap.add_argument("--count", type=int, default=10_000_000, help="candidates per round")
+    ap.add_argument("--rounds", type=int, default=10)
+    ap.add_argument("--gen", default="perturb", choices=["perturb", "random"])
+    ap.add_argument("--tau", type=int, default=8)
     ap.add_argument("--nmax", type=int, default=1024)
     ap.add_argument("--ref-sample", type=int, default=200_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gen == "random":
+        args.rounds = 1
     if args.impl == "reference":
         return run_reference(args)
     return run_pp(args)

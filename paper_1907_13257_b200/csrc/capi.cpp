@@ -59,6 +59,7 @@ UpdateFn update_for(int M, int gen) {
 struct ProjParams;
 struct CrossParams;
 int launch_pack_key(uint64_t *s, int rank, void *stream);
+int launch_patch_base(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, void *stream);
 int launch_contrib(uint64_t *s, int rank, void *stream);
 
 static int cuda_err(cudaError_t e, const char *what) {
@@ -88,25 +89,18 @@ struct Launch {
     KParams p{};
 };
 
-// Chooses the CTA size (largest of 256/128/64/32 whose per-lane state fits),
+// Chooses the CTA size (largest of 256/128/64/32 whose per-warp state fits),
 // the dynamic shared memory layout and a grid of (resident CTAs per SM) × SMs.
 static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin, uint64_t end, Launch &L) {
     const bool mem = g->cap > 0;
     L.k = kernel_for(M, gen, mem, write_all);
-    const uint32_t nslot = (uint32_t)g->W + 1;
+    const uint32_t nslot = (uint32_t)g->W + 2;                  // live + dead + zero
+    const uint32_t region = (nslot + (M > 2 ? (uint32_t)M : 0u)) * kSlotStride;
+    const uint32_t slots_off = (g->image_bytes + 127) & ~127u;
     int threads = 256;
     size_t smem = 0;
-    uint32_t slots_off = 0, free_off = 0, base_off = 0;
     for (; threads >= 32; threads >>= 1) {
-        size_t off = (g->image_bytes + 127) & ~size_t(127);
-        slots_off = (uint32_t)off;
-        off += (size_t)nslot * threads * 8;
-        free_off = (uint32_t)off;
-        if (M > 2) off += (size_t)M * threads * 8;
-        off = (off + 15) & ~size_t(15);
-        base_off = (uint32_t)off;
-        if (gen == GEN_PERTURB) off += g->base_bytes;
-        smem = off;
+        smem = slots_off + (size_t)(threads / 32) * region;
         if (smem <= (size_t)kMaxSmemBytes) break;
     }
     if (threads < 32) {
@@ -120,7 +114,7 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
     if (e != cudaSuccess) return cuda_err(e, "occupancy");
     if (occ < 1) occ = 1;
     const uint64_t n = end - begin;
-    const uint64_t tiles = (n + 31) / 32;
+    const uint64_t tiles = (n + 32 * kNP - 1) / (32 * kNP);
     const uint64_t wpb = threads / 32;
     uint64_t want = (tiles + wpb - 1) / wpb;
     uint64_t grid = std::min<uint64_t>((uint64_t)occ * g->sm_count, want);
@@ -130,20 +124,18 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
     L.smem = (int)smem;
     KParams &p = L.p;
     p.g_image = g->d_image;
-    p.g_base = g->d_base;
     p.begin = begin;
     p.end = end;
     p.cap = g->cap;
     p.image_bytes = g->image_bytes;
-    p.base_bytes = g->base_bytes;
     p.K = (uint32_t)g->K;
-    p.nslot = nslot;
-    p.off_edges = g->off_edges;
+    p.off_extra = g->off_extra;
     p.off_mem = g->off_mem;
     p.off_orig = g->off_orig;
     p.smem_slots_off = slots_off;
-    p.smem_free_off = free_off;
-    p.smem_base_off = base_off;
+    p.region_bytes = region;
+    p.free_off = nslot * kSlotStride;
+    p.zero_off = (uint32_t)(g->W + 1) * kSlotStride;
     p.g_partials = g->d_partials;
     p.g_ticket = g->d_ticket;
     p.g_out = g->d_scalars + SC_LOCAL_MK;
@@ -278,8 +270,9 @@ int pp_eval_generated(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t
     DeviceGuard dg(g->device);
     if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
     if (gen == GEN_PERTURB) {
-        cudaError_t e = cudaMemcpyAsync(g->d_base, d_base_pi, g->K, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
-        if (e != cudaSuccess) return cuda_err(e, "base copy");
+        if ((rc = launch_patch_base(g->d_image, g->d_base, d_base_pi, (uint32_t)g->K, stream)))
+            return cuda_err((cudaError_t)rc, "base patch");
+        g_launches++;
     }
     Launch L;
     rc = setup(g, M, gen, true, begin, begin + count, L);
@@ -301,8 +294,9 @@ int pp_search_range(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
     DeviceGuard dg(g->device);
     if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
     if (gen == GEN_PERTURB) {
-        cudaError_t e = cudaMemcpyAsync(g->d_base, d_base_pi, g->K, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
-        if (e != cudaSuccess) return cuda_err(e, "base copy");
+        if ((rc = launch_patch_base(g->d_image, g->d_base, d_base_pi, (uint32_t)g->K, stream)))
+            return cuda_err((cudaError_t)rc, "base patch");
+        g_launches++;
     }
     Launch L;
     rc = setup(g, M, gen, false, begin, end, L);
@@ -354,8 +348,11 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
             base[p] = desc->base[g->pi[p]];
             if (base[p] >= M) { set_error("base device out of range"); return PP_E_INVALID; }
         }
-    cudaError_t e = cudaMemcpyAsync(g->d_base, base.data(), g->base_bytes, cudaMemcpyHostToDevice, st);
+    cudaError_t e = cudaMemcpyAsync(g->d_winner, base.data(), g->base_bytes, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_err(e, "base upload");
+    if ((rc = launch_patch_base(g->d_image, g->d_base, g->d_winner, (uint32_t)K, stream)))
+        return cuda_err((cudaError_t)rc, "base patch");
+    g_launches++;
     uint64_t begin = 0, end = 0;
     pp_rank_slice(desc->count, rank, world, &begin, &end);
     UpdateFn upd = update_for(M, desc->gen);
@@ -406,7 +403,7 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
             if (nr != ncclSuccess) return nccl_err(nr, "allreduce index");
             g_launches += 2;
         }
-        UParams u{g->d_base, g->d_winner, g->d_best_place, g->d_scalars, seed_r, (uint32_t)K, desc->flip_thresh,
+        UParams u{g->d_image, g->d_base, g->d_winner, g->d_best_place, g->d_scalars, seed_r, (uint32_t)K, desc->flip_thresh,
                   r, comm ? 1 : 0};
         if ((rc = upd(u, stream))) return cuda_err((cudaError_t)rc, "round update");
         g_launches++;

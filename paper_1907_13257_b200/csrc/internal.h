@@ -2,20 +2,29 @@
 //
 // The shared-memory image (built by loader.cpp, read by search_kernel.cuh):
 //
-//   [OpRec  × 2K ]  one record per scheduled op, in issue order: steps
-//                   s = 0..K−1 are the forward ops of π positions p = s, steps
-//                   s = K..2K−1 the backward ops of p = 2K−1−s (reading R1/R2).
-//   [EdgeRec × NE]  the inputs of each step: forward step p lists its in-edges
-//                   (cost c_f), backward step p its out-edges (cost c_b) plus,
-//                   for a sink, a zero-cost "self" record that makes the
-//                   backward wait for its own forward (R1).
-//   [u64   × K  ]   M(k) by π position (only read when a memory cap is set)
-//   [u32   × K  ]   descriptor index of π position p (explicit placements)
+//   [OpRec    × 2K]  one 32-B record per scheduled op, in issue order: steps
+//                    s = 0..K−1 are the forward ops of π positions p = s, steps
+//                    s = K..2K−1 the backward ops of p = 2K−1−s (readings R1/R2).
+//                    The op's FIRST input edge is inlined in the record (most
+//                    ops of a training DFG have in-degree 1); an op without
+//                    inputs gets a zero-cost edge from the always-zero slot, a
+//                    sink's backward gets a zero-cost "self" edge from its own
+//                    forward finish time (it waits for its own forward, R1).
+//   [ExtraRec × NX]  the remaining input edges, consumed in step order.
+//   [u64   × K  ]    M(k) by π position (read only when a memory cap is set)
+//   [u32   × K  ]    descriptor index of π position p (explicit placements)
+//
+// Per-lane schedule state lives in a per-warp region of shared memory laid out
+// [slot][placement k < kNP][lane] × u64, so a slot's byte offset inside the
+// region is slot·kSlotStride (pre-multiplied in the records) and every access
+// of a warp touches 32 consecutive u64 (conflict-free).  Slots 0..W−1 hold
+// live finish times (liveness-allocated), slot W is the dead slot (values
+// nobody reads), slot W+1 is always zero.
 //
 // Times in the kernel are tagged: value = 8·t + device (t < 2^61), so one
 // slot read yields both a producer's finish time and its device; max over
 // tagged values has the max time in its upper bits (ties differ only in the
-// tag, which is cleared before use).  OpRec.cost8 / EdgeRec.c8 hold 8·cost.
+// tag, which is cleared before use).  cost8 / c8 hold 8·cost.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -25,19 +34,25 @@
 
 namespace pp {
 
+constexpr int kNP = 2;                          // placements per lane
+constexpr uint32_t kSlotStride = 256u * kNP;    // bytes between consecutive slots
+
 struct OpRec {
     uint64_t cost8;       // 8·Δf(p) or 8·Δb(p)
-    uint32_t edge_begin;  // first EdgeRec of this step
-    uint32_t nedge_slot;  // n_edges (bits 0..15) | out_slot (bits 16..31)
+    uint64_t c8;          // 8·c of the first input edge (0 for the zero / self edge)
+    uint32_t src_off;     // region byte offset of the first input's slot
+    uint32_t out_off;     // region byte offset of the output slot
+    uint32_t n_extra;     // further input edges (ExtraRec), consumed in order
+    uint32_t base;        // PERTURB base device of this op (patched every round)
 };
-static_assert(sizeof(OpRec) == 16, "OpRec is 16 B");
+static_assert(sizeof(OpRec) == 32, "OpRec is 32 B");
 
-struct EdgeRec {
-    uint64_t c8;          // 8·c(e) (c = ⌈D·10^12/BW⌉ + L), 0 for a self record
-    uint32_t src_slot;    // slot holding the producer's tagged finish time
+struct ExtraRec {
+    uint64_t c8;          // 8·c(e) (c = ⌈D·10^12/BW⌉ + L)
+    uint32_t src_off;     // region byte offset of the producer's slot
     uint32_t pad;
 };
-static_assert(sizeof(EdgeRec) == 16, "EdgeRec is 16 B");
+static_assert(sizeof(ExtraRec) == 16, "ExtraRec is 16 B");
 
 enum GenKind : int { GEN_GRAY = 0, GEN_RANDOM = 1, GEN_PERTURB = 2, GEN_EXPLICIT = 3 };
 
@@ -48,7 +63,6 @@ constexpr int kMaxSmemBytes = 227 * 1024;
 // Kernel parameters (by value).
 struct KParams {
     const uint8_t *g_image;      // device image (16-B aligned, padded)
-    const uint8_t *g_base;       // PERTURB base, π order, padded to 16 B (device)
     const uint8_t *g_place;      // explicit placements [count][K] (device)
     uint64_t *g_makespan;        // write-all output [end-begin]
     uint64_t *g_partials;        // [grid][2] per-CTA argmin
@@ -57,14 +71,14 @@ struct KParams {
     uint64_t begin, end;         // candidate range
     uint64_t seed;               // seed of this round (RANDOM/PERTURB)
     uint64_t cap;                // memory cap (0 = none)
-    uint32_t image_bytes, base_bytes;
+    uint32_t image_bytes;
     uint32_t K;
-    uint32_t nslot;              // W + 1 (dead slot last)
-    uint32_t off_edges, off_mem, off_orig;
+    uint32_t off_extra, off_mem, off_orig;
     uint32_t tau;
-    uint32_t smem_slots_off;     // byte offset of the per-lane state in smem
-    uint32_t smem_free_off;      // byte offset of per-lane free[M] (M ≥ 3)
-    uint32_t smem_base_off;      // byte offset of the base copy
+    uint32_t smem_slots_off;     // byte offset of the first warp region in smem
+    uint32_t region_bytes;       // bytes per warp region
+    uint32_t free_off;           // region offset of free[M] (M ≥ 3)
+    uint32_t zero_off;           // region offset of the always-zero slot
 };
 
 // Device scalar slots of pp_dfg::d_scalars (u64).
@@ -77,6 +91,7 @@ enum ScalarSlot : int {
 };
 
 struct UParams {
+    uint8_t *image;       // device image: the PERTURB base is patched into OpRec.base
     uint8_t *base;        // PERTURB base, π order (device)
     uint8_t *winner;      // scratch [K]
     uint8_t *best_place;  // [K] best placement so far, π order
@@ -109,7 +124,7 @@ struct pp_dfg {
     std::vector<int32_t> pi;     // π position → descriptor index
     std::vector<int32_t> pos;    // descriptor index → π position
     std::vector<uint8_t> image;  // host copy of the image
-    uint32_t off_edges = 0, off_mem = 0, off_orig = 0, image_bytes = 0;
+    uint32_t off_extra = 0, off_mem = 0, off_orig = 0, image_bytes = 0;
     uint32_t base_bytes = 0;     // K rounded up to 16
     // device memory
     uint8_t *d_image = nullptr;

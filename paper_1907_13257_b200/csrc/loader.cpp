@@ -156,40 +156,41 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
         if (last < 0) continue;   // dead value: written to the dead slot
         int sl = take();
         (fwd ? slot_f : slot_b)[p] = sl;
-        expire[last].push_back(sl);   // freed before the write of step `last`... see below
+        expire[last].push_back(sl);
     }
-    // NOTE: a slot freed "at" step `last` becomes available for the output of
-    // step `last` itself (the kernel reads all inputs of a step before it
-    // writes the output), which is what pushing into expire[last] and
-    // draining expire[s] at the top of step s achieves.
+    // a slot freed at step `last` is reusable for the output of step `last`
+    // itself: the kernel reads all inputs of a step before it writes the output
     const int W = nslots;
-    const int dead = W;
-    if (W + 1 > 65535) return fail(PP_E_TOO_LARGE, "too many live slots");
+    const uint32_t dead_off = (uint32_t)W * kSlotStride, zero_off = (uint32_t)(W + 1) * kSlotStride;
+    if (W + 2 > 4096) return fail(PP_E_TOO_LARGE, "too many live slots");
 
-    // ---- records
+    // ---- records: first input edge inlined in the op record, the rest as extras
     std::vector<OpRec> ops(S);
-    std::vector<EdgeRec> er;
+    std::vector<ExtraRec> xr;
     for (int s = 0; s < S; s++) {
         bool fwd = s < K;
         int p = fwd ? s : S - 1 - s;
         int k = pi[p];
+        std::vector<std::pair<uint64_t, uint32_t>> in;   // (c8, src_off)
+        if (fwd) {
+            for (int e : in_e[p]) in.push_back({8ull * cf[e], (uint32_t)slot_f[pos[src[e]]] * kSlotStride});
+            if (in.empty()) in.push_back({0, zero_off});
+        } else {
+            for (int e : out_e[p]) in.push_back({8ull * cb[e], (uint32_t)slot_b[pos[dst[e]]] * kSlotStride});
+            if (out_e[p].empty()) in.push_back({0, (uint32_t)slot_f[p] * kSlotStride});   // sink: own forward
+        }
         OpRec &o = ops[s];
         o.cost8 = 8ull * (fwd ? d->fwd_ps[k] : d->bwd_ps[k]);
-        o.edge_begin = (uint32_t)er.size();
-        if (fwd) {
-            for (int e : in_e[p]) er.push_back(EdgeRec{8ull * cf[e], (uint32_t)slot_f[pos[src[e]]], 0});
-        } else {
-            for (int e : out_e[p]) er.push_back(EdgeRec{8ull * cb[e], (uint32_t)slot_b[pos[dst[e]]], 0});
-            if (out_e[p].empty()) er.push_back(EdgeRec{0, (uint32_t)slot_f[p], 0});
-        }
-        uint32_t ne = (uint32_t)er.size() - o.edge_begin;
-        if (ne > 65535) return fail(PP_E_TOO_LARGE, "op with more than 65535 edges");
+        o.c8 = in[0].first;
+        o.src_off = in[0].second;
         int out_slot = fwd ? slot_f[p] : slot_b[p];
-        if (out_slot < 0) out_slot = dead;
-        o.nedge_slot = ne | ((uint32_t)out_slot << 16);
+        o.out_off = out_slot < 0 ? dead_off : (uint32_t)out_slot * kSlotStride;
+        o.n_extra = (uint32_t)in.size() - 1;
+        o.base = 0;
+        for (size_t q = 1; q < in.size(); q++) xr.push_back(ExtraRec{in[q].first, in[q].second, 0});
     }
-    size_t off_edges = sizeof(OpRec) * S;
-    size_t off_mem = off_edges + sizeof(EdgeRec) * er.size();
+    size_t off_extra = sizeof(OpRec) * S;
+    size_t off_mem = off_extra + sizeof(ExtraRec) * xr.size();
     size_t off_orig = off_mem + 8ull * K;
     size_t bytes = off_orig + 4ull * K;
     bytes = (bytes + 15) & ~size_t(15);
@@ -209,14 +210,14 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
     g->pos = pos;
     g->image.assign(bytes, 0);
     memcpy(g->image.data(), ops.data(), sizeof(OpRec) * S);
-    if (!er.empty()) memcpy(g->image.data() + off_edges, er.data(), sizeof(EdgeRec) * er.size());
+    if (!xr.empty()) memcpy(g->image.data() + off_extra, xr.data(), sizeof(ExtraRec) * xr.size());
     for (int p = 0; p < K; p++) {
         uint64_t m = d->mem_bytes ? d->mem_bytes[pi[p]] : 0;
         memcpy(g->image.data() + off_mem + 8ull * p, &m, 8);
         uint32_t o = (uint32_t)pi[p];
         memcpy(g->image.data() + off_orig + 4ull * p, &o, 4);
     }
-    g->off_edges = (uint32_t)off_edges;
+    g->off_extra = (uint32_t)off_extra;
     g->off_mem = (uint32_t)off_mem;
     g->off_orig = (uint32_t)off_orig;
     g->image_bytes = (uint32_t)bytes;

@@ -2,11 +2,12 @@
 // forward+backward in-order list schedule of each candidate placement, and
 // the (makespan, index) argmin, for sm_100a.
 //
-// Kernel shape: LANE PER PLACEMENT.  A warp evaluates 32
-// candidate placements in lockstep over the same DFG records, so every record
-// read is a warp-uniform shared-memory broadcast; the only per-lane state is
-// the finish-time slots ([slot][lane] in shared memory, conflict-free) and the
-// per-device free times (registers for M ≤ 2, [device][lane] shared memory
+// Kernel shape: LANE PER PLACEMENT, kNP = 2 placements
+// per lane.  A warp evaluates 64 candidate placements in lockstep over the
+// same DFG records, so every record read is a warp-uniform shared-memory
+// broadcast shared by 64 placements; the per-placement state is the
+// finish-time slots (a per-warp shared region [slot][k][lane], conflict-free)
+// and the per-device free times (registers for M ≤ 2, the warp region
 // otherwise).  The recurrence (PAPER.md:443–453 dependency with Δ_e,
 // :465–476 one op at a time per device, :497–503 back-to-back + overlapped
 // communication; readings R1, R2):
@@ -43,15 +44,16 @@ struct Bits {
 };
 
 // ------------------------------------------------------------- generators
-// Each generator yields the device of π position p, called with p = 0..K−1
-// (forward) and then p = K−1..0 (backward).
+// dev(p, base) yields the device of π position p; it is called with
+// p = 0..K−1 (forward) and then p = K−1..0 (backward).  `base` is the PERTURB
+// base device of p, read from the op record.
 
 template <int M>
 struct GrayGen {                           // O5: reflected M-ary Gray code
     static constexpr int b = Bits<M>::b;
     static constexpr int PF = b ? 64 / b : 64;     // fields per register
-    uint64_t lo, hi;
-    __device__ __forceinline__ void init(uint64_t i, uint32_t K) {
+    uint64_t lo[kNP], hi[kNP];
+    __device__ __forceinline__ static void one(uint64_t i, uint32_t K, uint64_t &lo, uint64_t &hi) {
         lo = hi = 0;
         if (M == 1) return;
         if ((M & (M - 1)) == 0) {
@@ -78,11 +80,18 @@ struct GrayGen {                           // O5: reflected M-ary Gray code
             }
         }
     }
-    __device__ __forceinline__ uint32_t dev(uint32_t p) const {
-        if (M == 1) return 0;
-        uint64_t w = (p < (uint32_t)PF) ? lo : hi;
-        uint32_t sh = (p < (uint32_t)PF) ? p * b : (p - PF) * b;
-        return (uint32_t)(w >> sh) & ((1u << b) - 1);
+    template <int N>
+    __device__ __forceinline__ void init(const uint64_t (&i)[N], uint32_t K) {
+#pragma unroll
+        for (int k = 0; k < N; k++) one(i[k], K, lo[k], hi[k]);
+    }
+    template <int N>
+    __device__ __forceinline__ void devs(uint32_t p, uint32_t, uint32_t (&d)[N]) {
+        const bool first = p < (uint32_t)PF;
+        const uint32_t sh = first ? p * b : (p - PF) * b;
+#pragma unroll
+        for (int k = 0; k < N; k++)
+            d[k] = (M == 1) ? 0u : (uint32_t)((first ? lo[k] : hi[k]) >> sh) & ((1u << b) - 1);
     }
 };
 
@@ -90,27 +99,40 @@ template <int M>
 struct RandomGen {                         // O6 RANDOM
     static constexpr int b = Bits<M>::b;
     static constexpr int P = b ? 64 / b : 64;
-    uint64_t key;       // seed + γ·(i·Wd + 1)
-    uint64_t w;
-    uint32_t cur;
-    bool zero;
-    __device__ __forceinline__ void init(uint64_t i, uint64_t seed, uint32_t K) {
+    uint64_t key[kNP];   // seed + γ·(i·Wd + 1)
+    uint64_t w[kNP];
+    uint64_t keep[kNP];  // 0 for candidate 0 (all zeros), else ~0
+    uint32_t cur;        // word index held in w (shared by the lane's placements)
+    template <int N>
+    __device__ __forceinline__ void init(const uint64_t (&i)[N], uint64_t seed, uint32_t K) {
         const uint64_t Wd = (K + P - 1) / P;
-        key = seed + 0x9E3779B97F4A7C15ull * (i * Wd + 1);
-        zero = (i == 0);
+#pragma unroll
+        for (int k = 0; k < N; k++) {
+            key[k] = seed + 0x9E3779B97F4A7C15ull * (i[k] * Wd + 1);
+            keep[k] = (i[k] == 0) ? 0ull : ~0ull;
+            w[k] = 0;
+        }
         cur = 0xFFFFFFFFu;
-        w = 0;
     }
-    __device__ __forceinline__ uint32_t dev(uint32_t p) {
-        if (M == 1) return 0;
-        uint32_t t = p / P;
+    template <int N>
+    __device__ __forceinline__ void devs(uint32_t p, uint32_t, uint32_t (&d)[N]) {
+        if (M == 1) {
+#pragma unroll
+            for (int k = 0; k < N; k++) d[k] = 0;
+            return;
+        }
+        const uint32_t t = p / P;
         if (t != cur) {   // warp-uniform
             cur = t;
-            w = mix64(key + 0x9E3779B97F4A7C15ull * t);
+#pragma unroll
+            for (int k = 0; k < N; k++) w[k] = mix64(key[k] + 0x9E3779B97F4A7C15ull * t) & keep[k];
         }
-        uint32_t x = (uint32_t)(w >> (b * (p - t * P))) & ((1u << b) - 1);
-        uint32_t d = (x * M) >> b;
-        return zero ? 0u : d;
+        const uint32_t sh = b * (p - t * P);
+#pragma unroll
+        for (int k = 0; k < N; k++) {
+            const uint32_t x = (uint32_t)(w[k] >> sh) & ((1u << b) - 1);
+            d[k] = ((M & (M - 1)) == 0) ? x : (x * M) >> b;
+        }
     }
 };
 
@@ -119,40 +141,85 @@ struct PerturbGen {                        // O6 PERTURB
     static constexpr int b = Bits<M>::b;
     static constexpr int FB = 8 + b;
     static constexpr int P = 64 / FB;
-    uint64_t key;
-    uint64_t w;
+    uint64_t key[kNP];
+    uint64_t w[kNP];
+    uint32_t tau[kNP];   // 0 for candidate 0 (the base itself)
     uint32_t cur;
-    uint32_t tau;       // 0 for candidate 0 (the base itself)
-    const uint8_t *base;
-    __device__ __forceinline__ void init(uint64_t i, uint64_t seed, uint32_t K, uint32_t tau_,
-                                         const uint8_t *base_) {
+    template <int N>
+    __device__ __forceinline__ void init(const uint64_t (&i)[N], uint64_t seed, uint32_t K, uint32_t tau_) {
         const uint64_t Wd = (K + P - 1) / P;
-        key = (seed ^ 0xD1B54A32D192ED03ull) + 0x9E3779B97F4A7C15ull * (i * Wd + 1);
-        tau = (i == 0) ? 0u : tau_;
+#pragma unroll
+        for (int k = 0; k < N; k++) {
+            key[k] = (seed ^ 0xD1B54A32D192ED03ull) + 0x9E3779B97F4A7C15ull * (i[k] * Wd + 1);
+            tau[k] = (i[k] == 0) ? 0u : tau_;
+            w[k] = 0;
+        }
         cur = 0xFFFFFFFFu;
-        w = 0;
-        base = base_;
     }
-    __device__ __forceinline__ uint32_t dev(uint32_t p) {
-        uint32_t bs = base[p];   // uniform broadcast
-        if (M == 1) return 0;
-        uint32_t t = p / P;
+    template <int N>
+    __device__ __forceinline__ void devs(uint32_t p, uint32_t bs, uint32_t (&d)[N]) {
+        if (M == 1) {
+#pragma unroll
+            for (int k = 0; k < N; k++) d[k] = 0;
+            return;
+        }
+        const uint32_t t = p / P;
         if (t != cur) {
             cur = t;
-            w = mix64(key + 0x9E3779B97F4A7C15ull * t);
+#pragma unroll
+            for (int k = 0; k < N; k++) w[k] = mix64(key[k] + 0x9E3779B97F4A7C15ull * t);
         }
-        uint32_t f = (uint32_t)(w >> (FB * (p - t * P))) & ((1u << FB) - 1);
-        uint32_t u = f & 0xFF, y = f >> 8;
-        uint32_t flip = (bs + 1 + (M > 1 ? y % (uint32_t)(M > 1 ? M - 1 : 1) : 0)) % (uint32_t)M;
-        return (u >= tau) ? bs : flip;
+        const uint32_t sh = FB * (p - t * P);
+#pragma unroll
+        for (int k = 0; k < N; k++) {
+            const uint32_t f = (uint32_t)(w[k] >> sh) & ((1u << FB) - 1);
+            uint32_t flip;
+            if (M == 2) flip = bs ^ 1u;
+            else flip = (bs + 1 + (f >> 8) % (uint32_t)(M > 1 ? M - 1 : 1)) % (uint32_t)M;
+            d[k] = ((f & 0xFF) >= tau[k]) ? bs : flip;
+        }
     }
 };
 
 struct ExplicitGen {                       // rows of a [count][K] uint8 array
-    const uint8_t *row;
+    const uint8_t *row[kNP];
     const uint32_t *orig;
-    __device__ __forceinline__ uint32_t dev(uint32_t p) const { return row[orig[p]]; }
+    template <int N>
+    __device__ __forceinline__ void devs(uint32_t p, uint32_t, uint32_t (&d)[N]) const {
+        const uint32_t o = orig[p];
+#pragma unroll
+        for (int k = 0; k < N; k++) d[k] = row[k][o];
+    }
 };
+
+__device__ __forceinline__ uint64_t u64max(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+// 32-bit shared-window addressing (kept in program order: volatile)
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint64_t v) {
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+// v + (tag(v) ≠ dev ? c : 0): the cut-edge charge as two predicated adds
+__device__ __forceinline__ uint64_t add_if_cut(uint64_t v, uint32_t dev, uint64_t c) {
+    uint64_t t;
+    asm("{\n .reg .pred p;\n .reg .b32 x, lo, hi, clo, chi;\n"
+        " mov.b64 {lo, hi}, %1;\n mov.b64 {clo, chi}, %3;\n"
+        " xor.b32 x, lo, %2;\n and.b32 x, x, 7;\n setp.ne.u32 p, x, 0;\n"
+        " @p add.cc.u32 lo, lo, clo;\n @p addc.u32 hi, hi, chi;\n"
+        " mov.b64 %0, {lo, hi};\n}"
+        : "=l"(t)
+        : "l"(v), "r"(dev), "l"(c));
+    return t;
+}
 
 // ------------------------------------------------------ per-device state
 template <int M, bool SMEM>
@@ -161,7 +228,7 @@ struct FreeTimes;
 template <int M>
 struct FreeTimes<M, false> {               // registers, select chains (M ≤ 2)
     uint64_t f[M];
-    __device__ __forceinline__ void init(uint64_t *, uint32_t) {
+    __device__ __forceinline__ void init(uint32_t) {
 #pragma unroll
         for (int d = 0; d < M; d++) f[d] = 0;
     }
@@ -184,21 +251,19 @@ struct FreeTimes<M, false> {               // registers, select chains (M ≤ 2)
 };
 
 template <int M>
-struct FreeTimes<M, true> {                // shared memory [device][lane] (M ≥ 3)
-    uint64_t *f;
-    uint32_t stride;
-    __device__ __forceinline__ void init(uint64_t *base, uint32_t s) {
+struct FreeTimes<M, true> {                // warp region [device][k][lane] (M ≥ 3)
+    uint32_t f;                            // shared address of this lane's / placement's device-0 entry
+    __device__ __forceinline__ void init(uint32_t base) {
         f = base;
-        stride = s;
 #pragma unroll
-        for (int d = 0; d < M; d++) f[d * stride] = 0;
+        for (int d = 0; d < M; d++) sts64(f + d * kSlotStride, 0);
     }
-    __device__ __forceinline__ uint64_t get(uint32_t dev) const { return f[dev * stride]; }
-    __device__ __forceinline__ void set(uint32_t dev, uint64_t v) { f[dev * stride] = v; }
+    __device__ __forceinline__ uint64_t get(uint32_t dev) const { return lds64(f + dev * kSlotStride); }
+    __device__ __forceinline__ void set(uint32_t dev, uint64_t v) { sts64(f + dev * kSlotStride, v); }
     __device__ __forceinline__ uint64_t max_all() const {
-        uint64_t v = f[0];
+        uint64_t v = 0;
 #pragma unroll
-        for (int d = 1; d < M; d++) v = f[d * stride] > v ? f[d * stride] : v;
+        for (int d = 0; d < M; d++) v = u64max(v, lds64(f + d * kSlotStride));
         return v;
     }
 };
@@ -214,7 +279,6 @@ struct MemUse {
 #pragma unroll
         for (int d = 0; d < M; d++) u[d] += (dev == (uint32_t)d) ? m : 0;
     }
-    // Σ over a device may exceed 2^64 only if Σ M(k) does; saturate
     __device__ __forceinline__ bool over(uint64_t cap) const {
         bool o = false;
 #pragma unroll
@@ -223,47 +287,59 @@ struct MemUse {
     }
 };
 
-// --------------------------------------------------------- one placement
-// Evaluates the schedule of the placement produced by `gen` for this lane.
+// -------------------------------------------------- kNP placements per lane
+// lane: shared address of this lane's entry in its warp region (region +
+// 8·lane); placement k's copy of a slot is at +k·256.
 template <int M, bool MEM, class Gen>
-__device__ __forceinline__ uint64_t schedule_one(Gen &gen, const OpRec *__restrict__ ops,
-                                                 const EdgeRec *__restrict__ er,
-                                                 const uint64_t *__restrict__ mem, uint64_t *slots,
-                                                 uint32_t stride, uint64_t *free_base, uint32_t K,
-                                                 uint64_t cap) {
+__device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
+                                            const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
+                                            uint32_t K, uint64_t cap) {
     constexpr bool FREE_SMEM = (M > 2);
-    FreeTimes<M, FREE_SMEM> fr;
-    fr.init(free_base, stride);
-    MemUse<M> mu;
-    if (MEM) mu.init();
-
-    auto step = [&](uint32_t s, uint32_t p) {
-        const OpRec op = ops[s];
-        const uint32_t dev = gen.dev(p);
-        uint64_t r = 0;
-        const uint32_t ne = op.nedge_slot & 0xFFFFu;
-        const EdgeRec *e = er + op.edge_begin;
-        for (uint32_t q = 0; q < ne; q++) {
-            const EdgeRec rec = e[q];
-            const uint64_t v = slots[rec.src_slot * stride];
-            const uint64_t t = v + ((((uint32_t)v & 7u) != dev) ? rec.c8 : 0ull);
-            r = t > r ? t : r;
-        }
-        const uint64_t f = fr.get(dev);
-        const uint64_t st = r > f ? r : f;
-        const uint64_t fin = ((st & ~7ull) | dev) + op.cost8;
-        slots[(op.nedge_slot >> 16) * stride] = fin;
-        fr.set(dev, fin);
-        return dev;
-    };
-    for (uint32_t p = 0; p < K; p++) {
-        uint32_t dev = step(p, p);
-        if (MEM) mu.add(dev, mem[p]);
+    FreeTimes<M, FREE_SMEM> fr[kNP];
+    MemUse<M> mu[kNP];
+#pragma unroll
+    for (int k = 0; k < kNP; k++) {
+        fr[k].init(lane + free_off + k * 256);
+        if (MEM) mu[k].init();
     }
-    for (uint32_t p = K; p-- > 0;) step(2 * K - 1 - p, p);
-    uint64_t mk = fr.max_all() >> 3;
-    if (MEM && mu.over(cap)) mk = kInfeasible;
-    return mk;
+    uint32_t op = ops;
+    uint32_t x = xr;
+
+    auto step = [&](uint32_t p, bool fwd) {
+        const uint4 a = lds128(op);
+        const uint4 b = lds128(op + 16);
+        op += sizeof(OpRec);
+        const uint64_t cost8 = ((uint64_t)a.y << 32) | a.x;
+        const uint64_t c8 = ((uint64_t)a.w << 32) | a.z;
+        uint32_t dev[kNP];
+        uint64_t r[kNP];
+        gen.devs(p, b.w, dev);
+#pragma unroll
+        for (int k = 0; k < kNP; k++) r[k] = add_if_cut(lds64(lane + b.x + k * 256), dev[k], c8);
+#pragma unroll 1
+        for (uint32_t q = 0; q < b.z; q++) {   // further inputs (uniform trip count)
+            const uint4 e = lds128(x);
+            x += sizeof(ExtraRec);
+            const uint64_t ce = ((uint64_t)e.y << 32) | e.x;
+#pragma unroll
+            for (int k = 0; k < kNP; k++) r[k] = u64max(r[k], add_if_cut(lds64(lane + e.z + k * 256), dev[k], ce));
+        }
+#pragma unroll
+        for (int k = 0; k < kNP; k++) {
+            const uint64_t s = u64max(r[k], fr[k].get(dev[k]));
+            const uint64_t fin = ((s & ~7ull) | dev[k]) + cost8;
+            sts64(lane + b.y + k * 256, fin);
+            fr[k].set(dev[k], fin);
+            if (MEM && fwd) mu[k].add(dev[k], mem[p]);
+        }
+    };
+    for (uint32_t p = 0; p < K; p++) step(p, true);
+    for (uint32_t p = K; p-- > 0;) step(p, false);
+#pragma unroll
+    for (int k = 0; k < kNP; k++) {
+        mk[k] = fr[k].max_all() >> 3;
+        if (MEM && mu[k].over(cap)) mk[k] = kInfeasible;
+    }
 }
 
 __device__ __forceinline__ bool lex_less(uint64_t m1, uint64_t i1, uint64_t m2, uint64_t i2) {
@@ -282,7 +358,7 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams P) {
     const uint32_t lane = tid & 31, warp = tid >> 5;
     const uint32_t nthreads = blockDim.x;
 
-    // ---- stage the image (and the PERTURB base) with bulk TMA copies
+    // ---- stage the image with bulk TMA copies completing on one mbarrier
     const uint32_t mbar_addr = (uint32_t)__cvta_generic_to_shared(&mbar);
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_addr));
@@ -290,8 +366,7 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams P) {
     }
     __syncthreads();
     if (tid == 0) {
-        uint32_t total = P.image_bytes + ((GEN == GEN_PERTURB) ? P.base_bytes : 0);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_addr), "r"(total)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_addr), "r"(P.image_bytes)
                      : "memory");
         const uint32_t chunk = 32768;
         for (uint32_t off = 0; off < P.image_bytes; off += chunk) {
@@ -302,14 +377,12 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams P) {
                 "l"(P.g_image + off), "r"(n), "r"(mbar_addr)
                 : "memory");
         }
-        if (GEN == GEN_PERTURB) {
-            uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem + P.smem_base_off);
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                "l"(P.g_base), "r"(P.base_bytes), "r"(mbar_addr)
-                : "memory");
-        }
     }
+    // this lane's state; the always-zero slot is never written again
+    const uint32_t smem_base = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t lane_region = smem_base + P.smem_slots_off + warp * P.region_bytes + lane * 8;
+#pragma unroll
+    for (int k = 0; k < kNP; k++) sts64(lane_region + P.zero_off + k * 256, 0);
     {
         uint32_t done = 0;
         while (!done) {
@@ -321,48 +394,55 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams P) {
         }
     }
 
-    const OpRec *ops = reinterpret_cast<const OpRec *>(smem);
-    const EdgeRec *er = reinterpret_cast<const EdgeRec *>(smem + P.off_edges);
+    const uint32_t ops = smem_base;
+    const uint32_t xr = smem_base + P.off_extra;
     const uint64_t *mem = reinterpret_cast<const uint64_t *>(smem + P.off_mem);
     const uint32_t *orig = reinterpret_cast<const uint32_t *>(smem + P.off_orig);
-    uint64_t *slots = reinterpret_cast<uint64_t *>(smem + P.smem_slots_off) + tid;
-    uint64_t *free_base = reinterpret_cast<uint64_t *>(smem + P.smem_free_off) + tid;
-    const uint8_t *base = smem + P.smem_base_off;
 
     uint64_t best_mk = kInfeasible, best_i = kInfeasible;
     bool have = false;
     const uint64_t n = P.end - P.begin;
-    const uint64_t ntiles = (n + 31) >> 5;
+    constexpr uint32_t TILE = 32 * kNP;
+    const uint64_t ntiles = (n + TILE - 1) / TILE;
     const uint64_t wpb = nthreads >> 5;
     for (uint64_t tile = blockIdx.x * wpb + warp; tile < ntiles; tile += (uint64_t)gridDim.x * wpb) {
-        const uint64_t off = (tile << 5) + lane;
-        const bool valid = off < n;
-        const uint64_t i = P.begin + (valid ? off : n - 1);
-        uint64_t mk;
+        uint64_t off[kNP], idx[kNP];
+        bool valid[kNP];
+#pragma unroll
+        for (int k = 0; k < kNP; k++) {
+            off[k] = tile * TILE + k * 32 + lane;
+            valid[k] = off[k] < n;
+            idx[k] = P.begin + (valid[k] ? off[k] : n - 1);
+        }
+        uint64_t mk[kNP];
         if (GEN == GEN_GRAY) {
             GrayGen<M> g;
-            g.init(i, P.K);
-            mk = schedule_one<M, MEM>(g, ops, er, mem, slots, nthreads, free_base, P.K, P.cap);
+            g.init(idx, P.K);
+            schedule_np<M, MEM>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap);
         } else if (GEN == GEN_RANDOM) {
             RandomGen<M> g;
-            g.init(i, P.seed, P.K);
-            mk = schedule_one<M, MEM>(g, ops, er, mem, slots, nthreads, free_base, P.K, P.cap);
+            g.init(idx, P.seed, P.K);
+            schedule_np<M, MEM>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap);
         } else if (GEN == GEN_PERTURB) {
             PerturbGen<M> g;
-            g.init(i, P.seed, P.K, P.tau, base);
-            mk = schedule_one<M, MEM>(g, ops, er, mem, slots, nthreads, free_base, P.K, P.cap);
+            g.init(idx, P.seed, P.K, P.tau);
+            schedule_np<M, MEM>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap);
         } else {
             ExplicitGen g;
-            g.row = P.g_place + (i - P.begin) * (uint64_t)P.K;
+#pragma unroll
+            for (int k = 0; k < kNP; k++) g.row[k] = P.g_place + (idx[k] - P.begin) * (uint64_t)P.K;
             g.orig = orig;
-            mk = schedule_one<M, MEM>(g, ops, er, mem, slots, nthreads, free_base, P.K, P.cap);
+            schedule_np<M, MEM>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap);
         }
-        if (WRITE_ALL) {
-            if (valid) P.g_makespan[off] = mk;
-        } else if (valid && (!have || lex_less(mk, i, best_mk, best_i))) {
-            best_mk = mk;
-            best_i = i;
-            have = true;
+#pragma unroll
+        for (int k = 0; k < kNP; k++) {
+            if (WRITE_ALL) {
+                if (valid[k]) P.g_makespan[off[k]] = mk[k];
+            } else if (valid[k] && (!have || lex_less(mk[k], idx[k], best_mk, best_i))) {
+                best_mk = mk[k];
+                best_i = idx[k];
+                have = true;
+            }
         }
     }
     if (WRITE_ALL) return;
@@ -416,7 +496,8 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams P) {
 // GPU, or the NCCL-reduced key/index on several — regenerates its placement,
 // keeps the overall best (first round reaching the minimum) and moves the
 // PERTURB base to the winner (candidate 0 is the base, so the winner differs
-// from the base only when it is strictly better).
+// from the base only when it is strictly better), patching
+// the new base into the op records of the device image.
 template <int M, int GEN>
 __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
     __shared__ uint64_t mk_s, idx_s;
@@ -440,26 +521,32 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
     __syncthreads();
     const uint64_t idx = idx_s;
     for (uint32_t p = threadIdx.x; p < U.K; p += blockDim.x) {
-        uint32_t d;
+        const uint64_t ii[1] = {idx};
+        uint32_t d[1];
         if (GEN == GEN_GRAY) {
             GrayGen<M> g;
-            g.init(idx, U.K);
-            d = g.dev(p);
+            g.init(ii, U.K);
+            g.devs(p, 0, d);
         } else if (GEN == GEN_RANDOM) {
             RandomGen<M> g;
-            g.init(idx, U.seed, U.K);
-            d = g.dev(p);
+            g.init(ii, U.seed, U.K);
+            g.devs(p, 0, d);
         } else {
             PerturbGen<M> g;
-            g.init(idx, U.seed, U.K, U.tau, U.base);
-            d = g.dev(p);
+            g.init(ii, U.seed, U.K, U.tau);
+            g.devs(p, U.base[p], d);
         }
-        U.winner[p] = (uint8_t)d;
+        U.winner[p] = (uint8_t)d[0];
     }
     __syncthreads();
+    OpRec *ops = reinterpret_cast<OpRec *>(U.image);
     for (uint32_t p = threadIdx.x; p < U.K; p += blockDim.x) {
         uint8_t d = U.winner[p];
-        if (GEN == GEN_PERTURB) U.base[p] = d;
+        if (GEN == GEN_PERTURB) {
+            U.base[p] = d;
+            ops[p].base = d;
+            ops[2 * U.K - 1 - p].base = d;
+        }
         if (improve) U.best_place[p] = d;
     }
     if (threadIdx.x == 0 && improve) {
@@ -469,15 +556,15 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
     }
 }
 
-template <int M, int GEN>
-int launch_update(const UParams &u, void *stream) {
-    round_update_kernel<M, GEN><<<1, 256, 0, (cudaStream_t)stream>>>(u);
-    return (int)cudaGetLastError();
-}
-
 template <int M, int GEN, bool MEM, bool WRITE_ALL>
 int launch_search(const KParams &p, int grid, int threads, int smem, void *stream) {
     search_kernel<M, GEN, MEM, WRITE_ALL><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
+    return (int)cudaGetLastError();
+}
+
+template <int M, int GEN>
+int launch_update(const UParams &u, void *stream) {
+    round_update_kernel<M, GEN><<<1, 256, 0, (cudaStream_t)stream>>>(u);
     return (int)cudaGetLastError();
 }
 
