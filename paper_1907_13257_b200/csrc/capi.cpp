@@ -26,21 +26,21 @@ void note_launch() { g_launches++; }
 
 int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp_dfg **out);
 
-#define PP_DECL_M(m)                                        \
-    KernelInfo kernel_for_m##m(int gen, bool mem, bool wa); \
+#define PP_DECL_M(m)                                                  \
+    KernelInfo kernel_for_m##m(int gen, bool mem, bool wa, bool f64); \
     UpdateFn update_for_m##m(int gen);
 PP_DECL_M(1) PP_DECL_M(2) PP_DECL_M(3) PP_DECL_M(4) PP_DECL_M(5) PP_DECL_M(6) PP_DECL_M(7) PP_DECL_M(8)
 
-KernelInfo kernel_for(int M, int gen, bool mem, bool wa) {
+KernelInfo kernel_for(int M, int gen, bool mem, bool wa, bool f64) {
     switch (M) {
-        case 1: return kernel_for_m1(gen, mem, wa);
-        case 2: return kernel_for_m2(gen, mem, wa);
-        case 3: return kernel_for_m3(gen, mem, wa);
-        case 4: return kernel_for_m4(gen, mem, wa);
-        case 5: return kernel_for_m5(gen, mem, wa);
-        case 6: return kernel_for_m6(gen, mem, wa);
-        case 7: return kernel_for_m7(gen, mem, wa);
-        default: return kernel_for_m8(gen, mem, wa);
+        case 1: return kernel_for_m1(gen, mem, wa, f64);
+        case 2: return kernel_for_m2(gen, mem, wa, f64);
+        case 3: return kernel_for_m3(gen, mem, wa, f64);
+        case 4: return kernel_for_m4(gen, mem, wa, f64);
+        case 5: return kernel_for_m5(gen, mem, wa, f64);
+        case 6: return kernel_for_m6(gen, mem, wa, f64);
+        case 7: return kernel_for_m7(gen, mem, wa, f64);
+        default: return kernel_for_m8(gen, mem, wa, f64);
     }
 }
 UpdateFn update_for(int M, int gen) {
@@ -93,21 +93,27 @@ struct Launch {
 // the dynamic shared memory layout and a grid of (resident CTAs per SM) × SMs.
 static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin, uint64_t end, Launch &L) {
     const bool mem = g->cap > 0;
-    L.k = kernel_for(M, gen, mem, write_all);
-    const uint32_t nslot = (uint32_t)g->W + 2;                  // live + dead + zero
+    L.k = kernel_for(M, gen, mem, write_all, g->f64);
+    const uint32_t nslot = (uint32_t)g->W + 1;                  // live + zero
     const uint32_t region = (nslot + (M > 2 ? (uint32_t)M : 0u)) * kSlotStride;
     const uint32_t slots_off = (g->image_bytes + 127) & ~127u;
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, L.k.func);
+    if (e != cudaSuccess) return cuda_err(e, "cudaFuncGetAttributes");
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device);
+    const size_t max_dyn = (size_t)std::min<int>(optin, kMaxSmemBytes) - fa.sharedSizeBytes - 1024;
     int threads = 256;
     size_t smem = 0;
     for (; threads >= 32; threads >>= 1) {
         smem = slots_off + (size_t)(threads / 32) * region;
-        if (smem <= (size_t)kMaxSmemBytes) break;
+        if (smem <= max_dyn) break;
     }
     if (threads < 32) {
         set_error("per-lane schedule state does not fit in shared memory");
         return PP_E_TOO_LARGE;
     }
-    cudaError_t e = cudaFuncSetAttribute(L.k.func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(L.k.func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.k.func, threads, smem);
@@ -135,7 +141,8 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
     p.smem_slots_off = slots_off;
     p.region_bytes = region;
     p.free_off = nslot * kSlotStride;
-    p.zero_off = (uint32_t)(g->W + 1) * kSlotStride;
+    p.zero_off = (uint32_t)g->W * kSlotStride;
+    p.one = 1.0;
     p.g_partials = g->d_partials;
     p.g_ticket = g->d_ticket;
     p.g_out = g->d_scalars + SC_LOCAL_MK;

@@ -18,13 +18,19 @@
 // [slot][placement k < kNP][lane] × u64, so a slot's byte offset inside the
 // region is slot·kSlotStride (pre-multiplied in the records) and every access
 // of a warp touches 32 consecutive u64 (conflict-free).  Slots 0..W−1 hold
-// live finish times (liveness-allocated), slot W is the dead slot (values
-// nobody reads), slot W+1 is always zero.
+// live finish times (liveness-allocated), slot W is always zero.  An input
+// produced by the immediately preceding step is forwarded in a register
+// (kFromPrev) and a value that no later step reads from a slot is not stored.
 //
-// Times in the kernel are tagged: value = 8·t + device (t < 2^61), so one
-// slot read yields both a producer's finish time and its device; max over
-// tagged values has the max time in its upper bits (ties differ only in the
-// tag, which is cleared before use).  cost8 / c8 hold 8·cost.
+// Times in the kernel are TAGGED with the producer's device, so one slot read
+// yields both a finish time and its device:
+//   u64 arithmetic: value = 8·t + device (t < 2^61);
+//   f64 arithmetic (all times < 2^49): value = the double t with the device in
+//   its 3 low mantissa bits, i.e. t + device·ulp(t) — integers below 2^49 have
+//   those bits clear, adds of integers stay exact, and the tag never reaches
+//   the integer part.
+// A max over tagged values has the max time in its integer part (ties differ
+// only in the tag, which is cleared before use).
 #pragma once
 #include <cstdint>
 #include <string>
@@ -37,11 +43,16 @@ namespace pp {
 constexpr int kNP = 2;                          // placements per lane
 constexpr uint32_t kSlotStride = 256u * kNP;    // bytes between consecutive slots
 
+constexpr uint32_t kFromPrev = 0xFFFFFFFFu;     // OpRec.src_off: previous step's output (register)
+constexpr uint32_t kNoStore = 0xFFFFFFFFu;      // OpRec.out_off: output never read from a slot
+
+// cost8 / c8 / ExtraRec.c8 hold the ENCODED cost: 8·ps for the tagged-u64
+// arithmetic, the bits of (double)ps for the tagged-f64 arithmetic.
 struct OpRec {
-    uint64_t cost8;       // 8·Δf(p) or 8·Δb(p)
-    uint64_t c8;          // 8·c of the first input edge (0 for the zero / self edge)
-    uint32_t src_off;     // region byte offset of the first input's slot
-    uint32_t out_off;     // region byte offset of the output slot
+    uint64_t cost8;       // encoded Δf(p) or Δb(p)
+    uint64_t c8;          // encoded c of the first input edge (0 for the zero / self edge)
+    uint32_t src_off;     // region byte offset of the first input's slot, or kFromPrev
+    uint32_t out_off;     // region byte offset of the output slot, or kNoStore
     uint32_t n_extra;     // further input edges (ExtraRec), consumed in order
     uint32_t base;        // PERTURB base device of this op (patched every round)
 };
@@ -79,6 +90,7 @@ struct KParams {
     uint32_t region_bytes;       // bytes per warp region
     uint32_t free_off;           // region offset of free[M] (M ≥ 3)
     uint32_t zero_off;           // region offset of the always-zero slot
+    double one;                  // 1.0, opaque to the compiler (f64 predicated moves)
 };
 
 // Device scalar slots of pp_dfg::d_scalars (u64).
@@ -112,7 +124,7 @@ struct KernelInfo {
 };
 
 // search_inst.cu (compiled once per M with -DPP_M): kernel_for_m<M>(...)
-KernelInfo kernel_for(int M, int gen, bool mem, bool write_all);
+KernelInfo kernel_for(int M, int gen, bool mem, bool write_all, bool f64);
 UpdateFn update_for(int M, int gen);
 
 }  // namespace pp
@@ -120,6 +132,7 @@ UpdateFn update_for(int M, int gen);
 struct pp_dfg {
     int device = 0;
     int K = 0, E = 0, W = 0;
+    bool f64 = false;            // tagged-f64 arithmetic (bound < 2^49) else tagged-u64
     uint64_t t1 = 0, grad_bytes = 0, cap = 0;
     std::vector<int32_t> pi;     // π position → descriptor index
     std::vector<int32_t> pos;    // descriptor index → π position

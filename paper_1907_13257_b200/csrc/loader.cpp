@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <queue>
 #include <unordered_set>
@@ -123,71 +124,100 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
         out_e[pos[src[e]]].push_back(e);
     }
 
-    // ---- liveness: value F(p) produced at step p, B(p) at step 2K−1−p
+    // ---- inputs of every step.  Value ids: step s produces value s (forward
+    // finish time of p = s, or backward finish time of p = 2K−1−s); −1 = zero.
     const int S = 2 * K;
-    std::vector<int> last_f(K, -1), last_b(K, -1);
-    for (int e = 0; e < E; e++) {
-        int u = pos[src[e]], v = pos[dst[e]];
-        last_f[u] = std::max(last_f[u], v);             // forward consumer at step v
-        last_b[v] = std::max(last_b[v], S - 1 - u);     // backward of u reads B(v)
+    std::vector<std::vector<std::pair<int, uint64_t>>> inputs(S);   // (value id, cost ps)
+    for (int s = 0; s < S; s++) {
+        const bool fwd = s < K;
+        const int p = fwd ? s : S - 1 - s;
+        auto &in = inputs[s];
+        if (fwd) {
+            for (int e : in_e[p]) in.push_back({pos[src[e]], cf[e]});
+            if (in.empty()) in.push_back({-1, 0});
+        } else {
+            for (int e : out_e[p]) in.push_back({S - 1 - pos[dst[e]], cb[e]});
+            if (out_e[p].empty()) in.push_back({p, 0});   // sink: waits for its own forward (R1)
+        }
     }
-    for (int p = 0; p < K; p++)
-        if (out_e[p].empty()) last_f[p] = std::max(last_f[p], S - 1 - p);   // sink self record
-    // linear-scan allocation in step order; reads happen before the write
-    std::vector<int> slot_f(K, -1), slot_b(K, -1);
-    std::vector<std::vector<int>> expire(S);   // slots freed after step s
+    // register forwarding: an input produced by the previous step goes first
+    // and is read from a register instead of shared memory
+    std::vector<char> fwd_first(S, 0);
+    for (int s = 1; s < S; s++) {
+        auto &in = inputs[s];
+        for (size_t j = 0; j < in.size(); j++)
+            if (in[j].first == s - 1) {
+                std::swap(in[0], in[j]);
+                fwd_first[s] = 1;
+                break;
+            }
+    }
+    // liveness over the remaining (shared-memory) reads
+    std::vector<int> last(S, -1);
+    for (int s = 0; s < S; s++)
+        for (size_t j = 0; j < inputs[s].size(); j++) {
+            const int v = inputs[s][j].first;
+            if (v < 0 || (j == 0 && fwd_first[s])) continue;
+            last[v] = std::max(last[v], s);
+        }
+    // linear-scan slot allocation in step order; a slot whose value is last
+    // read at step s is reusable for the output of step s itself (the kernel
+    // reads all inputs of a step before it writes the output)
+    std::vector<int> slot(S, -1);
+    std::vector<std::vector<int>> expire(S);
     std::vector<int> free_slots;               // min-heap of free slot ids
     int nslots = 0;
-    auto take = [&]() {
-        if (free_slots.empty()) return nslots++;
-        std::pop_heap(free_slots.begin(), free_slots.end(), std::greater<int>());
-        int s = free_slots.back();
-        free_slots.pop_back();
-        return s;
-    };
     for (int s = 0; s < S; s++) {
         for (int sl : expire[s]) {
             free_slots.push_back(sl);
             std::push_heap(free_slots.begin(), free_slots.end(), std::greater<int>());
         }
-        bool fwd = s < K;
-        int p = fwd ? s : S - 1 - s;
-        int last = fwd ? last_f[p] : last_b[p];
-        if (last < 0) continue;   // dead value: written to the dead slot
-        int sl = take();
-        (fwd ? slot_f : slot_b)[p] = sl;
-        expire[last].push_back(sl);
+        if (last[s] < 0) continue;             // never read from shared memory: no store
+        int sl;
+        if (free_slots.empty()) sl = nslots++;
+        else {
+            std::pop_heap(free_slots.begin(), free_slots.end(), std::greater<int>());
+            sl = free_slots.back();
+            free_slots.pop_back();
+        }
+        slot[s] = sl;
+        expire[last[s]].push_back(sl);
     }
-    // a slot freed at step `last` is reusable for the output of step `last`
-    // itself: the kernel reads all inputs of a step before it writes the output
     const int W = nslots;
-    const uint32_t dead_off = (uint32_t)W * kSlotStride, zero_off = (uint32_t)(W + 1) * kSlotStride;
-    if (W + 2 > 4096) return fail(PP_E_TOO_LARGE, "too many live slots");
+    const uint32_t zero_off = (uint32_t)W * kSlotStride;   // slot W always holds 0
+    if (W + 1 > 4096) return fail(PP_E_TOO_LARGE, "too many live slots");
 
-    // ---- records: first input edge inlined in the op record, the rest as extras
+    // ---- arithmetic: exact integer ps in doubles when every time is < 2^49
+    // (device tag in the 3 low mantissa bits), else tagged u64 (8·t + device)
+    bool f64 = (bound >> 49) == 0;
+    if (const char *a = getenv("PP_ARITH")) {
+        if (!strcmp(a, "int64")) f64 = false;
+    }
+    auto enc = [&](uint64_t ps) -> uint64_t {
+        if (!f64) return 8ull * ps;
+        double x = (double)ps;   // exact: ps < 2^49
+        uint64_t bits;
+        memcpy(&bits, &x, 8);
+        return bits;
+    };
+
+    // ---- records: first input inlined in the op record, the rest as extras
     std::vector<OpRec> ops(S);
     std::vector<ExtraRec> xr;
+    auto src_off = [&](int v) -> uint32_t { return v < 0 ? zero_off : (uint32_t)slot[v] * kSlotStride; };
     for (int s = 0; s < S; s++) {
-        bool fwd = s < K;
-        int p = fwd ? s : S - 1 - s;
-        int k = pi[p];
-        std::vector<std::pair<uint64_t, uint32_t>> in;   // (c8, src_off)
-        if (fwd) {
-            for (int e : in_e[p]) in.push_back({8ull * cf[e], (uint32_t)slot_f[pos[src[e]]] * kSlotStride});
-            if (in.empty()) in.push_back({0, zero_off});
-        } else {
-            for (int e : out_e[p]) in.push_back({8ull * cb[e], (uint32_t)slot_b[pos[dst[e]]] * kSlotStride});
-            if (out_e[p].empty()) in.push_back({0, (uint32_t)slot_f[p] * kSlotStride});   // sink: own forward
-        }
+        const bool fwd = s < K;
+        const int p = fwd ? s : S - 1 - s;
+        const int k = pi[p];
+        const auto &in = inputs[s];
         OpRec &o = ops[s];
-        o.cost8 = 8ull * (fwd ? d->fwd_ps[k] : d->bwd_ps[k]);
-        o.c8 = in[0].first;
-        o.src_off = in[0].second;
-        int out_slot = fwd ? slot_f[p] : slot_b[p];
-        o.out_off = out_slot < 0 ? dead_off : (uint32_t)out_slot * kSlotStride;
+        o.cost8 = enc(fwd ? d->fwd_ps[k] : d->bwd_ps[k]);
+        o.c8 = enc(in[0].second);
+        o.src_off = fwd_first[s] ? kFromPrev : src_off(in[0].first);
+        o.out_off = slot[s] < 0 ? kNoStore : (uint32_t)slot[s] * kSlotStride;
         o.n_extra = (uint32_t)in.size() - 1;
         o.base = 0;
-        for (size_t q = 1; q < in.size(); q++) xr.push_back(ExtraRec{in[q].first, in[q].second, 0});
+        for (size_t q = 1; q < in.size(); q++) xr.push_back(ExtraRec{enc(in[q].second), src_off(in[q].first), 0});
     }
     size_t off_extra = sizeof(OpRec) * S;
     size_t off_mem = off_extra + sizeof(ExtraRec) * xr.size();
@@ -201,6 +231,7 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
     g->K = K;
     g->E = E;
     g->W = W;
+    g->f64 = f64;
     g->t1 = (uint64_t)t1;
     g->cap = link->dev_mem_cap_bytes;
     g->grad_bytes = 0;

@@ -11,25 +11,30 @@
 
 namespace pp {
 
-template <int GEN, bool MEM, bool WA>
-static KernelInfo info() {
-    return KernelInfo{&launch_search<PP_M, GEN, MEM, WA>,
-                      reinterpret_cast<const void *>(&search_kernel<PP_M, GEN, MEM, WA>)};
+template <int GEN, bool MEM, bool WA, bool F64>
+static KernelInfo info1() {
+    return KernelInfo{&launch_search<PP_M, GEN, MEM, WA, F64>,
+                      reinterpret_cast<const void *>(&search_kernel<PP_M, GEN, MEM, WA, F64>)};
 }
 
-KernelInfo PP_CAT(kernel_for_m, PP_M)(int gen, bool mem, bool wa) {
+template <int GEN, bool MEM, bool WA>
+static KernelInfo info_f(bool f64) {
+    return f64 ? info1<GEN, MEM, WA, true>() : info1<GEN, MEM, WA, false>();
+}
+
+KernelInfo PP_CAT(kernel_for_m, PP_M)(int gen, bool mem, bool wa, bool f64) {
     switch (gen) {
         case GEN_GRAY:
-            return mem ? (wa ? info<GEN_GRAY, true, true>() : info<GEN_GRAY, true, false>())
-                       : (wa ? info<GEN_GRAY, false, true>() : info<GEN_GRAY, false, false>());
+            return mem ? (wa ? info_f<GEN_GRAY, true, true>(f64) : info_f<GEN_GRAY, true, false>(f64))
+                       : (wa ? info_f<GEN_GRAY, false, true>(f64) : info_f<GEN_GRAY, false, false>(f64));
         case GEN_RANDOM:
-            return mem ? (wa ? info<GEN_RANDOM, true, true>() : info<GEN_RANDOM, true, false>())
-                       : (wa ? info<GEN_RANDOM, false, true>() : info<GEN_RANDOM, false, false>());
+            return mem ? (wa ? info_f<GEN_RANDOM, true, true>(f64) : info_f<GEN_RANDOM, true, false>(f64))
+                       : (wa ? info_f<GEN_RANDOM, false, true>(f64) : info_f<GEN_RANDOM, false, false>(f64));
         case GEN_PERTURB:
-            return mem ? (wa ? info<GEN_PERTURB, true, true>() : info<GEN_PERTURB, true, false>())
-                       : (wa ? info<GEN_PERTURB, false, true>() : info<GEN_PERTURB, false, false>());
+            return mem ? (wa ? info_f<GEN_PERTURB, true, true>(f64) : info_f<GEN_PERTURB, true, false>(f64))
+                       : (wa ? info_f<GEN_PERTURB, false, true>(f64) : info_f<GEN_PERTURB, false, false>(f64));
         default:
-            return mem ? info<GEN_EXPLICIT, true, true>() : info<GEN_EXPLICIT, false, true>();
+            return mem ? info_f<GEN_EXPLICIT, true, true>(f64) : info_f<GEN_EXPLICIT, false, true>(f64);
     }
 }
 

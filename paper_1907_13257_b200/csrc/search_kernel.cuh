@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "internal.h"
 
 namespace pp {
@@ -208,62 +210,150 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
-// v + (tag(v) ≠ dev ? c : 0): the cut-edge charge as two predicated adds
-__device__ __forceinline__ uint64_t add_if_cut(uint64_t v, uint32_t dev, uint64_t c) {
-    uint64_t t;
-    asm("{\n .reg .pred p;\n .reg .b32 x, lo, hi, clo, chi;\n"
-        " mov.b64 {lo, hi}, %1;\n mov.b64 {clo, chi}, %3;\n"
-        " xor.b32 x, lo, %2;\n and.b32 x, x, 7;\n setp.ne.u32 p, x, 0;\n"
-        " @p add.cc.u32 lo, lo, clo;\n @p addc.u32 hi, hi, chi;\n"
-        " mov.b64 %0, {lo, hi};\n}"
-        : "=l"(t)
-        : "l"(v), "r"(dev), "l"(c));
-    return t;
-}
+// ---------------------------------------------------------- arithmetic
+// Two exact representations of a tagged finish time (internal.h):
+//   ArithU64: 8·t + device in a u64 (INT32 pipes: 2 ops per add, 4 per max);
+//   ArithF64: t + device·ulp(t) in a double, t < 2^49 (DADD on the FP64 pipe,
+//             max = DSETP + predicated DMUL by an opaque 1.0, no ALU work).
+struct ArithU64 {
+    typedef uint64_t V;
+    static __device__ __forceinline__ V from_bits(uint64_t b) { return b; }
+    static __device__ __forceinline__ uint64_t to_bits(V v) { return v; }
+    // v + (tag(v) ≠ dev ? c : 0): the cut-edge charge as predicated adds
+    static __device__ __forceinline__ V cut_add(V v, uint32_t dev, uint64_t c) {
+        uint64_t t;
+        asm("{\n .reg .pred p;\n .reg .b32 x, lo, hi, clo, chi;\n"
+            " mov.b64 {lo, hi}, %1;\n mov.b64 {clo, chi}, %3;\n"
+            " xor.b32 x, lo, %2;\n and.b32 x, x, 7;\n setp.ne.u32 p, x, 0;\n"
+            " @p add.cc.u32 lo, lo, clo;\n @p addc.u32 hi, hi, chi;\n"
+            " mov.b64 %0, {lo, hi};\n}"
+            : "=l"(t)
+            : "l"(v), "r"(dev), "l"(c));
+        return t;
+    }
+    static __device__ __forceinline__ void vmax(V &r, V t, double) { r = t > r ? t : r; }
+    static __device__ __forceinline__ V finish(V s, uint32_t dev, uint64_t cost) { return ((s & ~7ull) | dev) + cost; }
+    static __device__ __forceinline__ uint64_t ps(V v) { return v >> 3; }
+};
+
+struct ArithF64 {
+    typedef double V;
+    static __device__ __forceinline__ V from_bits(uint64_t b) { return __longlong_as_double((long long)b); }
+    static __device__ __forceinline__ uint64_t to_bits(V v) { return (uint64_t)__double_as_longlong(v); }
+    static __device__ __forceinline__ V cut_add(V v, uint32_t dev, uint64_t c) {
+        double t;
+        asm("{\n .reg .pred p;\n .reg .b32 x, lo, hi;\n"
+            " mov.b64 {lo, hi}, %1;\n xor.b32 x, lo, %2;\n and.b32 x, x, 7;\n setp.ne.u32 p, x, 0;\n"
+            " mov.f64 %0, %1;\n @p add.rn.f64 %0, %1, %3;\n}"
+            : "=d"(t)
+            : "d"(v), "r"(dev), "d"(__longlong_as_double((long long)c)));
+        return t;
+    }
+    static __device__ __forceinline__ void vmax(V &r, V t, double one) {
+        asm("{\n .reg .pred p;\n setp.gt.f64 p, %1, %0;\n @p mul.rn.f64 %0, %1, %2;\n}"
+            : "+d"(r)
+            : "d"(t), "d"(one));
+    }
+    // ((s with the tag cleared) + cost) with the tag set to dev
+    static __device__ __forceinline__ V finish(V s, uint32_t dev, uint64_t cost) {
+        double r;
+        asm("{\n .reg .b32 lo, hi;\n .reg .f64 x;\n"
+            " mov.b64 {lo, hi}, %1;\n and.b32 lo, lo, -8;\n mov.b64 x, {lo, hi};\n"
+            " add.rn.f64 x, x, %3;\n mov.b64 {lo, hi}, x;\n or.b32 lo, lo, %2;\n mov.b64 %0, {lo, hi};\n}"
+            : "=d"(r)
+            : "d"(s), "r"(dev), "d"(__longlong_as_double((long long)cost)));
+        return r;
+    }
+    static __device__ __forceinline__ uint64_t ps(V v) {
+        uint64_t b = (uint64_t)__double_as_longlong(v) & ~7ull;
+        return (uint64_t)__double2ull_rz(__longlong_as_double((long long)b));
+    }
+};
 
 // ------------------------------------------------------ per-device state
-template <int M, bool SMEM>
+// free[d]: the tagged finish time of the last op issued on device d.
+// max_with(r, dev) = max(r, free[dev]); set(dev, v): free[dev] = v.
+template <class A, int M, int KIND>
 struct FreeTimes;
 
-template <int M>
-struct FreeTimes<M, false> {               // registers, select chains (M ≤ 2)
-    uint64_t f[M];
+template <class A, int M>
+struct FreeTimes<A, M, 0> {                // registers, select chains (u64, M ≤ 2)
+    typedef typename A::V V;
+    V f[M];
     __device__ __forceinline__ void init(uint32_t) {
 #pragma unroll
-        for (int d = 0; d < M; d++) f[d] = 0;
+        for (int d = 0; d < M; d++) f[d] = A::from_bits(0);
     }
-    __device__ __forceinline__ uint64_t get(uint32_t dev) const {
-        uint64_t v = f[0];
+    __device__ __forceinline__ V max_with(V r, uint32_t dev, double one) {
+        V v = f[0];
 #pragma unroll
         for (int d = 1; d < M; d++) v = (dev == (uint32_t)d) ? f[d] : v;
-        return v;
+        A::vmax(r, v, one);
+        return r;
     }
-    __device__ __forceinline__ void set(uint32_t dev, uint64_t v) {
+    __device__ __forceinline__ void set(uint32_t dev, V v, double) {
 #pragma unroll
         for (int d = 0; d < M; d++) f[d] = (dev == (uint32_t)d) ? v : f[d];
     }
-    __device__ __forceinline__ uint64_t max_all() const {
-        uint64_t v = f[0];
+    __device__ __forceinline__ V max_all(double one) const {
+        V v = f[0];
 #pragma unroll
-        for (int d = 1; d < M; d++) v = f[d] > v ? f[d] : v;
+        for (int d = 1; d < M; d++) A::vmax(v, f[d], one);
         return v;
     }
 };
 
 template <int M>
-struct FreeTimes<M, true> {                // warp region [device][k][lane] (M ≥ 3)
+struct FreeTimes<ArithF64, M, 1> {         // registers, predicated FP64 moves (f64, M ≤ 2)
+    double f0, f1;
+    __device__ __forceinline__ void init(uint32_t) { f0 = f1 = 0.0; }
+    __device__ __forceinline__ double max_with(double r, uint32_t dev, double one) {
+        if (M == 1) {
+            ArithF64::vmax(r, f0, one);
+            return r;
+        }
+        asm("{\n .reg .pred pd, p0, p1;\n setp.ne.u32 pd, %1, 0;\n"
+            " setp.gt.and.f64 p0, %2, %0, !pd;\n setp.gt.and.f64 p1, %3, %0, pd;\n"
+            " @p0 mul.rn.f64 %0, %2, %4;\n @p1 mul.rn.f64 %0, %3, %4;\n}"
+            : "+d"(r)
+            : "r"(dev), "d"(f0), "d"(f1), "d"(one));
+        return r;
+    }
+    __device__ __forceinline__ void set(uint32_t dev, double v, double one) {
+        if (M == 1) {
+            f0 = v;
+            return;
+        }
+        asm("{\n .reg .pred pd;\n setp.ne.u32 pd, %2, 0;\n"
+            " @!pd mul.rn.f64 %0, %3, %4;\n @pd mul.rn.f64 %1, %3, %4;\n}"
+            : "+d"(f0), "+d"(f1)
+            : "r"(dev), "d"(v), "d"(one));
+    }
+    __device__ __forceinline__ double max_all(double one) const {
+        double v = f0;
+        if (M > 1) ArithF64::vmax(v, f1, one);
+        return v;
+    }
+};
+
+template <class A, int M>
+struct FreeTimes<A, M, 2> {                // warp region [device][k][lane] (M ≥ 3)
+    typedef typename A::V V;
     uint32_t f;                            // shared address of this lane's / placement's device-0 entry
     __device__ __forceinline__ void init(uint32_t base) {
         f = base;
 #pragma unroll
         for (int d = 0; d < M; d++) sts64(f + d * kSlotStride, 0);
     }
-    __device__ __forceinline__ uint64_t get(uint32_t dev) const { return lds64(f + dev * kSlotStride); }
-    __device__ __forceinline__ void set(uint32_t dev, uint64_t v) { sts64(f + dev * kSlotStride, v); }
-    __device__ __forceinline__ uint64_t max_all() const {
-        uint64_t v = 0;
+    __device__ __forceinline__ V max_with(V r, uint32_t dev, double one) {
+        A::vmax(r, A::from_bits(lds64(f + dev * kSlotStride)), one);
+        return r;
+    }
+    __device__ __forceinline__ void set(uint32_t dev, V v, double) { sts64(f + dev * kSlotStride, A::to_bits(v)); }
+    __device__ __forceinline__ V max_all(double one) const {
+        V v = A::from_bits(0);
 #pragma unroll
-        for (int d = 0; d < M; d++) v = u64max(v, lds64(f + d * kSlotStride));
+        for (int d = 0; d < M; d++) A::vmax(v, A::from_bits(lds64(f + d * kSlotStride)), one);
         return v;
     }
 };
@@ -290,17 +380,21 @@ struct MemUse {
 // -------------------------------------------------- kNP placements per lane
 // lane: shared address of this lane's entry in its warp region (region +
 // 8·lane); placement k's copy of a slot is at +k·256.
-template <int M, bool MEM, class Gen>
+template <int M, bool MEM, bool F64, class Gen>
 __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
                                             const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
-                                            uint32_t K, uint64_t cap) {
-    constexpr bool FREE_SMEM = (M > 2);
-    FreeTimes<M, FREE_SMEM> fr[kNP];
+                                            uint32_t K, uint64_t cap, double one) {
+    typedef typename std::conditional<F64, ArithF64, ArithU64>::type A;
+    typedef typename A::V V;
+    constexpr int KIND = (M > 2) ? 2 : (F64 ? 1 : 0);
+    FreeTimes<A, M, KIND> fr[kNP];
     MemUse<M> mu[kNP];
+    V prev[kNP];
 #pragma unroll
     for (int k = 0; k < kNP; k++) {
         fr[k].init(lane + free_off + k * 256);
         if (MEM) mu[k].init();
+        prev[k] = A::from_bits(0);
     }
     uint32_t op = ops;
     uint32_t x = xr;
@@ -309,35 +403,44 @@ __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint3
         const uint4 a = lds128(op);
         const uint4 b = lds128(op + 16);
         op += sizeof(OpRec);
-        const uint64_t cost8 = ((uint64_t)a.y << 32) | a.x;
-        const uint64_t c8 = ((uint64_t)a.w << 32) | a.z;
+        const uint64_t cost = ((uint64_t)a.y << 32) | a.x;
+        const uint64_t c = ((uint64_t)a.w << 32) | a.z;
         uint32_t dev[kNP];
-        uint64_t r[kNP];
+        V r[kNP];
         gen.devs(p, b.w, dev);
+        if (b.x == kFromPrev) {                // uniform: chain edge, value in a register
 #pragma unroll
-        for (int k = 0; k < kNP; k++) r[k] = add_if_cut(lds64(lane + b.x + k * 256), dev[k], c8);
+            for (int k = 0; k < kNP; k++) r[k] = A::cut_add(prev[k], dev[k], c);
+        } else {
+#pragma unroll
+            for (int k = 0; k < kNP; k++) r[k] = A::cut_add(A::from_bits(lds64(lane + b.x + k * 256)), dev[k], c);
+        }
 #pragma unroll 1
         for (uint32_t q = 0; q < b.z; q++) {   // further inputs (uniform trip count)
             const uint4 e = lds128(x);
             x += sizeof(ExtraRec);
             const uint64_t ce = ((uint64_t)e.y << 32) | e.x;
 #pragma unroll
-            for (int k = 0; k < kNP; k++) r[k] = u64max(r[k], add_if_cut(lds64(lane + e.z + k * 256), dev[k], ce));
+            for (int k = 0; k < kNP; k++)
+                A::vmax(r[k], A::cut_add(A::from_bits(lds64(lane + e.z + k * 256)), dev[k], ce), one);
         }
 #pragma unroll
         for (int k = 0; k < kNP; k++) {
-            const uint64_t s = u64max(r[k], fr[k].get(dev[k]));
-            const uint64_t fin = ((s & ~7ull) | dev[k]) + cost8;
-            sts64(lane + b.y + k * 256, fin);
-            fr[k].set(dev[k], fin);
+            const V s = fr[k].max_with(r[k], dev[k], one);
+            prev[k] = A::finish(s, dev[k], cost);
+            fr[k].set(dev[k], prev[k], one);
             if (MEM && fwd) mu[k].add(dev[k], mem[p]);
+        }
+        if (b.y != kNoStore) {
+#pragma unroll
+            for (int k = 0; k < kNP; k++) sts64(lane + b.y + k * 256, A::to_bits(prev[k]));
         }
     };
     for (uint32_t p = 0; p < K; p++) step(p, true);
     for (uint32_t p = K; p-- > 0;) step(p, false);
 #pragma unroll
     for (int k = 0; k < kNP; k++) {
-        mk[k] = fr[k].max_all() >> 3;
+        mk[k] = A::ps(fr[k].max_all(one));
         if (MEM && mu[k].over(cap)) mk[k] = kInfeasible;
     }
 }
@@ -347,7 +450,7 @@ __device__ __forceinline__ bool lex_less(uint64_t m1, uint64_t i1, uint64_t m2, 
 }
 
 // ------------------------------------------------------------------ kernel
-template <int M, int GEN, bool MEM, bool WRITE_ALL>
+template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64>
 __global__ void __launch_bounds__(256) search_kernel(const KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t mbar;
@@ -418,21 +521,21 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams P) {
         if (GEN == GEN_GRAY) {
             GrayGen<M> g;
             g.init(idx, P.K);
-            schedule_np<M, MEM>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap);
+            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap, P.one);
         } else if (GEN == GEN_RANDOM) {
             RandomGen<M> g;
             g.init(idx, P.seed, P.K);
-            schedule_np<M, MEM>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap);
+            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap, P.one);
         } else if (GEN == GEN_PERTURB) {
             PerturbGen<M> g;
             g.init(idx, P.seed, P.K, P.tau);
-            schedule_np<M, MEM>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap);
+            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap, P.one);
         } else {
             ExplicitGen g;
 #pragma unroll
             for (int k = 0; k < kNP; k++) g.row[k] = P.g_place + (idx[k] - P.begin) * (uint64_t)P.K;
             g.orig = orig;
-            schedule_np<M, MEM>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap);
+            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap, P.one);
         }
 #pragma unroll
         for (int k = 0; k < kNP; k++) {
@@ -556,9 +659,9 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
     }
 }
 
-template <int M, int GEN, bool MEM, bool WRITE_ALL>
+template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64>
 int launch_search(const KParams &p, int grid, int threads, int smem, void *stream) {
-    search_kernel<M, GEN, MEM, WRITE_ALL><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
+    search_kernel<M, GEN, MEM, WRITE_ALL, F64><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
     return (int)cudaGetLastError();
 }
 

@@ -333,9 +333,11 @@ def independent(K, fwd, bwd):
 
 
 def random_dag(seed, K, avg_deg=1.5, max_in=4, max_cost=1000, max_bytes=2000, bw=10**12,
-               lat_max=50, zero_frac=0.05, shuffle_ids=True, param=False):
+               lat_max=50, zero_frac=0.05, shuffle_ids=True, param=False, window=None):
     """Seeded random DAG: edges only from lower to higher creation index, ids
-    shuffled so π is not the identity; parallel edges allowed."""
+    shuffled so π is not the identity; parallel edges allowed.
+    `window` bounds how far back a producer may be (None = anywhere), which
+    bounds the number of simultaneously live values like a real DFG."""
     rng = random.Random(seed)
     fwd = [0 if rng.random() < zero_frac else rng.randint(1, max_cost) for _ in range(K)]
     bwd = [0 if rng.random() < zero_frac else rng.randint(1, 2 * max_cost) for _ in range(K)]
@@ -343,11 +345,14 @@ def random_dag(seed, K, avg_deg=1.5, max_in=4, max_cost=1000, max_bytes=2000, bw
     for v in range(1, K):
         nin = min(max_in, v, max(0, int(rng.expovariate(1.0 / avg_deg) + 0.5)))
         for _ in range(nin):
-            u = rng.randrange(v) if rng.random() < 0.5 else max(0, v - 1 - rng.randrange(min(v, 4)))
+            lo = 0 if window is None else max(0, v - window)
+            u = rng.randrange(lo, v) if rng.random() < 0.5 else max(0, v - 1 - rng.randrange(min(v, 4)))
             edges.append((u, v, rng.randint(0, max_bytes)))
     ids = list(range(K))
-    if shuffle_ids:
+    if shuffle_ids and window is None:
         ids = rng.sample(range(10 * K), K)
+    elif shuffle_ids:
+        ids = sorted(rng.sample(range(10 * K), K))   # keep creation order = π (locality)
     bwd_bytes = [rng.randint(0, max_bytes) for _ in edges] if rng.random() < 0.5 else None
     d = _plain(f"random{seed}", fwd, bwd, edges, bw, rng.randint(0, lat_max), bwd_bytes=bwd_bytes,
                ids=ids)

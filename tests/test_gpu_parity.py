@@ -130,7 +130,7 @@ def test_fuzz_random_dags(seed):
     rng = random.Random(seed)
     K = rng.choice([1, 2, 7, 33, 100, 257, 600, 1024])
     deg = rng.choice([0.5, 1.5, 3.0]) if K < 600 else 1.0
-    spec = synth.random_dag(seed, K, avg_deg=deg, max_in=rng.choice([2, 4, 9]),
+    spec = synth.random_dag(seed, K, avg_deg=deg, max_in=rng.choice([2, 4, 9]), window=None if K < 200 else 48,
                             max_cost=rng.choice([10, 10**6]), max_bytes=rng.choice([0, 100, 10**7]),
                             lat_max=rng.choice([0, 1000]))
     if rng.random() < 0.3:
@@ -204,13 +204,25 @@ def test_edge_cases():
 
 def test_large_image_reduces_cta():
     # K + E near the 96 KB image cap, large W
-    spec = synth.random_dag(77, 1100, avg_deg=0.9, max_in=3)
+    spec = synth.random_dag(77, 1100, avg_deg=0.9, max_in=3, window=40)
     g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
     assert g.image_bytes > 60_000
     for M in (2, 8):
         got = pp.u64(g.eval_generated(M, pp.GEN_RANDOM, 4, 0, None, 0, 100))
         want = _oracle_candidates(od, M, O.GEN_RANDOM, 4, 0, None, range(100))
         assert np.array_equal(got, want)
+
+
+def test_state_too_large_is_reported():
+    # producers anywhere in a 1000-op DAG keep hundreds of values live: the
+    # per-warp state cannot fit in shared memory -> PP_E_TOO_LARGE (pp.h)
+    spec = synth.random_dag(5, 1000, avg_deg=1.5)
+    g = pp.Dfg(spec)
+    if g.W < 300:
+        pytest.skip(f"W={g.W} fits")
+    with pytest.raises(pp.PPError) as e:
+        g.eval_generated(2, pp.GEN_RANDOM, 1, 0, None, 0, 64)
+    assert e.value.code == -4
 
 
 def test_error_codes_match_oracle():
