@@ -317,8 +317,17 @@ static uint64_t word_at(uint64_t seed, uint64_t i, uint64_t Wd, uint64_t t) {
 
 /* Writes placement d[0..K-1] (π positions) of candidate i.
  * GRAY   : O5, reflected M-ary Gray code of i.
- * RANDOM : O6, bits from SplitMix64 words; i = 0 is all zeros.
- * PERTURB: O6, per-op flip of base with probability τ/256; i = 0 is the base. */
+ * RANDOM : O6, b = ⌈log2 M⌉ bits per op, P = 8·⌊8/b⌋ ops per SplitMix64
+ *          word (64, 32, 16 for b = 1, 2, 3), d = (x·M) >> b; i = 0 is all
+ *          zeros.
+ * PERTURB: O6, one byte per op, 8 ops per word: op j flips iff
+ *          u_j = byte (j mod 8) of word'(i, ⌊j/8⌋) < τ (probability τ/256),
+ *          to 1 − base (M = 2) or to (base + 1 + y_j mod (M−1)) mod M with
+ *          y_j = byte (j mod 8) of word''(i, ⌊j/8⌋); i = 0 is the base.
+ *          word' uses seed_r ^ 0xD1B54A32D192ED03, word'' seed_r ^
+ *          0x8CB92BA72F3D8DD7.
+ * (Generator spec revision 2: word boundaries fall on 8-op groups; DESIGN.md
+ * §Generators.  The paper has no generator; this is the shared spec.)      */
 void or_gen(int K, int M, int gen, uint64_t seed_r, uint32_t tau,
             const uint8_t *base, uint64_t i, uint8_t *d) {
     if (M == 1) { for (int j = 0; j < K; j++) d[j] = 0; return; }
@@ -339,7 +348,7 @@ void or_gen(int K, int M, int gen, uint64_t seed_r, uint32_t tau,
     int b = ceil_log2(M);
     if (gen == OR_GEN_RANDOM) {
         if (i == 0) { for (int j = 0; j < K; j++) d[j] = 0; return; }
-        uint64_t P = (uint64_t)(64 / b);
+        uint64_t P = 8 * (uint64_t)(8 / b);
         uint64_t Wd = ((uint64_t)K + P - 1) / P;
         for (int j = 0; j < K; j++) {
             uint64_t w = word_at(seed_r, i, Wd, (uint64_t)j / P);
@@ -350,16 +359,14 @@ void or_gen(int K, int M, int gen, uint64_t seed_r, uint32_t tau,
     }
     /* PERTURB */
     if (i == 0) { for (int j = 0; j < K; j++) d[j] = base[j]; return; }
-    uint64_t s2 = seed_r ^ 0xD1B54A32D192ED03ULL;
-    uint64_t fb = 8 + (uint64_t)b;
-    uint64_t P = 64 / fb;
-    uint64_t Wd = ((uint64_t)K + P - 1) / P;
+    uint64_t s1 = seed_r ^ 0xD1B54A32D192ED03ULL, s2 = seed_r ^ 0x8CB92BA72F3D8DD7ULL;
+    uint64_t Wd = ((uint64_t)K + 7) / 8;
     for (int j = 0; j < K; j++) {
-        uint64_t w = word_at(s2, i, Wd, (uint64_t)j / P);
-        uint64_t f = (w >> (fb * ((uint64_t)j % P))) & ((1ULL << fb) - 1);
-        uint64_t u = f & 0xFF, y = f >> 8;
-        if (u >= tau) d[j] = base[j];
-        else d[j] = (uint8_t)((base[j] + 1 + (y % (uint64_t)(M - 1))) % (uint64_t)M);
+        uint64_t u = (word_at(s1, i, Wd, (uint64_t)j / 8) >> (8 * ((uint64_t)j % 8))) & 0xFF;
+        if (u >= tau) { d[j] = base[j]; continue; }
+        if (M == 2) { d[j] = (uint8_t)(1 - base[j]); continue; }
+        uint64_t y = (word_at(s2, i, Wd, (uint64_t)j / 8) >> (8 * ((uint64_t)j % 8))) & 0xFF;
+        d[j] = (uint8_t)((base[j] + 1 + (y % (uint64_t)(M - 1))) % (uint64_t)M);
     }
 }
 
