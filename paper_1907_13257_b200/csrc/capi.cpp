@@ -59,7 +59,7 @@ UpdateFn update_for(int M, int gen) {
 struct ProjParams;
 struct CrossParams;
 int launch_pack_key(uint64_t *s, int rank, void *stream);
-int launch_patch_base(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, void *stream);
+int launch_patch_base(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8, void *stream);
 int launch_contrib(uint64_t *s, int rank, void *stream);
 
 static int cuda_err(cudaError_t e, const char *what) {
@@ -135,6 +135,7 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
     p.cap = g->cap;
     p.image_bytes = g->image_bytes;
     p.K = (uint32_t)g->K;
+    p.K8 = (uint32_t)g->K8;
     p.off_extra = g->off_extra;
     p.off_mem = g->off_mem;
     p.off_orig = g->off_orig;
@@ -142,7 +143,6 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
     p.region_bytes = region;
     p.free_off = nslot * kSlotStride;
     p.zero_off = (uint32_t)g->W * kSlotStride;
-    p.one = 1.0;
     p.g_partials = g->d_partials;
     p.g_ticket = g->d_ticket;
     p.g_out = g->d_scalars + SC_LOCAL_MK;
@@ -277,7 +277,7 @@ int pp_eval_generated(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t
     DeviceGuard dg(g->device);
     if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
     if (gen == GEN_PERTURB) {
-        if ((rc = launch_patch_base(g->d_image, g->d_base, d_base_pi, (uint32_t)g->K, stream)))
+        if ((rc = launch_patch_base(g->d_image, g->d_base, d_base_pi, (uint32_t)g->K, (uint32_t)g->K8, stream)))
             return cuda_err((cudaError_t)rc, "base patch");
         g_launches++;
     }
@@ -301,7 +301,7 @@ int pp_search_range(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
     DeviceGuard dg(g->device);
     if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
     if (gen == GEN_PERTURB) {
-        if ((rc = launch_patch_base(g->d_image, g->d_base, d_base_pi, (uint32_t)g->K, stream)))
+        if ((rc = launch_patch_base(g->d_image, g->d_base, d_base_pi, (uint32_t)g->K, (uint32_t)g->K8, stream)))
             return cuda_err((cudaError_t)rc, "base patch");
         g_launches++;
     }
@@ -357,7 +357,7 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
         }
     cudaError_t e = cudaMemcpyAsync(g->d_winner, base.data(), g->base_bytes, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_err(e, "base upload");
-    if ((rc = launch_patch_base(g->d_image, g->d_base, g->d_winner, (uint32_t)K, stream)))
+    if ((rc = launch_patch_base(g->d_image, g->d_base, g->d_winner, (uint32_t)K, (uint32_t)g->K8, stream)))
         return cuda_err((cudaError_t)rc, "base patch");
     g_launches++;
     uint64_t begin = 0, end = 0;
@@ -410,7 +410,8 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
             if (nr != ncclSuccess) return nccl_err(nr, "allreduce index");
             g_launches += 2;
         }
-        UParams u{g->d_image, g->d_base, g->d_winner, g->d_best_place, g->d_scalars, seed_r, (uint32_t)K, desc->flip_thresh,
+        UParams u{g->d_image, g->d_base, g->d_winner, g->d_best_place, g->d_scalars, seed_r, (uint32_t)K,
+                  (uint32_t)g->K8, desc->flip_thresh,
                   r, comm ? 1 : 0};
         if ((rc = upd(u, stream))) return cuda_err((cudaError_t)rc, "round update");
         g_launches++;

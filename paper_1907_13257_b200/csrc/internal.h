@@ -2,17 +2,20 @@
 //
 // The shared-memory image (built by loader.cpp, read by search_kernel.cuh):
 //
-//   [OpRec    × 2K]  one 32-B record per scheduled op, in issue order: steps
-//                    s = 0..K−1 are the forward ops of π positions p = s, steps
-//                    s = K..2K−1 the backward ops of p = 2K−1−s (readings R1/R2).
+//   [OpRec   × 2K8]  one 32-B record per scheduled op, in issue order: steps
+//                    s = 0..K8−1 are the forward ops of π positions p = s, steps
+//                    s = K8..2K8−1 the backward ops of p = 2K8−1−s (readings
+//                    R1/R2).  K8 = K rounded up to a multiple of 8; positions
+//                    p ≥ K are no-op pads (zero cost, zero input) that leave
+//                    every device's free time unchanged.
 //                    The op's FIRST input edge is inlined in the record (most
 //                    ops of a training DFG have in-degree 1); an op without
 //                    inputs gets a zero-cost edge from the always-zero slot, a
 //                    sink's backward gets a zero-cost "self" edge from its own
 //                    forward finish time (it waits for its own forward, R1).
 //   [ExtraRec × NX]  the remaining input edges, consumed in step order.
-//   [u64   × K  ]    M(k) by π position (read only when a memory cap is set)
-//   [u32   × K  ]    descriptor index of π position p (explicit placements)
+//   [u64   × K8 ]    M(k) by π position (read only when a memory cap is set)
+//   [u32   × K8 ]    descriptor index of π position p (explicit placements)
 //
 // Per-lane schedule state lives in a per-warp region of shared memory laid out
 // [slot][placement k < kNP][lane] × u64, so a slot's byte offset inside the
@@ -53,7 +56,8 @@ struct OpRec {
     uint64_t c8;          // encoded c of the first input edge (0 for the zero / self edge)
     uint32_t src_off;     // region byte offset of the first input's slot, or kFromPrev
     uint32_t out_off;     // region byte offset of the output slot, or kNoStore
-    uint32_t n_extra;     // further input edges (ExtraRec), consumed in order
+    uint32_t ctrl;        // 0: fast chain step (first input = previous step, no extras);
+                          // else 0x10000 | n_extra (further inputs, ExtraRec in order)
     uint32_t base;        // PERTURB base device of this op (patched every round)
 };
 static_assert(sizeof(OpRec) == 32, "OpRec is 32 B");
@@ -83,14 +87,13 @@ struct KParams {
     uint64_t seed;               // seed of this round (RANDOM/PERTURB)
     uint64_t cap;                // memory cap (0 = none)
     uint32_t image_bytes;
-    uint32_t K;
+    uint32_t K, K8;
     uint32_t off_extra, off_mem, off_orig;
     uint32_t tau;
     uint32_t smem_slots_off;     // byte offset of the first warp region in smem
     uint32_t region_bytes;       // bytes per warp region
     uint32_t free_off;           // region offset of free[M] (M ≥ 3)
     uint32_t zero_off;           // region offset of the always-zero slot
-    double one;                  // 1.0, opaque to the compiler (f64 predicated moves)
 };
 
 // Device scalar slots of pp_dfg::d_scalars (u64).
@@ -109,7 +112,7 @@ struct UParams {
     uint8_t *best_place;  // [K] best placement so far, π order
     uint64_t *s;          // d_scalars
     uint64_t seed;        // seed of this round
-    uint32_t K, tau, round;
+    uint32_t K, K8, tau, round;
     int multi;            // 1: winner comes from the NCCL-reduced slots
 };
 typedef int (*UpdateFn)(const UParams &, void *stream);
@@ -131,7 +134,7 @@ UpdateFn update_for(int M, int gen);
 
 struct pp_dfg {
     int device = 0;
-    int K = 0, E = 0, W = 0;
+    int K = 0, K8 = 0, E = 0, W = 0;
     bool f64 = false;            // tagged-f64 arithmetic (bound < 2^49) else tagged-u64
     uint64_t t1 = 0, grad_bytes = 0, cap = 0;
     std::vector<int32_t> pi;     // π position → descriptor index

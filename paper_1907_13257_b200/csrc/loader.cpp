@@ -124,15 +124,19 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
         out_e[pos[src[e]]].push_back(e);
     }
 
-    // ---- inputs of every step.  Value ids: step s produces value s (forward
-    // finish time of p = s, or backward finish time of p = 2K−1−s); −1 = zero.
-    const int S = 2 * K;
+    // ---- inputs of every step.  K8 = K padded to a multiple of 8 (no-op pads
+    // at π positions p ≥ K).  Value ids: step s produces value s (forward
+    // finish time of p = s, or backward finish time of p = 2K8−1−s); −1 = zero.
+    const int K8 = (K + 7) / 8 * 8;
+    const int S = 2 * K8;
     std::vector<std::vector<std::pair<int, uint64_t>>> inputs(S);   // (value id, cost ps)
     for (int s = 0; s < S; s++) {
-        const bool fwd = s < K;
+        const bool fwd = s < K8;
         const int p = fwd ? s : S - 1 - s;
         auto &in = inputs[s];
-        if (fwd) {
+        if (p >= K) {
+            in.push_back({-1, 0});                       // pad
+        } else if (fwd) {
             for (int e : in_e[p]) in.push_back({pos[src[e]], cf[e]});
             if (in.empty()) in.push_back({-1, 0});
         } else {
@@ -206,29 +210,31 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
     std::vector<ExtraRec> xr;
     auto src_off = [&](int v) -> uint32_t { return v < 0 ? zero_off : (uint32_t)slot[v] * kSlotStride; };
     for (int s = 0; s < S; s++) {
-        const bool fwd = s < K;
+        const bool fwd = s < K8;
         const int p = fwd ? s : S - 1 - s;
-        const int k = pi[p];
         const auto &in = inputs[s];
         OpRec &o = ops[s];
-        o.cost8 = enc(fwd ? d->fwd_ps[k] : d->bwd_ps[k]);
+        o.cost8 = p < K ? enc(fwd ? d->fwd_ps[pi[p]] : d->bwd_ps[pi[p]]) : enc(0);
         o.c8 = enc(in[0].second);
         o.src_off = fwd_first[s] ? kFromPrev : src_off(in[0].first);
         o.out_off = slot[s] < 0 ? kNoStore : (uint32_t)slot[s] * kSlotStride;
-        o.n_extra = (uint32_t)in.size() - 1;
+        const uint32_t n_extra = (uint32_t)in.size() - 1;
+        if (n_extra > 0xFFFF) return fail(PP_E_TOO_LARGE, "op with more than 65536 inputs");
+        o.ctrl = (fwd_first[s] && n_extra == 0) ? 0u : (0x10000u | n_extra);
         o.base = 0;
         for (size_t q = 1; q < in.size(); q++) xr.push_back(ExtraRec{enc(in[q].second), src_off(in[q].first), 0});
     }
     size_t off_extra = sizeof(OpRec) * S;
     size_t off_mem = off_extra + sizeof(ExtraRec) * xr.size();
-    size_t off_orig = off_mem + 8ull * K;
-    size_t bytes = off_orig + 4ull * K;
+    size_t off_orig = off_mem + 8ull * K8;
+    size_t bytes = off_orig + 4ull * K8;
     bytes = (bytes + 15) & ~size_t(15);
     if (bytes > (size_t)kMaxImageBytes) return fail(PP_E_TOO_LARGE, "DFG image exceeds 96 KB of shared memory");
 
     pp_dfg *g = new pp_dfg();
     g->device = cuda_device;
     g->K = K;
+    g->K8 = K8;
     g->E = E;
     g->W = W;
     g->f64 = f64;
@@ -242,10 +248,10 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
     g->image.assign(bytes, 0);
     memcpy(g->image.data(), ops.data(), sizeof(OpRec) * S);
     if (!xr.empty()) memcpy(g->image.data() + off_extra, xr.data(), sizeof(ExtraRec) * xr.size());
-    for (int p = 0; p < K; p++) {
-        uint64_t m = d->mem_bytes ? d->mem_bytes[pi[p]] : 0;
+    for (int p = 0; p < K8; p++) {
+        uint64_t m = (p < K && d->mem_bytes) ? d->mem_bytes[pi[p]] : 0;
         memcpy(g->image.data() + off_mem + 8ull * p, &m, 8);
-        uint32_t o = (uint32_t)pi[p];
+        uint32_t o = p < K ? (uint32_t)pi[p] : 0u;
         memcpy(g->image.data() + off_orig + 4ull * p, &o, 4);
     }
     g->off_extra = (uint32_t)off_extra;

@@ -237,17 +237,17 @@ __global__ void contrib_kernel(uint64_t *s, int rank) {
 }
 // Copies a π-order base into the canonical buffer and into OpRec.base of the
 // forward and backward records of every op (PERTURB).
-__global__ void patch_base_kernel(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K) {
+__global__ void patch_base_kernel(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8) {
     OpRec *ops = reinterpret_cast<OpRec *>(image);
     for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < K; p += gridDim.x * blockDim.x) {
         uint8_t d = src[p];
         base[p] = d;
         ops[p].base = d;
-        ops[2 * K - 1 - p].base = d;
+        ops[2 * K8 - 1 - p].base = d;
     }
 }
-int launch_patch_base(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, void *stream) {
-    patch_base_kernel<<<(K + 255) / 256, 256, 0, (cudaStream_t)stream>>>(image, base, src, K);
+int launch_patch_base(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8, void *stream) {
+    patch_base_kernel<<<(K + 255) / 256, 256, 0, (cudaStream_t)stream>>>(image, base, src, K, K8);
     return (int)cudaGetLastError();
 }
 int launch_pack_key(uint64_t *s, int rank, void *stream) {

@@ -5,12 +5,9 @@
 // Kernel shape: LANE PER PLACEMENT, kNP = 2 placements
 // per lane.  A warp evaluates 64 candidate placements in lockstep over the
 // same DFG records, so every record read is a warp-uniform shared-memory
-// broadcast shared by 64 placements; the per-placement state is the
-// finish-time slots (a per-warp shared region [slot][k][lane], conflict-free)
-// and the per-device free times (registers for M ≤ 2, the warp region
-// otherwise).  The recurrence (PAPER.md:443–453 dependency with Δ_e,
-// :465–476 one op at a time per device, :497–503 back-to-back + overlapped
-// communication; readings R1, R2):
+// broadcast shared by 64 placements.  The recurrence (PAPER.md:443–453
+// dependency with Δ_e, :465–476 one op at a time per device, :497–503
+// back-to-back ops + overlapped communication; readings R1, R2):
 //
 //   forward, p in π order:      r = max_{(u,p)} fin[u] + [d_u≠d_p]·c_f
 //   backward, p in reverse π:   r = max_{(p,w)} finb[w] + [d_w≠d_p]·c_b
@@ -18,8 +15,16 @@
 //   s = max(r, free[d_p]);  fin = s + Δ;  free[d_p] = fin
 //   makespan = max_d free[d]   (memory cap violated ⇒ UINT64_MAX)
 //
-// The DFG image is staged global → shared once per CTA with a bulk TMA copy
-// (cp.async.bulk + mbarrier).  No tensor cores: this is integer max-plus work.
+// Per-placement state: `prev` = the finish time of the previous step (its tag
+// is that op's device, so free[tag(prev)] = prev), plus for M = 2 `oth` = the
+// free time of the other device (registers), for M ≥ 3 free[] in the warp's
+// shared region.  Chain edges (the first input produced by the previous step)
+// are read from `prev`; other inputs from liveness-allocated shared slots.
+// The schedule loop is unrolled by 8 ops (one generator word per 8 ops); K is
+// padded to a multiple of 8 with state-preserving no-op records.
+//
+// The DFG image is staged global → shared once per CTA with bulk TMA copies
+// (cp.async.bulk + mbarrier).  No tensor cores: integer max-plus work.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -30,8 +35,10 @@
 
 namespace pp {
 
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
-    // SplitMix64 finaliser (generator spec, SURVEY.md §8(c) O6)
+    // SplitMix64 finaliser (generator spec, SURVEY.md §8(c) O6, DESIGN.md §Generators)
     z ^= z >> 30;
     z *= 0xBF58476D1CE4E5B9ull;
     z ^= z >> 27;
@@ -46,9 +53,9 @@ struct Bits {
 };
 
 // ------------------------------------------------------------- generators
-// dev(p, base) yields the device of π position p; it is called with
-// p = 0..K−1 (forward) and then p = K−1..0 (backward).  `base` is the PERTURB
-// base device of p, read from the op record.
+// refresh(g) prepares the 8-op group g (ops 8g..8g+7); dev(k, p, c, base)
+// yields the device of π position p = 8g + c for placement k (c is a
+// compile-time constant in the unrolled schedule loop).
 
 template <int M>
 struct GrayGen {                           // O5: reflected M-ary Gray code
@@ -87,115 +94,98 @@ struct GrayGen {                           // O5: reflected M-ary Gray code
 #pragma unroll
         for (int k = 0; k < N; k++) one(i[k], K, lo[k], hi[k]);
     }
-    template <int N>
-    __device__ __forceinline__ void devs(uint32_t p, uint32_t, uint32_t (&d)[N]) {
+    __device__ __forceinline__ void refresh(uint32_t) {}
+    __device__ __forceinline__ uint32_t dev(int k, uint32_t p, uint32_t, uint32_t) const {
+        if (M == 1) return 0;
         const bool first = p < (uint32_t)PF;
         const uint32_t sh = first ? p * b : (p - PF) * b;
-#pragma unroll
-        for (int k = 0; k < N; k++)
-            d[k] = (M == 1) ? 0u : (uint32_t)((first ? lo[k] : hi[k]) >> sh) & ((1u << b) - 1);
+        return (sh < 64) ? (uint32_t)((first ? lo[k] : hi[k]) >> sh) & ((1u << b) - 1) : 0u;
     }
 };
 
 template <int M>
-struct RandomGen {                         // O6 RANDOM
+struct RandomGen {                         // O6 RANDOM: b bits per op, P = 8·⌊8/b⌋ ops per word
     static constexpr int b = Bits<M>::b;
-    static constexpr int P = b ? 64 / b : 64;
+    static constexpr int GPW = b ? 8 / b : 8;      // 8-op groups per word
     uint64_t key[kNP];   // seed + γ·(i·Wd + 1)
-    uint64_t w[kNP];
     uint64_t keep[kNP];  // 0 for candidate 0 (all zeros), else ~0
+    uint64_t w[kNP];     // current word
+    uint32_t wg[kNP];    // the current group's 8·b bits
     uint32_t cur;        // word index held in w (shared by the lane's placements)
     template <int N>
     __device__ __forceinline__ void init(const uint64_t (&i)[N], uint64_t seed, uint32_t K) {
+        const uint64_t P = 8ull * GPW;
         const uint64_t Wd = (K + P - 1) / P;
 #pragma unroll
         for (int k = 0; k < N; k++) {
-            key[k] = seed + 0x9E3779B97F4A7C15ull * (i[k] * Wd + 1);
+            key[k] = seed + kGamma * (i[k] * Wd + 1);
             keep[k] = (i[k] == 0) ? 0ull : ~0ull;
             w[k] = 0;
+            wg[k] = 0;
         }
         cur = 0xFFFFFFFFu;
     }
-    template <int N>
-    __device__ __forceinline__ void devs(uint32_t p, uint32_t, uint32_t (&d)[N]) {
-        if (M == 1) {
-#pragma unroll
-            for (int k = 0; k < N; k++) d[k] = 0;
-            return;
-        }
-        const uint32_t t = p / P;
+    __device__ __forceinline__ void refresh(uint32_t g) {
+        if (M == 1) return;
+        const uint32_t t = g / GPW;
         if (t != cur) {   // warp-uniform
             cur = t;
 #pragma unroll
-            for (int k = 0; k < N; k++) w[k] = mix64(key[k] + 0x9E3779B97F4A7C15ull * t) & keep[k];
+            for (int k = 0; k < kNP; k++) w[k] = mix64(key[k] + kGamma * t) & keep[k];
         }
-        const uint32_t sh = b * (p - t * P);
+        const uint32_t sh = 8 * b * (g - t * GPW);
 #pragma unroll
-        for (int k = 0; k < N; k++) {
-            const uint32_t x = (uint32_t)(w[k] >> sh) & ((1u << b) - 1);
-            d[k] = ((M & (M - 1)) == 0) ? x : (x * M) >> b;
-        }
+        for (int k = 0; k < kNP; k++) wg[k] = (uint32_t)(w[k] >> sh);
+    }
+    __device__ __forceinline__ uint32_t dev(int k, uint32_t, uint32_t c, uint32_t) const {
+        if (M == 1) return 0;
+        const uint32_t x = (wg[k] >> (b * c)) & ((1u << b) - 1);
+        return ((M & (M - 1)) == 0) ? x : (x * M) >> b;
     }
 };
 
 template <int M>
-struct PerturbGen {                        // O6 PERTURB
-    static constexpr int b = Bits<M>::b;
-    static constexpr int FB = 8 + b;
-    static constexpr int P = 64 / FB;
-    uint64_t key[kNP];
-    uint64_t w[kNP];
+struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops per word
+    uint64_t key1[kNP], key2[kNP];
+    uint64_t w[kNP], y[kNP];
     uint32_t tau[kNP];   // 0 for candidate 0 (the base itself)
-    uint32_t cur;
     template <int N>
     __device__ __forceinline__ void init(const uint64_t (&i)[N], uint64_t seed, uint32_t K, uint32_t tau_) {
-        const uint64_t Wd = (K + P - 1) / P;
+        const uint64_t Wd = (K + 7) / 8;
 #pragma unroll
         for (int k = 0; k < N; k++) {
-            key[k] = (seed ^ 0xD1B54A32D192ED03ull) + 0x9E3779B97F4A7C15ull * (i[k] * Wd + 1);
+            key1[k] = (seed ^ 0xD1B54A32D192ED03ull) + kGamma * (i[k] * Wd + 1);
+            key2[k] = (seed ^ 0x8CB92BA72F3D8DD7ull) + kGamma * (i[k] * Wd + 1);
             tau[k] = (i[k] == 0) ? 0u : tau_;
-            w[k] = 0;
+            w[k] = y[k] = 0;
         }
-        cur = 0xFFFFFFFFu;
     }
-    template <int N>
-    __device__ __forceinline__ void devs(uint32_t p, uint32_t bs, uint32_t (&d)[N]) {
-        if (M == 1) {
+    __device__ __forceinline__ void refresh(uint32_t g) {
+        if (M == 1) return;
 #pragma unroll
-            for (int k = 0; k < N; k++) d[k] = 0;
-            return;
+        for (int k = 0; k < kNP; k++) {
+            w[k] = mix64(key1[k] + kGamma * g);
+            if (M > 2) y[k] = mix64(key2[k] + kGamma * g);
         }
-        const uint32_t t = p / P;
-        if (t != cur) {
-            cur = t;
-#pragma unroll
-            for (int k = 0; k < N; k++) w[k] = mix64(key[k] + 0x9E3779B97F4A7C15ull * t);
-        }
-        const uint32_t sh = FB * (p - t * P);
-#pragma unroll
-        for (int k = 0; k < N; k++) {
-            const uint32_t f = (uint32_t)(w[k] >> sh) & ((1u << FB) - 1);
-            uint32_t flip;
-            if (M == 2) flip = bs ^ 1u;
-            else flip = (bs + 1 + (f >> 8) % (uint32_t)(M > 1 ? M - 1 : 1)) % (uint32_t)M;
-            d[k] = ((f & 0xFF) >= tau[k]) ? bs : flip;
-        }
+    }
+    __device__ __forceinline__ uint32_t dev(int k, uint32_t, uint32_t c, uint32_t bs) const {
+        if (M == 1) return 0;
+        const uint32_t u = (uint32_t)(w[k] >> (8 * c)) & 0xFFu;
+        uint32_t flip;
+        if (M == 2) flip = bs ^ 1u;
+        else flip = (bs + 1 + ((uint32_t)(y[k] >> (8 * c)) & 0xFFu) % (uint32_t)(M > 1 ? M - 1 : 1)) % (uint32_t)M;
+        return (u < tau[k]) ? flip : bs;
     }
 };
 
 struct ExplicitGen {                       // rows of a [count][K] uint8 array
     const uint8_t *row[kNP];
     const uint32_t *orig;
-    template <int N>
-    __device__ __forceinline__ void devs(uint32_t p, uint32_t, uint32_t (&d)[N]) const {
-        const uint32_t o = orig[p];
-#pragma unroll
-        for (int k = 0; k < N; k++) d[k] = row[k][o];
-    }
+    __device__ __forceinline__ void refresh(uint32_t) {}
+    __device__ __forceinline__ uint32_t dev(int k, uint32_t p, uint32_t, uint32_t) const { return row[k][orig[p]]; }
 };
 
-__device__ __forceinline__ uint64_t u64max(uint64_t a, uint64_t b) { return a > b ? a : b; }
-
+// -------------------------------------------------- shared-memory access
 // 32-bit shared-window addressing (kept in program order: volatile)
 __device__ __forceinline__ uint64_t lds64(uint32_t a) {
     uint64_t v;
@@ -210,28 +200,19 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
+
 // ---------------------------------------------------------- arithmetic
 // Two exact representations of a tagged finish time (internal.h):
-//   ArithU64: 8·t + device in a u64 (INT32 pipes: 2 ops per add, 4 per max);
-//   ArithF64: t + device·ulp(t) in a double, t < 2^49 (DADD on the FP64 pipe,
-//             max = DSETP + predicated DMUL by an opaque 1.0, no ALU work).
+//   ArithU64: 8·t + device in a u64;
+//   ArithF64: t + device·ulp(t) in a double, t < 2^49 (adds and compares on
+//             the FP64 pipe instead of the INT32 ALU pipe).
 struct ArithU64 {
     typedef uint64_t V;
     static __device__ __forceinline__ V from_bits(uint64_t b) { return b; }
     static __device__ __forceinline__ uint64_t to_bits(V v) { return v; }
-    // v + (tag(v) ≠ dev ? c : 0): the cut-edge charge as predicated adds
-    static __device__ __forceinline__ V cut_add(V v, uint32_t dev, uint64_t c) {
-        uint64_t t;
-        asm("{\n .reg .pred p;\n .reg .b32 x, lo, hi, clo, chi;\n"
-            " mov.b64 {lo, hi}, %1;\n mov.b64 {clo, chi}, %3;\n"
-            " xor.b32 x, lo, %2;\n and.b32 x, x, 7;\n setp.ne.u32 p, x, 0;\n"
-            " @p add.cc.u32 lo, lo, clo;\n @p addc.u32 hi, hi, chi;\n"
-            " mov.b64 %0, {lo, hi};\n}"
-            : "=l"(t)
-            : "l"(v), "r"(dev), "l"(c));
-        return t;
-    }
-    static __device__ __forceinline__ void vmax(V &r, V t, double) { r = t > r ? t : r; }
+    static __device__ __forceinline__ uint32_t lo(V v) { return (uint32_t)v; }
+    static __device__ __forceinline__ V add(V v, uint64_t c) { return v + c; }
+    static __device__ __forceinline__ V vmax(V a, V b) { return a > b ? a : b; }
     static __device__ __forceinline__ V finish(V s, uint32_t dev, uint64_t cost) { return ((s & ~7ull) | dev) + cost; }
     static __device__ __forceinline__ uint64_t ps(V v) { return v >> 3; }
 };
@@ -240,123 +221,29 @@ struct ArithF64 {
     typedef double V;
     static __device__ __forceinline__ V from_bits(uint64_t b) { return __longlong_as_double((long long)b); }
     static __device__ __forceinline__ uint64_t to_bits(V v) { return (uint64_t)__double_as_longlong(v); }
-    static __device__ __forceinline__ V cut_add(V v, uint32_t dev, uint64_t c) {
-        double t;
-        asm("{\n .reg .pred p;\n .reg .b32 x, lo, hi;\n"
-            " mov.b64 {lo, hi}, %1;\n xor.b32 x, lo, %2;\n and.b32 x, x, 7;\n setp.ne.u32 p, x, 0;\n"
-            " mov.f64 %0, %1;\n @p add.rn.f64 %0, %1, %3;\n}"
-            : "=d"(t)
-            : "d"(v), "r"(dev), "d"(__longlong_as_double((long long)c)));
-        return t;
-    }
-    static __device__ __forceinline__ void vmax(V &r, V t, double one) {
-        asm("{\n .reg .pred p;\n setp.gt.f64 p, %1, %0;\n @p mul.rn.f64 %0, %1, %2;\n}"
-            : "+d"(r)
-            : "d"(t), "d"(one));
-    }
+    static __device__ __forceinline__ uint32_t lo(V v) { return (uint32_t)__double2loint(v); }
+    static __device__ __forceinline__ V add(V v, uint64_t c) { return __dadd_rn(v, from_bits(c)); }
+    static __device__ __forceinline__ V vmax(V a, V b) { return a > b ? a : b; }
     // ((s with the tag cleared) + cost) with the tag set to dev
     static __device__ __forceinline__ V finish(V s, uint32_t dev, uint64_t cost) {
-        double r;
-        asm("{\n .reg .b32 lo, hi;\n .reg .f64 x;\n"
-            " mov.b64 {lo, hi}, %1;\n and.b32 lo, lo, -8;\n mov.b64 x, {lo, hi};\n"
-            " add.rn.f64 x, x, %3;\n mov.b64 {lo, hi}, x;\n or.b32 lo, lo, %2;\n mov.b64 %0, {lo, hi};\n}"
-            : "=d"(r)
-            : "d"(s), "r"(dev), "d"(__longlong_as_double((long long)cost)));
-        return r;
+        const double t = __hiloint2double(__double2hiint(s), __double2loint(s) & ~7);
+        const double x = __dadd_rn(t, from_bits(cost));
+        return __hiloint2double(__double2hiint(x), __double2loint(x) | (int)dev);
     }
     static __device__ __forceinline__ uint64_t ps(V v) {
-        uint64_t b = (uint64_t)__double_as_longlong(v) & ~7ull;
-        return (uint64_t)__double2ull_rz(__longlong_as_double((long long)b));
+        return (uint64_t)__double2ull_rz(__hiloint2double(__double2hiint(v), __double2loint(v) & ~7));
     }
 };
 
-// ------------------------------------------------------ per-device state
-// free[d]: the tagged finish time of the last op issued on device d.
-// max_with(r, dev) = max(r, free[dev]); set(dev, v): free[dev] = v.
-template <class A, int M, int KIND>
-struct FreeTimes;
-
-template <class A, int M>
-struct FreeTimes<A, M, 0> {                // registers, select chains (u64, M ≤ 2)
-    typedef typename A::V V;
-    V f[M];
-    __device__ __forceinline__ void init(uint32_t) {
-#pragma unroll
-        for (int d = 0; d < M; d++) f[d] = A::from_bits(0);
-    }
-    __device__ __forceinline__ V max_with(V r, uint32_t dev, double one) {
-        V v = f[0];
-#pragma unroll
-        for (int d = 1; d < M; d++) v = (dev == (uint32_t)d) ? f[d] : v;
-        A::vmax(r, v, one);
-        return r;
-    }
-    __device__ __forceinline__ void set(uint32_t dev, V v, double) {
-#pragma unroll
-        for (int d = 0; d < M; d++) f[d] = (dev == (uint32_t)d) ? v : f[d];
-    }
-    __device__ __forceinline__ V max_all(double one) const {
-        V v = f[0];
-#pragma unroll
-        for (int d = 1; d < M; d++) A::vmax(v, f[d], one);
-        return v;
-    }
-};
-
-template <int M>
-struct FreeTimes<ArithF64, M, 1> {         // registers, predicated FP64 moves (f64, M ≤ 2)
-    double f0, f1;
-    __device__ __forceinline__ void init(uint32_t) { f0 = f1 = 0.0; }
-    __device__ __forceinline__ double max_with(double r, uint32_t dev, double one) {
-        if (M == 1) {
-            ArithF64::vmax(r, f0, one);
-            return r;
-        }
-        asm("{\n .reg .pred pd, p0, p1;\n setp.ne.u32 pd, %1, 0;\n"
-            " setp.gt.and.f64 p0, %2, %0, !pd;\n setp.gt.and.f64 p1, %3, %0, pd;\n"
-            " @p0 mul.rn.f64 %0, %2, %4;\n @p1 mul.rn.f64 %0, %3, %4;\n}"
-            : "+d"(r)
-            : "r"(dev), "d"(f0), "d"(f1), "d"(one));
-        return r;
-    }
-    __device__ __forceinline__ void set(uint32_t dev, double v, double one) {
-        if (M == 1) {
-            f0 = v;
-            return;
-        }
-        asm("{\n .reg .pred pd;\n setp.ne.u32 pd, %2, 0;\n"
-            " @!pd mul.rn.f64 %0, %3, %4;\n @pd mul.rn.f64 %1, %3, %4;\n}"
-            : "+d"(f0), "+d"(f1)
-            : "r"(dev), "d"(v), "d"(one));
-    }
-    __device__ __forceinline__ double max_all(double one) const {
-        double v = f0;
-        if (M > 1) ArithF64::vmax(v, f1, one);
-        return v;
-    }
-};
-
-template <class A, int M>
-struct FreeTimes<A, M, 2> {                // warp region [device][k][lane] (M ≥ 3)
-    typedef typename A::V V;
-    uint32_t f;                            // shared address of this lane's / placement's device-0 entry
-    __device__ __forceinline__ void init(uint32_t base) {
-        f = base;
-#pragma unroll
-        for (int d = 0; d < M; d++) sts64(f + d * kSlotStride, 0);
-    }
-    __device__ __forceinline__ V max_with(V r, uint32_t dev, double one) {
-        A::vmax(r, A::from_bits(lds64(f + dev * kSlotStride)), one);
-        return r;
-    }
-    __device__ __forceinline__ void set(uint32_t dev, V v, double) { sts64(f + dev * kSlotStride, A::to_bits(v)); }
-    __device__ __forceinline__ V max_all(double one) const {
-        V v = A::from_bits(0);
-#pragma unroll
-        for (int d = 0; d < M; d++) A::vmax(v, A::from_bits(lds64(f + d * kSlotStride)), one);
-        return v;
-    }
-};
+template <class A>
+__device__ __forceinline__ bool same_dev(typename A::V v, uint32_t dev) {
+    return ((A::lo(v) ^ dev) & 7u) == 0;
+}
+// v + (tag(v) ≠ dev ? c : 0): the cut-edge charge
+template <class A>
+__device__ __forceinline__ typename A::V cut_add(typename A::V v, uint32_t dev, uint64_t c) {
+    return same_dev<A>(v, dev) ? v : A::add(v, c);
+}
 
 template <int M>
 struct MemUse {
@@ -383,64 +270,118 @@ struct MemUse {
 template <int M, bool MEM, bool F64, class Gen>
 __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
                                             const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
-                                            uint32_t K, uint64_t cap, double one) {
+                                            uint32_t K8, uint64_t cap) {
     typedef typename std::conditional<F64, ArithF64, ArithU64>::type A;
     typedef typename A::V V;
-    constexpr int KIND = (M > 2) ? 2 : (F64 ? 1 : 0);
-    FreeTimes<A, M, KIND> fr[kNP];
+    V prev[kNP], oth[kNP];
     MemUse<M> mu[kNP];
-    V prev[kNP];
 #pragma unroll
     for (int k = 0; k < kNP; k++) {
-        fr[k].init(lane + free_off + k * 256);
-        if (MEM) mu[k].init();
         prev[k] = A::from_bits(0);
+        oth[k] = A::from_bits(0);
+        if (MEM) mu[k].init();
+        if (M > 2) {
+#pragma unroll
+            for (int d = 0; d < M; d++) sts64(lane + free_off + d * kSlotStride + k * 256, 0);
+        }
     }
-    uint32_t op = ops;
     uint32_t x = xr;
 
-    auto step = [&](uint32_t p, bool fwd) {
-        const uint4 a = lds128(op);
-        const uint4 b = lds128(op + 16);
-        op += sizeof(OpRec);
+    auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
+        const uint4 a = lds128(rec);
+        const uint4 b = lds128(rec + 16);
         const uint64_t cost = ((uint64_t)a.y << 32) | a.x;
-        const uint64_t c = ((uint64_t)a.w << 32) | a.z;
+        const uint64_t c0 = ((uint64_t)a.w << 32) | a.z;
         uint32_t dev[kNP];
-        V r[kNP];
-        gen.devs(p, b.w, dev);
-        if (b.x == kFromPrev) {                // uniform: chain edge, value in a register
 #pragma unroll
-            for (int k = 0; k < kNP; k++) r[k] = A::cut_add(prev[k], dev[k], c);
+        for (int k = 0; k < kNP; k++) dev[k] = gen.dev(k, p, c, b.w);
+        if (M <= 2 && b.z == 0) {
+            // fast path: the only input is the previous step's output (a chain edge)
+#pragma unroll
+            for (int k = 0; k < kNP; k++) {
+                V s;
+                if (M == 1) {
+                    s = prev[k];
+                } else {
+                    const bool same = same_dev<A>(prev[k], dev[k]);   // also: not a cut edge
+                    const V m = A::vmax(A::add(prev[k], c0), oth[k]);
+                    s = same ? prev[k] : m;
+                    oth[k] = same ? oth[k] : prev[k];
+                }
+                prev[k] = A::finish(s, dev[k], cost);
+            }
         } else {
+            V r[kNP];
+            if (b.x == kFromPrev) {
 #pragma unroll
-            for (int k = 0; k < kNP; k++) r[k] = A::cut_add(A::from_bits(lds64(lane + b.x + k * 256)), dev[k], c);
-        }
+                for (int k = 0; k < kNP; k++) r[k] = cut_add<A>(prev[k], dev[k], c0);
+            } else {
+#pragma unroll
+                for (int k = 0; k < kNP; k++) r[k] = cut_add<A>(A::from_bits(lds64(lane + b.x + k * 256)), dev[k], c0);
+            }
+            const uint32_t nx = b.z & 0xFFFFu;
 #pragma unroll 1
-        for (uint32_t q = 0; q < b.z; q++) {   // further inputs (uniform trip count)
-            const uint4 e = lds128(x);
-            x += sizeof(ExtraRec);
-            const uint64_t ce = ((uint64_t)e.y << 32) | e.x;
+            for (uint32_t q = 0; q < nx; q++) {   // further inputs (uniform trip count)
+                const uint4 e = lds128(x);
+                x += sizeof(ExtraRec);
+                const uint64_t ce = ((uint64_t)e.y << 32) | e.x;
 #pragma unroll
-            for (int k = 0; k < kNP; k++)
-                A::vmax(r[k], A::cut_add(A::from_bits(lds64(lane + e.z + k * 256)), dev[k], ce), one);
-        }
+                for (int k = 0; k < kNP; k++)
+                    r[k] = A::vmax(r[k], cut_add<A>(A::from_bits(lds64(lane + e.z + k * 256)), dev[k], ce));
+            }
 #pragma unroll
-        for (int k = 0; k < kNP; k++) {
-            const V s = fr[k].max_with(r[k], dev[k], one);
-            prev[k] = A::finish(s, dev[k], cost);
-            fr[k].set(dev[k], prev[k], one);
-            if (MEM && fwd) mu[k].add(dev[k], mem[p]);
+            for (int k = 0; k < kNP; k++) {
+                V s;
+                if (M == 1) {
+                    s = A::vmax(r[k], prev[k]);
+                } else if (M == 2) {
+                    const bool same = same_dev<A>(prev[k], dev[k]);
+                    s = A::vmax(r[k], same ? prev[k] : oth[k]);
+                    oth[k] = same ? oth[k] : prev[k];
+                } else {
+                    const uint32_t fa = lane + free_off + dev[k] * kSlotStride + k * 256;
+                    s = A::vmax(r[k], A::from_bits(lds64(fa)));
+                    prev[k] = A::finish(s, dev[k], cost);
+                    sts64(fa, A::to_bits(prev[k]));
+                    continue;
+                }
+                prev[k] = A::finish(s, dev[k], cost);
+            }
         }
         if (b.y != kNoStore) {
 #pragma unroll
             for (int k = 0; k < kNP; k++) sts64(lane + b.y + k * 256, A::to_bits(prev[k]));
         }
+        if (MEM && fwd) {
+            const uint64_t m = mem[p];
+#pragma unroll
+            for (int k = 0; k < kNP; k++) mu[k].add(dev[k], m);
+        }
     };
-    for (uint32_t p = 0; p < K; p++) step(p, true);
-    for (uint32_t p = K; p-- > 0;) step(p, false);
+    const uint32_t G = K8 / 8;
+    for (uint32_t g = 0; g < G; g++) {           // forward, π order
+        gen.refresh(g);
+        const uint32_t rec = ops + g * 8 * (uint32_t)sizeof(OpRec);
+#pragma unroll
+        for (uint32_t c = 0; c < 8; c++) step(rec + c * (uint32_t)sizeof(OpRec), g * 8 + c, c, true);
+    }
+    for (uint32_t g = G; g-- > 0;) {             // backward, reverse π order
+        gen.refresh(g);
+        const uint32_t rec = ops + (2 * K8 - 1 - g * 8) * (uint32_t)sizeof(OpRec);
+#pragma unroll
+        for (int c = 7; c >= 0; c--) step(rec - (uint32_t)c * (uint32_t)sizeof(OpRec), g * 8 + c, c, false);
+    }
 #pragma unroll
     for (int k = 0; k < kNP; k++) {
-        mk[k] = A::ps(fr[k].max_all(one));
+        V v;
+        if (M <= 2) {
+            v = A::vmax(prev[k], oth[k]);
+        } else {
+            v = A::from_bits(0);
+#pragma unroll
+            for (int d = 0; d < M; d++) v = A::vmax(v, A::from_bits(lds64(lane + free_off + d * kSlotStride + k * 256)));
+        }
+        mk[k] = A::ps(v);
         if (MEM && mu[k].over(cap)) mk[k] = kInfeasible;
     }
 }
@@ -521,21 +462,21 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams P) {
         if (GEN == GEN_GRAY) {
             GrayGen<M> g;
             g.init(idx, P.K);
-            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap, P.one);
+            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap);
         } else if (GEN == GEN_RANDOM) {
             RandomGen<M> g;
             g.init(idx, P.seed, P.K);
-            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap, P.one);
+            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap);
         } else if (GEN == GEN_PERTURB) {
             PerturbGen<M> g;
             g.init(idx, P.seed, P.K, P.tau);
-            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap, P.one);
+            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap);
         } else {
             ExplicitGen g;
 #pragma unroll
             for (int k = 0; k < kNP; k++) g.row[k] = P.g_place + (idx[k] - P.begin) * (uint64_t)P.K;
             g.orig = orig;
-            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K, P.cap, P.one);
+            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap);
         }
 #pragma unroll
         for (int k = 0; k < kNP; k++) {
@@ -622,24 +563,27 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
         improve = (U.round == 0) || (mk < s[SC_BEST_MK]);
     }
     __syncthreads();
-    const uint64_t idx = idx_s;
+    uint64_t ii[kNP];
+#pragma unroll
+    for (int k = 0; k < kNP; k++) ii[k] = idx_s;
     for (uint32_t p = threadIdx.x; p < U.K; p += blockDim.x) {
-        const uint64_t ii[1] = {idx};
-        uint32_t d[1];
+        uint32_t d;
         if (GEN == GEN_GRAY) {
             GrayGen<M> g;
             g.init(ii, U.K);
-            g.devs(p, 0, d);
+            d = g.dev(0, p, p % 8, 0);
         } else if (GEN == GEN_RANDOM) {
             RandomGen<M> g;
             g.init(ii, U.seed, U.K);
-            g.devs(p, 0, d);
+            g.refresh(p / 8);
+            d = g.dev(0, p, p % 8, 0);
         } else {
             PerturbGen<M> g;
             g.init(ii, U.seed, U.K, U.tau);
-            g.devs(p, U.base[p], d);
+            g.refresh(p / 8);
+            d = g.dev(0, p, p % 8, U.base[p]);
         }
-        U.winner[p] = (uint8_t)d[0];
+        U.winner[p] = (uint8_t)d;
     }
     __syncthreads();
     OpRec *ops = reinterpret_cast<OpRec *>(U.image);
@@ -648,7 +592,7 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
         if (GEN == GEN_PERTURB) {
             U.base[p] = d;
             ops[p].base = d;
-            ops[2 * U.K - 1 - p].base = d;
+            ops[2 * U.K8 - 1 - p].base = d;
         }
         if (improve) U.best_place[p] = d;
     }

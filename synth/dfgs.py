@@ -348,6 +348,13 @@ def random_dag(seed, K, avg_deg=1.5, max_in=4, max_cost=1000, max_bytes=2000, bw
             lo = 0 if window is None else max(0, v - window)
             u = rng.randrange(lo, v) if rng.random() < 0.5 else max(0, v - 1 - rng.randrange(min(v, 4)))
             edges.append((u, v, rng.randint(0, max_bytes)))
+    if window is not None:
+        # like a training DFG, let only the last op be a sink: a sink's forward
+        # finish time stays live until its own backward step
+        has_out = set(u for u, _, _ in edges)
+        for v in range(K - 1):
+            if v not in has_out:
+                edges.append((v, rng.randint(v + 1, min(K - 1, v + window)), rng.randint(0, max_bytes)))
     ids = list(range(K))
     if shuffle_ids and window is None:
         ids = rng.sample(range(10 * K), K)
