@@ -170,6 +170,13 @@ struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops
     }
     __device__ __forceinline__ uint32_t dev(int k, uint32_t, uint32_t c, uint32_t bs) const {
         if (M == 1) return 0;
+        if (M == 2) {
+            // device = base + [u < τ], read modulo 2 (see Dev<M>): the byte
+            // is extracted with one PRMT and the comparison is a sign bit
+            const uint32_t half = (c < 4) ? (uint32_t)w[k] : (uint32_t)(w[k] >> 32);
+            const uint32_t u = __byte_perm(half, 0, 0x4440u | (c & 3u));
+            return bs + ((uint32_t)((int)u - (int)tau[k]) >> 31);
+        }
         const uint32_t u = (uint32_t)(w[k] >> (8 * c)) & 0xFFu;
         uint32_t flip;
         if (M == 2) flip = bs ^ 1u;
@@ -235,14 +242,22 @@ struct ArithF64 {
     }
 };
 
-template <class A>
+// For M = 2 a device is any integer read modulo 2 (the PERTURB generator
+// yields base + flip ∈ {0, 1, 2}); tags compare on bit 0 only.  Otherwise
+// devices are 0..M−1 and tags compare on the 3 tag bits.
+template <int M>
+struct Dev {
+    static constexpr uint32_t mask = (M == 2) ? 1u : 7u;
+    static __device__ __forceinline__ uint32_t canon(uint32_t d) { return d & mask; }
+};
+template <class A, int M>
 __device__ __forceinline__ bool same_dev(typename A::V v, uint32_t dev) {
-    return ((A::lo(v) ^ dev) & 7u) == 0;
+    return ((A::lo(v) ^ dev) & Dev<M>::mask) == 0;
 }
 // v + (tag(v) ≠ dev ? c : 0): the cut-edge charge
-template <class A>
+template <class A, int M>
 __device__ __forceinline__ typename A::V cut_add(typename A::V v, uint32_t dev, uint64_t c) {
-    return same_dev<A>(v, dev) ? v : A::add(v, c);
+    return same_dev<A, M>(v, dev) ? v : A::add(v, c);
 }
 
 template <int M>
@@ -302,8 +317,25 @@ __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint3
                 V s;
                 if (M == 1) {
                     s = prev[k];
+                } else if (F64) {
+                    // x = 1 iff the chain edge is cut (then free[dev] = oth),
+                    // x = 0 iff dev = tag(prev) (then free[dev] = prev).  With
+                    // cut = (double)x and same = 1 − cut, all exact:
+                    //   t = prev + cut·c0,  f = oth − same·2^50 (< 0 if same),
+                    //   s = max(t, f),      oth' = cut·prev + same·oth
+                    const uint32_t xbit = (A::lo(prev[k]) ^ dev[k]) & 1u;
+                    const double cut = __hiloint2double((int)(xbit * 0x3FF00000u), 0);
+                    const double same = __hiloint2double((int)((1u - xbit) * 0x3FF00000u), 0);
+                    const double pv = reinterpret_cast<const double &>(prev[k]);
+                    const double ov = reinterpret_cast<const double &>(oth[k]);
+                    const double t = __fma_rn(__longlong_as_double((long long)c0), cut, pv);
+                    const double f = __fma_rn(same, -1125899906842624.0, ov);
+                    const double sv = t > f ? t : f;
+                    const double on = __fma_rn(cut, pv, __dmul_rn(same, ov));
+                    s = reinterpret_cast<const V &>(sv);
+                    oth[k] = reinterpret_cast<const V &>(on);
                 } else {
-                    const bool same = same_dev<A>(prev[k], dev[k]);   // also: not a cut edge
+                    const bool same = same_dev<A, M>(prev[k], dev[k]);   // also: not a cut edge
                     const V m = A::vmax(A::add(prev[k], c0), oth[k]);
                     s = same ? prev[k] : m;
                     oth[k] = same ? oth[k] : prev[k];
@@ -314,10 +346,10 @@ __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint3
             V r[kNP];
             if (b.x == kFromPrev) {
 #pragma unroll
-                for (int k = 0; k < kNP; k++) r[k] = cut_add<A>(prev[k], dev[k], c0);
+                for (int k = 0; k < kNP; k++) r[k] = cut_add<A, M>(prev[k], dev[k], c0);
             } else {
 #pragma unroll
-                for (int k = 0; k < kNP; k++) r[k] = cut_add<A>(A::from_bits(lds64(lane + b.x + k * 256)), dev[k], c0);
+                for (int k = 0; k < kNP; k++) r[k] = cut_add<A, M>(A::from_bits(lds64(lane + b.x + k * 256)), dev[k], c0);
             }
             const uint32_t nx = b.z & 0xFFFFu;
 #pragma unroll 1
@@ -327,7 +359,7 @@ __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint3
                 const uint64_t ce = ((uint64_t)e.y << 32) | e.x;
 #pragma unroll
                 for (int k = 0; k < kNP; k++)
-                    r[k] = A::vmax(r[k], cut_add<A>(A::from_bits(lds64(lane + e.z + k * 256)), dev[k], ce));
+                    r[k] = A::vmax(r[k], cut_add<A, M>(A::from_bits(lds64(lane + e.z + k * 256)), dev[k], ce));
             }
 #pragma unroll
             for (int k = 0; k < kNP; k++) {
@@ -335,7 +367,7 @@ __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint3
                 if (M == 1) {
                     s = A::vmax(r[k], prev[k]);
                 } else if (M == 2) {
-                    const bool same = same_dev<A>(prev[k], dev[k]);
+                    const bool same = same_dev<A, M>(prev[k], dev[k]);
                     s = A::vmax(r[k], same ? prev[k] : oth[k]);
                     oth[k] = same ? oth[k] : prev[k];
                 } else {
@@ -355,7 +387,7 @@ __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint3
         if (MEM && fwd) {
             const uint64_t m = mem[p];
 #pragma unroll
-            for (int k = 0; k < kNP; k++) mu[k].add(dev[k], m);
+            for (int k = 0; k < kNP; k++) mu[k].add(Dev<M>::canon(dev[k]), m);
         }
     };
     const uint32_t G = K8 / 8;
@@ -583,7 +615,7 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
             g.refresh(p / 8);
             d = g.dev(0, p, p % 8, U.base[p]);
         }
-        U.winner[p] = (uint8_t)d;
+        U.winner[p] = (uint8_t)Dev<M>::canon(d);
     }
     __syncthreads();
     OpRec *ops = reinterpret_cast<OpRec *>(U.image);
