@@ -43,7 +43,7 @@
 
 namespace pp {
 
-constexpr int kNP = 2;                          // placements per lane
+constexpr int kNP = 4;                          // placements per lane
 constexpr uint32_t kSlotStride = 256u * kNP;    // bytes between consecutive slots
 
 constexpr uint32_t kFromPrev = 0xFFFFFFFFu;     // OpRec.src_off: previous step's output (register)

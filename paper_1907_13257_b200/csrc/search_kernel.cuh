@@ -2,10 +2,10 @@
 // forward+backward in-order list schedule of each candidate placement, and
 // the (makespan, index) argmin, for sm_100a.
 //
-// Kernel shape (DESIGN.md Â§Kernels): LANE PER PLACEMENT, kNP = 2 placements
-// per lane.  A warp evaluates 64 candidate placements in lockstep over the
+// Kernel shape (DESIGN.md Â§Kernels): LANE PER PLACEMENT, kNP placements per
+// lane.  A warp evaluates 32Â·kNP candidate placements in lockstep over the
 // same DFG records, so every record read is a warp-uniform shared-memory
-// broadcast shared by 64 placements.  The recurrence (PAPER.md:443â€“453
+// broadcast shared by 32Â·kNP placements.  The recurrence (PAPER.md:443â€“453
 // dependency with Î”_e, :465â€“476 one op at a time per device, :497â€“503
 // back-to-back ops + overlapped communication; readings R1, R2):
 //
@@ -20,8 +20,9 @@
 // free time of the other device (registers), for M â‰¥ 3 free[] in the warp's
 // shared region.  Chain edges (the first input produced by the previous step)
 // are read from `prev`; other inputs from liveness-allocated shared slots.
-// The schedule loop is unrolled by 8 ops (one generator word per 8 ops); K is
-// padded to a multiple of 8 with state-preserving no-op records.
+// The schedule loop runs over 8-op groups (one generator word per group),
+// each as two half-groups of 4 unrolled steps; K is padded to a multiple of 8
+// with state-preserving no-op records.
 //
 // The DFG image is staged global â†’ shared once per CTA with bulk TMA copies
 // (cp.async.bulk + mbarrier).  No tensor cores: integer max-plus work.
@@ -95,6 +96,7 @@ struct GrayGen {                           // O5: reflected M-ary Gray code
         for (int k = 0; k < N; k++) one(i[k], K, lo[k], hi[k]);
     }
     __device__ __forceinline__ void refresh(uint32_t) {}
+    __device__ __forceinline__ void sub(uint32_t) {}
     __device__ __forceinline__ uint32_t dev(int k, uint32_t p, uint32_t, uint32_t) const {
         if (M == 1) return 0;
         const bool first = p < (uint32_t)PF;
@@ -111,6 +113,7 @@ struct RandomGen {                         // O6 RANDOM: b bits per op, P = 8Â·â
     uint64_t keep[kNP];  // 0 for candidate 0 (all zeros), else ~0
     uint64_t w[kNP];     // current word
     uint32_t wg[kNP];    // the current group's 8Â·b bits
+    uint32_t wh[kNP];    // the current half-group's 4Â·b bits
     uint32_t cur;        // word index held in w (shared by the lane's placements)
     template <int N>
     __device__ __forceinline__ void init(const uint64_t (&i)[N], uint64_t seed, uint32_t K) {
@@ -122,6 +125,7 @@ struct RandomGen {                         // O6 RANDOM: b bits per op, P = 8Â·â
             keep[k] = (i[k] == 0) ? 0ull : ~0ull;
             w[k] = 0;
             wg[k] = 0;
+            wh[k] = 0;
         }
         cur = 0xFFFFFFFFu;
     }
@@ -137,9 +141,15 @@ struct RandomGen {                         // O6 RANDOM: b bits per op, P = 8Â·â
 #pragma unroll
         for (int k = 0; k < kNP; k++) wg[k] = (uint32_t)(w[k] >> sh);
     }
-    __device__ __forceinline__ uint32_t dev(int k, uint32_t, uint32_t c, uint32_t) const {
+    // half-group h (ops 8g + 4h .. 8g + 4h + 3)
+    __device__ __forceinline__ void sub(uint32_t h) {
+#pragma unroll
+        for (int k = 0; k < kNP; k++) wh[k] = wg[k] >> (4 * b * h);
+    }
+    // cc = position within the half-group (compile-time in the schedule loop)
+    __device__ __forceinline__ uint32_t dev(int k, uint32_t, uint32_t cc, uint32_t) const {
         if (M == 1) return 0;
-        const uint32_t x = (wg[k] >> (b * c)) & ((1u << b) - 1);
+        const uint32_t x = (wh[k] >> (b * cc)) & ((1u << b) - 1);
         return ((M & (M - 1)) == 0) ? x : (x * M) >> b;
     }
 };
@@ -148,6 +158,7 @@ template <int M>
 struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops per word
     uint64_t key1[kNP], key2[kNP];
     uint64_t w[kNP], y[kNP];
+    uint32_t uh[kNP], yh[kNP];   // the current half-group's u / y bytes
     uint32_t tau[kNP];   // 0 for candidate 0 (the base itself)
     template <int N>
     __device__ __forceinline__ void init(const uint64_t (&i)[N], uint64_t seed, uint32_t K, uint32_t tau_) {
@@ -158,6 +169,7 @@ struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops
             key2[k] = (seed ^ 0x8CB92BA72F3D8DD7ull) + kGamma * (i[k] * Wd + 1);
             tau[k] = (i[k] == 0) ? 0u : tau_;
             w[k] = y[k] = 0;
+            uh[k] = yh[k] = 0;
         }
     }
     __device__ __forceinline__ void refresh(uint32_t g) {
@@ -168,19 +180,23 @@ struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops
             if (M > 2) y[k] = mix64(key2[k] + kGamma * g);
         }
     }
-    __device__ __forceinline__ uint32_t dev(int k, uint32_t, uint32_t c, uint32_t bs) const {
+    __device__ __forceinline__ void sub(uint32_t h) {
+#pragma unroll
+        for (int k = 0; k < kNP; k++) {
+            uh[k] = h ? (uint32_t)(w[k] >> 32) : (uint32_t)w[k];
+            if (M > 2) yh[k] = h ? (uint32_t)(y[k] >> 32) : (uint32_t)y[k];
+        }
+    }
+    // cc = position within the half-group (compile-time in the schedule loop)
+    __device__ __forceinline__ uint32_t dev(int k, uint32_t, uint32_t cc, uint32_t bs) const {
         if (M == 1) return 0;
+        const uint32_t u = __byte_perm(uh[k], 0, 0x4440u | (cc & 3u));
         if (M == 2) {
-            // device = base + [u < Ï„], read modulo 2 (see Dev<M>): the byte
-            // is extracted with one PRMT and the comparison is a sign bit
-            const uint32_t half = (c < 4) ? (uint32_t)w[k] : (uint32_t)(w[k] >> 32);
-            const uint32_t u = __byte_perm(half, 0, 0x4440u | (c & 3u));
+            // device = base + [u < Ï„], read modulo 2 (see Dev<M>): one PRMT and a sign bit
             return bs + ((uint32_t)((int)u - (int)tau[k]) >> 31);
         }
-        const uint32_t u = (uint32_t)(w[k] >> (8 * c)) & 0xFFu;
-        uint32_t flip;
-        if (M == 2) flip = bs ^ 1u;
-        else flip = (bs + 1 + ((uint32_t)(y[k] >> (8 * c)) & 0xFFu) % (uint32_t)(M > 1 ? M - 1 : 1)) % (uint32_t)M;
+        const uint32_t yv = __byte_perm(yh[k], 0, 0x4440u | (cc & 3u));
+        const uint32_t flip = (bs + 1 + yv % (uint32_t)(M > 1 ? M - 1 : 1)) % (uint32_t)M;
         return (u < tau[k]) ? flip : bs;
     }
 };
@@ -189,6 +205,7 @@ struct ExplicitGen {                       // rows of a [count][K] uint8 array
     const uint8_t *row[kNP];
     const uint32_t *orig;
     __device__ __forceinline__ void refresh(uint32_t) {}
+    __device__ __forceinline__ void sub(uint32_t) {}
     __device__ __forceinline__ uint32_t dev(int k, uint32_t p, uint32_t, uint32_t) const { return row[k][orig[p]]; }
 };
 
@@ -393,15 +410,24 @@ __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint3
     const uint32_t G = K8 / 8;
     for (uint32_t g = 0; g < G; g++) {           // forward, Ï€ order
         gen.refresh(g);
-        const uint32_t rec = ops + g * 8 * (uint32_t)sizeof(OpRec);
+#pragma unroll 1
+        for (uint32_t h = 0; h < 2; h++) {
+            gen.sub(h);
+            const uint32_t rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
 #pragma unroll
-        for (uint32_t c = 0; c < 8; c++) step(rec + c * (uint32_t)sizeof(OpRec), g * 8 + c, c, true);
+            for (uint32_t cc = 0; cc < 4; cc++) step(rec + cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, true);
+        }
     }
     for (uint32_t g = G; g-- > 0;) {             // backward, reverse Ï€ order
         gen.refresh(g);
-        const uint32_t rec = ops + (2 * K8 - 1 - g * 8) * (uint32_t)sizeof(OpRec);
+#pragma unroll 1
+        for (uint32_t h = 2; h-- > 0;) {
+            gen.sub(h);
+            const uint32_t rec = ops + (2 * K8 - 1 - g * 8 - h * 4) * (uint32_t)sizeof(OpRec);
 #pragma unroll
-        for (int c = 7; c >= 0; c--) step(rec - (uint32_t)c * (uint32_t)sizeof(OpRec), g * 8 + c, c, false);
+            for (int cc = 3; cc >= 0; cc--)
+                step(rec - (uint32_t)cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, false);
+        }
     }
 #pragma unroll
     for (int k = 0; k < kNP; k++) {
@@ -608,12 +634,14 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
             RandomGen<M> g;
             g.init(ii, U.seed, U.K);
             g.refresh(p / 8);
-            d = g.dev(0, p, p % 8, 0);
+            g.sub((p / 4) & 1);
+            d = g.dev(0, p, p % 4, 0);
         } else {
             PerturbGen<M> g;
             g.init(ii, U.seed, U.K, U.tau);
             g.refresh(p / 8);
-            d = g.dev(0, p, p % 8, U.base[p]);
+            g.sub((p / 4) & 1);
+            d = g.dev(0, p, p % 4, U.base[p]);
         }
         U.winner[p] = (uint8_t)Dev<M>::canon(d);
     }
