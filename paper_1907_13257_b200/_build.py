@@ -17,6 +17,7 @@ ROOT = os.path.dirname(HERE)
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+EXTRA = os.environ.get("PP_NVCC_FLAGS", "").split()   # experiments only
 
 
 def _nccl_include():
@@ -60,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(job):
         src, obj, extra = job
-        cmd = [nvcc, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, src), "-o", os.path.join(BUILD, obj)]
+        cmd = [nvcc, *ARCH, *COMMON, *EXTRA, *extra, "-c", os.path.join(CSRC, src), "-o", os.path.join(BUILD, obj)]
         if src.endswith(".cu"):
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
         else:

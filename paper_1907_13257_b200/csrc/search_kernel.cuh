@@ -34,6 +34,10 @@
 
 #include "internal.h"
 
+#ifndef PP_MIN_CTAS
+#define PP_MIN_CTAS 2   // resident CTAs per SM the register allocation targets (measured best)
+#endif
+
 namespace pp {
 
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
@@ -450,7 +454,7 @@ __device__ __forceinline__ bool lex_less(uint64_t m1, uint64_t i1, uint64_t m2, 
 
 // ------------------------------------------------------------------ kernel
 template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64>
-__global__ void __launch_bounds__(256) search_kernel(const KParams P) {
+__global__ void __launch_bounds__(256, PP_MIN_CTAS) search_kernel(const KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t mbar;
     __shared__ uint64_t red_mk[8], red_i[8];

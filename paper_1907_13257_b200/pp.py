@@ -282,13 +282,7 @@ class Comm:
     (the group only carries the 128-byte unique id)."""
 
     def __init__(self, rank, world, device, group=None):
-        import torch.distributed as dist
-        uid = (C.c_uint8 * 128)()
-        if rank == 0:
-            _check(lib().pp_comm_get_unique_id(uid))
-        obj = [bytes(uid)]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        uid = (C.c_uint8 * 128).from_buffer_copy(exchange_unique_id(rank, group))
         h = C.c_void_p()
         _check(lib().pp_comm_init(uid, rank, world, device, C.byref(h)))
         self._h = h
@@ -298,6 +292,18 @@ class Comm:
         if getattr(self, "_h", None):
             lib().pp_comm_destroy(self._h)
             self._h = None
+
+
+def exchange_unique_id(rank, group=None) -> bytes:
+    """Rank 0 creates the 128-byte NCCL unique id; a torch.distributed
+    broadcast (any backend) hands it to every rank."""
+    import torch.distributed as dist
+    uid = (C.c_uint8 * 128)()
+    if rank == 0:
+        _check(lib().pp_comm_get_unique_id(uid))
+    obj = [bytes(uid)]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
 
 
 def rank_slice(count, rank, world):

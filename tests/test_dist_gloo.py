@@ -1,0 +1,97 @@
+"""Multi-process (gloo, CPU) tests of the N > 1 protocol of pp_search_best
+(SURVEY.md §8(e)): contiguous rank slices, the packed (makespan << 3 | rank)
+min key, the winner-index exchange, and the NCCL unique-id hand-off.
+
+The per-slice argmin here is the oracle's (no GPU on this box); slicing, key
+packing and decoding are the product's exported host functions, and the
+collectives follow the order of capi.cpp (min all-reduce of the key, then min
+all-reduce of the winner's index).  The result must not depend on the number
+of ranks (GPU-count invariance)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+I64_MAX = (1 << 63) - 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _sharded_search(rank, world, spec_name, M, gen, seed, count, rounds, tau):
+    import oracle as O
+    import synth
+    import paper_1907_13257_b200 as pp
+    spec = getattr(synth, spec_name)() if spec_name != "random" else synth.random_dag(3, 40, window=8)
+    od = O.Dfg.from_spec(spec)
+    base = np.zeros(od.K, dtype=np.uint8)
+    best = None
+    for r in range(rounds):
+        b, e = pp.rank_slice(count, rank, world)
+        if e > b:
+            mk, idx = od.round(M, gen, seed + r, tau, base, b, e)
+        else:
+            mk, idx = pp.INFEASIBLE, pp.INFEASIBLE
+        key = torch.tensor([pp.pack_key(mk, rank)], dtype=torch.int64)
+        dist.all_reduce(key, op=dist.ReduceOp.MIN)
+        k = int(key.item())
+        contrib = torch.tensor([idx if pp.key_rank(k) == rank else I64_MAX], dtype=torch.int64)
+        dist.all_reduce(contrib, op=dist.ReduceOp.MIN)
+        wmk, widx = pp.key_makespan(k), int(contrib.item())
+        if best is None or wmk < best[0]:
+            best = (wmk, widx, r)
+        base = O.gen(od.K, M, gen, seed + r, tau, base, widx)   # every rank moves to the winner
+    return best
+
+
+def _worker(rank, world, port, cases, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    sys.path.insert(0, ROOT)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1907_13257_b200 as pp
+        uid = pp.exchange_unique_id(rank)
+        res = {"uid": uid.hex(), "best": [_sharded_search(rank, world, *c) for c in cases]}
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+CASES = [("toy12", 2, 0, 0, 4096, 1, 0),          # GRAY exhaustive
+         ("toy12", 3, 2, 17, 301, 4, 40),         # PERTURB rounds, ragged slices
+         ("random", 4, 1, 99, 1001, 1, 0),        # RANDOM
+         ("biglstm", 2, 2, 5, 203, 3, 16)]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_search_is_rank_count_invariant(world):
+    import oracle as O
+    import synth
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    results = [out[r] for r in range(world)]
+    assert len({r["uid"] for r in results}) == 1 and len(results[0]["uid"]) == 256
+    for ci, (name, M, gen, seed, count, rounds, tau) in enumerate(CASES):
+        spec = getattr(synth, name)() if name != "random" else synth.random_dag(3, 40, window=8)
+        ref = O.Dfg.from_spec(spec).search(M, gen, seed, count, rounds=rounds, tau=tau)
+        for r in range(world):
+            assert tuple(results[r]["best"][ci]) == (ref.best_makespan_ps, ref.best_index, ref.best_round)

@@ -245,3 +245,30 @@ def test_error_codes_match_oracle():
     with pytest.raises(pp.PPError) as e:
         g.search_best(2, pp.GEN_GRAY, 0, 10)
     assert e.value.code == -4
+
+
+def test_nccl_communicator_single_rank(dfgs):
+    """The NCCL path of pp_search_best (key and index min all-reduces every
+    round, winner decoded from the reduced key) at world size 1 equals the
+    communicator-free path."""
+    import os
+    import socket
+    import torch.distributed as dist
+    spec, g, od = dfgs["gnmt"]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = pp.Comm(0, 1, 0)
+        a = g.search_best(2, pp.GEN_PERTURB, 7, 30_001, rounds=3, tau=8, comm=comm)
+        b = g.search_best(2, pp.GEN_PERTURB, 7, 30_001, rounds=3, tau=8)
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+    assert (a.best_makespan_ps, a.best_index, a.best_round) == (b.best_makespan_ps, b.best_index, b.best_round)
+    assert np.array_equal(a.placement, b.placement)
+    o = od.search(2, O.GEN_PERTURB, 7, 30_001, rounds=3, tau=8)
+    assert a.best_makespan_ps == o.best_makespan_ps and a.best_index == o.best_index

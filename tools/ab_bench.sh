@@ -1,0 +1,14 @@
+#!/bin/bash
+# A/B: bench PERTURB and RANDOM with alternative libpp.so builds (tools/libpp_*.so)
+set -u
+cp paper_1907_13257_b200/libpp.so /tmp/libpp_default.so
+for lib in /tmp/libpp_default.so tools/libpp_*.so; do
+  [ -f "$lib" ] || continue
+  cp "$lib" paper_1907_13257_b200/libpp.so
+  for g in perturb random; do
+    c=$([ $g = random ] && echo 100000000 || echo 10000000)
+    timeout 300 python bench.py --gen $g --count $c --no-cpu-baseline --steps 3 > /tmp/ab.json 2>/dev/null
+    python -c "import json,sys;d=json.load(open('/tmp/ab.json'));print('$(basename $lib) $g', round(d['value']/1e9,3), 'G/s frac', round(d['roofline']['frac'],3), 'kern_ms', round(d['roofline']['kernel_ms_avg'],3))"
+  done
+done
+cp /tmp/libpp_default.so paper_1907_13257_b200/libpp.so
