@@ -107,6 +107,17 @@ def peaks(sm_count, clock_mhz):
             "smem_bytes_per_s": sm_count * 128 * clock_mhz * 1e6}
 
 
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the search
+    kernel from the committed ncu --set full capture (profiles/r*_traffic.json)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files:
+        return None
+    d = json.load(open(files[-1]))
+    return d["dram_bytes_read_per_launch"] + d["dram_bytes_write_per_launch"]
+
+
 def measured_clock():
     try:
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"]), "measured"
@@ -283,7 +294,8 @@ def run_pp(args):
             "gpu_launches": int(launches),
             "roofline": {"bound": "alu", "achieved": achieved_ops / 1e12, "peak": pk["int32_ops_per_s"] / 1e12,
                          "unit": "Tops/s (int32)", "frac": achieved_ops / pk["int32_ops_per_s"],
-                         "traffic": None, "kernel": f"pp::search_kernel<{M},{args.gen.upper()}>",
+                         "traffic": ncu_traffic(), "traffic_unit": "DRAM bytes per launch (ncu)",
+                         "kernel": f"pp::search_kernel<{M},{args.gen.upper()}>",
                          "kernel_ms_avg": kern_avg_s * 1e3, "kernel_share_of_step": kern_ms_max / tot_ms,
                          "alg_ops_per_placement": ops, "alg_smem_bytes_per_placement": smem_b,
                          "smem_frac": achieved_smem / pk["smem_bytes_per_s"],
