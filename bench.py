@@ -35,9 +35,20 @@ UNIT = "placements/s"
 SEED = 13257
 
 
+WORKLOADS = {"inception_v3": "Inception-V3-shaped (synth.inception_v3, batch 64)",
+             "gnmt": "GNMT-shaped (synth.gnmt, 4+4 LSTM x 1024, 18 chunks)",
+             "biglstm": "BigLSTM-shaped (synth.biglstm, 2 x LSTM 8192, 30 chunks)",
+             "toy12": "toy-12 (SURVEY 8(d) config 1)"}
+
+
 def workload(args):
-    spec = synth.inception_v3()
-    return spec
+    return getattr(synth, args.workload)()
+
+
+def scenario(args, t1, grad):
+    if args.workload == "toy12":
+        return synth.toy12_scenario(t1)
+    return synth.sweep_scenario(args.workload, t1, grad)
 
 
 def alg_counts(spec):
@@ -158,7 +169,7 @@ def run_reference(args):
         t = time.perf_counter()
         od = O.Dfg.from_spec(spec)
         r = od.search(args.M, gen, SEED, per_round, rounds=rounds, tau=args.tau)
-        sc = synth.sweep_scenario("inception_v3", od.t1, od.grad_bytes)
+        sc = scenario(args, od.t1, od.grad_bytes)
         cells = O.Scenario.from_spec(sc).project([1, args.M], [od.t1, r.best_makespan_ps], args.nmax)
         x = O.crossover(cells, [1, args.M], args.nmax)
         dt = time.perf_counter() - t
@@ -173,7 +184,7 @@ def run_reference(args):
             "config": config_dict(args, spec, per_step=n_step),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"{rounds} rounds x {per_round} {args.gen.upper()} candidates of the "
-                                       f"Inception-V3-shaped DFG per step (the GPU step runs {rounds} x {args.count}) "
+                                       f"{args.workload}-shaped DFG per step (the GPU step runs {rounds} x {args.count}) "
                                        f"+ projection N=1..{args.nmax} + crossover"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "crossover_n_star": x.n_star}
@@ -184,8 +195,8 @@ def run_reference(args):
 def config_dict(args, spec, per_step=None):
     gen = (f"PERTURB tau={args.tau}/256, {args.rounds} rounds x {args.count:.0e}" if args.gen == "perturb"
            else f"RANDOM {args.count:.0e}").replace("+0", "")
-    return {"workload": f"inception_v3_shaped_M{args.M}_{args.gen}_{args.count * args.rounds:.0e}".replace("+0", ""),
-            "dfg": "Inception-V3-shaped (synth.inception_v3, batch 64)", "K": len(spec["fwd_ps"]),
+    return {"workload": f"{args.workload}_shaped_M{args.M}_{args.gen}_{args.count * args.rounds:.0e}".replace("+0", ""),
+            "dfg": WORKLOADS[args.workload], "K": len(spec["fwd_ps"]),
             "E": len(spec["edge_src"]), "M": args.M, "generator": gen + " (SplitMix64)", "seed": SEED,
             "candidates_per_step": per_step or args.count * args.rounds,
             "projection": f"M in {{1,{args.M}}}, N=1..{args.nmax}, EQ5, ring AR on",
@@ -213,7 +224,7 @@ def run_pp(args):
     spec = workload(args)
     g = pp.Dfg(spec, device=local)
     M = args.M
-    sc = synth.sweep_scenario("inception_v3", g.t1, g.grad_bytes)
+    sc = scenario(args, g.t1, g.grad_bytes)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def barrier():
@@ -327,6 +338,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="pp", choices=["pp", "reference"])
     ap.add_argument("--M", type=int, default=2)
+    ap.add_argument("--workload", default="inception_v3", choices=sorted(WORKLOADS))
     ap.add_argument("--count", type=int, default=10_000_000, help="candidates per round")
     ap.add_argument("--rounds", type=int, default=10)
     ap.add_argument("--gen", default="perturb", choices=["perturb", "random"])

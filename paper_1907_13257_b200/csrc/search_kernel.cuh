@@ -304,7 +304,7 @@ struct MemUse {
 // lane: shared address of this lane's entry in its warp region (region +
 // 8·lane); placement k's copy of a slot is at +k·256.
 template <int M, bool MEM, bool F64, class Gen>
-__device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
+__device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
                                             const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
                                             uint32_t K8, uint64_t cap) {
     typedef typename std::conditional<F64, ArithF64, ArithU64>::type A;
@@ -446,6 +446,145 @@ __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint3
         mk[k] = A::ps(v);
         if (MEM && mu[k].over(cap)) mk[k] = kInfeasible;
     }
+}
+
+// ------------------------------------------ M = 2, tagged-f64 specialisation
+// State per placement: prev = finish time of the previous step as an exact
+// integer double (UNTAGGED), pdev = its device, oth = free time of the other
+// device (untagged).  Slot values stay tagged (t + d·ulp(t)) for the
+// non-chain reads; the tag is set only when a value is stored.  With
+// cut = [dev ≠ pdev] ∈ {0.0, 1.0} and same = 1 − cut, a chain step is
+//   s = max(prev + cut·c0, oth − same·2^50)      (free[dev] = prev if same, oth if cut)
+//   oth' = cut·prev + same·oth,  prev' = s + cost,  pdev' = dev
+// — every operation exact on integers < 2^49; only the max needs a select.
+__device__ __forceinline__ double one_if(uint32_t x) {   // x ∈ {0,1} → 0.0 / 1.0
+    return __hiloint2double((int)(x * 0x3FF00000u), 0);
+}
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ double with_tag(double v, uint32_t dev) {
+    return __hiloint2double(__double2hiint(v), __double2loint(v) | (int)dev);
+}
+__device__ __forceinline__ double clear_tag(double v) {
+    return __hiloint2double(__double2hiint(v), __double2loint(v) & ~7);
+}
+// v + [tag(v) ≠ dev]·c for a tagged slot value (M = 2: tags compare on bit 0)
+__device__ __forceinline__ double cut_add_m2(double v, uint32_t dev, double c) {
+    return __fma_rn(c, one_if(((uint32_t)__double2loint(v) ^ dev) & 1u), v);
+}
+
+template <bool MEM, class Gen>
+__device__ __forceinline__ void schedule_m2_f64(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
+                                                const uint64_t *__restrict__ mem, uint32_t lane, uint32_t K8,
+                                                uint64_t cap) {
+    constexpr double kBig = 1125899906842624.0;   // 2^50
+    double prev[kNP], oth[kNP];
+    uint32_t pdev[kNP];
+    MemUse<2> mu[kNP];
+#pragma unroll
+    for (int k = 0; k < kNP; k++) {
+        prev[k] = 0.0;
+        oth[k] = 0.0;
+        pdev[k] = 0;
+        if (MEM) mu[k].init();
+    }
+    uint32_t x = xr;
+
+    auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
+        const uint4 a = lds128(rec);
+        const uint4 b = lds128(rec + 16);
+        const double cost = __hiloint2double((int)a.y, (int)a.x);
+        const double c0 = __hiloint2double((int)a.w, (int)a.z);
+        uint32_t dev[kNP];
+#pragma unroll
+        for (int k = 0; k < kNP; k++) dev[k] = gen.dev(k, p, c, b.w);
+        if (b.z == 0) {
+            // chain step: the only input is the previous step's output
+#pragma unroll
+            for (int k = 0; k < kNP; k++) {
+                const double cut = one_if((pdev[k] ^ dev[k]) & 1u);
+                const double same = __dadd_rn(1.0, -cut);
+                const double t = __fma_rn(c0, cut, prev[k]);
+                const double f = __fma_rn(same, -kBig, oth[k]);
+                const double s = dmax(t, f);
+                oth[k] = __fma_rn(cut, prev[k], __dmul_rn(same, oth[k]));
+                prev[k] = __dadd_rn(s, cost);
+                pdev[k] = dev[k];
+            }
+        } else {
+            double r[kNP];
+            if (b.x == kFromPrev) {
+#pragma unroll
+                for (int k = 0; k < kNP; k++) r[k] = __fma_rn(c0, one_if((pdev[k] ^ dev[k]) & 1u), prev[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < kNP; k++)
+                    r[k] = cut_add_m2(__longlong_as_double((long long)lds64(lane + b.x + k * 256)), dev[k], c0);
+            }
+            const uint32_t nx = b.z & 0xFFFFu;
+#pragma unroll 1
+            for (uint32_t q = 0; q < nx; q++) {   // further inputs (uniform trip count)
+                const uint4 e = lds128(x);
+                x += sizeof(ExtraRec);
+                const double ce = __hiloint2double((int)e.y, (int)e.x);
+#pragma unroll
+                for (int k = 0; k < kNP; k++)
+                    r[k] = dmax(r[k], cut_add_m2(__longlong_as_double((long long)lds64(lane + e.z + k * 256)), dev[k], ce));
+            }
+#pragma unroll
+            for (int k = 0; k < kNP; k++) {
+                const bool same = ((pdev[k] ^ dev[k]) & 1u) == 0;
+                const double s = clear_tag(dmax(r[k], same ? prev[k] : oth[k]));
+                oth[k] = same ? oth[k] : prev[k];
+                prev[k] = __dadd_rn(s, cost);
+                pdev[k] = dev[k];
+            }
+        }
+        if (b.y != kNoStore) {
+#pragma unroll
+            for (int k = 0; k < kNP; k++)
+                sts64(lane + b.y + k * 256, (uint64_t)__double_as_longlong(with_tag(prev[k], dev[k] & 1u)));
+        }
+        if (MEM && fwd) {
+            const uint64_t m = mem[p];
+#pragma unroll
+            for (int k = 0; k < kNP; k++) mu[k].add(dev[k] & 1u, m);
+        }
+    };
+    const uint32_t G = K8 / 8;
+    for (uint32_t g = 0; g < G; g++) {           // forward, π order
+        gen.refresh(g);
+#pragma unroll 1
+        for (uint32_t h = 0; h < 2; h++) {
+            gen.sub(h);
+            const uint32_t rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
+#pragma unroll
+            for (uint32_t cc = 0; cc < 4; cc++) step(rec + cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, true);
+        }
+    }
+    for (uint32_t g = G; g-- > 0;) {             // backward, reverse π order
+        gen.refresh(g);
+#pragma unroll 1
+        for (uint32_t h = 2; h-- > 0;) {
+            gen.sub(h);
+            const uint32_t rec = ops + (2 * K8 - 1 - g * 8 - h * 4) * (uint32_t)sizeof(OpRec);
+#pragma unroll
+            for (int cc = 3; cc >= 0; cc--)
+                step(rec - (uint32_t)cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, false);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kNP; k++) {
+        mk[k] = (uint64_t)__double2ull_rz(dmax(prev[k], oth[k]));
+        if (MEM && mu[k].over(cap)) mk[k] = kInfeasible;
+    }
+}
+
+template <int M, bool MEM, bool F64, class Gen>
+__device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
+                                            const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
+                                            uint32_t K8, uint64_t cap) {
+    if constexpr (M == 2 && F64) schedule_m2_f64<MEM>(gen, mk, ops, xr, mem, lane, K8, cap);
+    else schedule_gen<M, MEM, F64>(gen, mk, ops, xr, mem, lane, free_off, K8, cap);
 }
 
 __device__ __forceinline__ bool lex_less(uint64_t m1, uint64_t i1, uint64_t m2, uint64_t i2) {
