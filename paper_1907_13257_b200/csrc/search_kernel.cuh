@@ -448,14 +448,17 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[kNP], uint
     }
 }
 
-// ------------------------------------------ M = 2, tagged-f64 specialisation
+// ------------------------------------------------ tagged-f64 specialisation
 // State per placement: prev = finish time of the previous step as an exact
-// integer double (UNTAGGED), pdev = its device, oth = free time of the other
-// device (untagged).  Slot values stay tagged (t + d·ulp(t)) for the
-// non-chain reads; the tag is set only when a value is stored.  With
-// cut = [dev ≠ pdev] ∈ {0.0, 1.0} and same = 1 − cut, a chain step is
-//   s = max(prev + cut·c0, oth − same·2^50)      (free[dev] = prev if same, oth if cut)
-//   oth' = cut·prev + same·oth,  prev' = s + cost,  pdev' = dev
+// integer double (UNTAGGED), pdev = its device, and the other devices' free
+// times: M = 2 — `oth` in a register; M ≥ 3 — free[d] in the warp's shared
+// region, where free[pdev] may be stale (≤ prev) because the live value is
+// prev.  Slot values stay tagged (t + d·ulp(t)) for the non-chain reads; the
+// tag is set only when a value is stored.  With cut = [dev ≠ pdev] ∈ {0.0,
+// 1.0} and same = 1 − cut, a chain step is
+//   s = max(prev + cut·c0, free[dev] − same·2^50)   (free[dev] = prev if same)
+//   prev' = s + cost, pdev' = dev, and the old prev becomes free[pdev]:
+//   M = 2: oth' = cut·prev + same·oth;  M ≥ 3: free[pdev] ← prev (always)
 // — every operation exact on integers < 2^49; only the max needs a select.
 __device__ __forceinline__ double one_if(uint32_t x) {   // x ∈ {0,1} → 0.0 / 1.0
     return __hiloint2double((int)(x * 0x3FF00000u), 0);
@@ -467,26 +470,40 @@ __device__ __forceinline__ double with_tag(double v, uint32_t dev) {
 __device__ __forceinline__ double clear_tag(double v) {
     return __hiloint2double(__double2hiint(v), __double2loint(v) & ~7);
 }
-// v + [tag(v) ≠ dev]·c for a tagged slot value (M = 2: tags compare on bit 0)
-__device__ __forceinline__ double cut_add_m2(double v, uint32_t dev, double c) {
-    return __fma_rn(c, one_if(((uint32_t)__double2loint(v) ^ dev) & 1u), v);
+__device__ __forceinline__ double ldd(uint32_t a) { return __longlong_as_double((long long)lds64(a)); }
+__device__ __forceinline__ void std_(uint32_t a, double v) { sts64(a, (uint64_t)__double_as_longlong(v)); }
+
+template <int M>
+__device__ __forceinline__ uint32_t cut_bit(uint32_t a, uint32_t b) {   // 1 iff devices differ
+    return (M == 2) ? ((a ^ b) & 1u) : (uint32_t)(((a ^ b) & 7u) != 0);
+}
+// v + [tag(v) ≠ dev]·c for a tagged slot value
+template <int M>
+__device__ __forceinline__ double cut_add_f64(double v, uint32_t dev, double c) {
+    return __fma_rn(c, one_if(cut_bit<M>((uint32_t)__double2loint(v), dev)), v);
 }
 
-template <bool MEM, class Gen>
-__device__ __forceinline__ void schedule_m2_f64(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
-                                                const uint64_t *__restrict__ mem, uint32_t lane, uint32_t K8,
-                                                uint64_t cap) {
+template <int M, bool MEM, class Gen>
+__device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
+                                             const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
+                                             uint32_t K8, uint64_t cap) {
     constexpr double kBig = 1125899906842624.0;   // 2^50
+    constexpr bool SM = M > 2;                    // free[] in shared memory
     double prev[kNP], oth[kNP];
     uint32_t pdev[kNP];
-    MemUse<2> mu[kNP];
+    MemUse<M> mu[kNP];
 #pragma unroll
     for (int k = 0; k < kNP; k++) {
         prev[k] = 0.0;
         oth[k] = 0.0;
         pdev[k] = 0;
         if (MEM) mu[k].init();
+        if (SM) {
+#pragma unroll
+            for (int d = 0; d < M; d++) std_(lane + free_off + d * kSlotStride + k * 256, 0.0);
+        }
     }
+    auto fslot = [&](int k, uint32_t d) { return lane + free_off + d * kSlotStride + k * 256; };
     uint32_t x = xr;
 
     auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
@@ -501,12 +518,17 @@ __device__ __forceinline__ void schedule_m2_f64(Gen &gen, uint64_t (&mk)[kNP], u
             // chain step: the only input is the previous step's output
 #pragma unroll
             for (int k = 0; k < kNP; k++) {
-                const double cut = one_if((pdev[k] ^ dev[k]) & 1u);
+                const double cut = one_if(cut_bit<M>(pdev[k], dev[k]));
                 const double same = __dadd_rn(1.0, -cut);
                 const double t = __fma_rn(c0, cut, prev[k]);
-                const double f = __fma_rn(same, -kBig, oth[k]);
-                const double s = dmax(t, f);
-                oth[k] = __fma_rn(cut, prev[k], __dmul_rn(same, oth[k]));
+                double s;
+                if (SM) {
+                    s = dmax(t, __fma_rn(same, -kBig, ldd(fslot(k, dev[k]))));
+                    std_(fslot(k, pdev[k]), prev[k]);
+                } else {
+                    s = dmax(t, __fma_rn(same, -kBig, oth[k]));
+                    oth[k] = __fma_rn(cut, prev[k], __dmul_rn(same, oth[k]));
+                }
                 prev[k] = __dadd_rn(s, cost);
                 pdev[k] = dev[k];
             }
@@ -514,11 +536,10 @@ __device__ __forceinline__ void schedule_m2_f64(Gen &gen, uint64_t (&mk)[kNP], u
             double r[kNP];
             if (b.x == kFromPrev) {
 #pragma unroll
-                for (int k = 0; k < kNP; k++) r[k] = __fma_rn(c0, one_if((pdev[k] ^ dev[k]) & 1u), prev[k]);
+                for (int k = 0; k < kNP; k++) r[k] = __fma_rn(c0, one_if(cut_bit<M>(pdev[k], dev[k])), prev[k]);
             } else {
 #pragma unroll
-                for (int k = 0; k < kNP; k++)
-                    r[k] = cut_add_m2(__longlong_as_double((long long)lds64(lane + b.x + k * 256)), dev[k], c0);
+                for (int k = 0; k < kNP; k++) r[k] = cut_add_f64<M>(ldd(lane + b.x + k * 256), dev[k], c0);
             }
             const uint32_t nx = b.z & 0xFFFFu;
 #pragma unroll 1
@@ -527,27 +548,31 @@ __device__ __forceinline__ void schedule_m2_f64(Gen &gen, uint64_t (&mk)[kNP], u
                 x += sizeof(ExtraRec);
                 const double ce = __hiloint2double((int)e.y, (int)e.x);
 #pragma unroll
-                for (int k = 0; k < kNP; k++)
-                    r[k] = dmax(r[k], cut_add_m2(__longlong_as_double((long long)lds64(lane + e.z + k * 256)), dev[k], ce));
+                for (int k = 0; k < kNP; k++) r[k] = dmax(r[k], cut_add_f64<M>(ldd(lane + e.z + k * 256), dev[k], ce));
             }
 #pragma unroll
             for (int k = 0; k < kNP; k++) {
-                const bool same = ((pdev[k] ^ dev[k]) & 1u) == 0;
-                const double s = clear_tag(dmax(r[k], same ? prev[k] : oth[k]));
-                oth[k] = same ? oth[k] : prev[k];
-                prev[k] = __dadd_rn(s, cost);
+                const bool same = cut_bit<M>(pdev[k], dev[k]) == 0;
+                double f;
+                if (SM) {
+                    f = same ? prev[k] : ldd(fslot(k, dev[k]));
+                    std_(fslot(k, pdev[k]), prev[k]);
+                } else {
+                    f = same ? prev[k] : oth[k];
+                    oth[k] = same ? oth[k] : prev[k];
+                }
+                prev[k] = __dadd_rn(clear_tag(dmax(r[k], f)), cost);
                 pdev[k] = dev[k];
             }
         }
         if (b.y != kNoStore) {
 #pragma unroll
-            for (int k = 0; k < kNP; k++)
-                sts64(lane + b.y + k * 256, (uint64_t)__double_as_longlong(with_tag(prev[k], dev[k] & 1u)));
+            for (int k = 0; k < kNP; k++) std_(lane + b.y + k * 256, with_tag(prev[k], Dev<M>::canon(dev[k])));
         }
         if (MEM && fwd) {
             const uint64_t m = mem[p];
 #pragma unroll
-            for (int k = 0; k < kNP; k++) mu[k].add(dev[k] & 1u, m);
+            for (int k = 0; k < kNP; k++) mu[k].add(Dev<M>::canon(dev[k]), m);
         }
     };
     const uint32_t G = K8 / 8;
@@ -574,7 +599,14 @@ __device__ __forceinline__ void schedule_m2_f64(Gen &gen, uint64_t (&mk)[kNP], u
     }
 #pragma unroll
     for (int k = 0; k < kNP; k++) {
-        mk[k] = (uint64_t)__double2ull_rz(dmax(prev[k], oth[k]));
+        double v = prev[k];
+        if (SM) {
+#pragma unroll
+            for (int d = 0; d < M; d++) v = dmax(v, ldd(fslot(k, d)));   // stale free[pdev] ≤ prev
+        } else {
+            v = dmax(v, oth[k]);
+        }
+        mk[k] = (uint64_t)__double2ull_rz(v);
         if (MEM && mu[k].over(cap)) mk[k] = kInfeasible;
     }
 }
@@ -583,7 +615,7 @@ template <int M, bool MEM, bool F64, class Gen>
 __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
                                             const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
                                             uint32_t K8, uint64_t cap) {
-    if constexpr (M == 2 && F64) schedule_m2_f64<MEM>(gen, mk, ops, xr, mem, lane, K8, cap);
+    if constexpr (F64 && M >= 2) schedule_f64<M, MEM>(gen, mk, ops, xr, mem, lane, free_off, K8, cap);
     else schedule_gen<M, MEM, F64>(gen, mk, ops, xr, mem, lane, free_off, K8, cap);
 }
 
