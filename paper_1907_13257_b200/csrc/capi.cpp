@@ -143,6 +143,7 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
     p.region_bytes = region;
     p.free_off = nslot * kSlotStride;
     p.zero_off = (uint32_t)g->W * kSlotStride;
+    p.one_hi = 0x3FF00000u;
     p.g_partials = g->d_partials;
     p.g_ticket = g->d_ticket;
     p.g_out = g->d_scalars + SC_LOCAL_MK;

@@ -94,6 +94,7 @@ struct KParams {
     uint32_t region_bytes;       // bytes per warp region
     uint32_t free_off;           // region offset of free[M] (M ≥ 3)
     uint32_t zero_off;           // region offset of the always-zero slot
+    uint32_t one_hi;             // 0x3FF00000, the high word of 1.0 (opaque to ptxas)
 };
 
 // Device scalar slots of pp_dfg::d_scalars (u64).

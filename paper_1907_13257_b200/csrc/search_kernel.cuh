@@ -460,8 +460,13 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[kNP], uint
 //   prev' = s + cost, pdev' = dev, and the old prev becomes free[pdev]:
 //   M = 2: oth' = cut·prev + same·oth;  M ≥ 3: free[pdev] ← prev (always)
 // — every operation exact on integers < 2^49; only the max needs a select.
-__device__ __forceinline__ double one_if(uint32_t x) {   // x ∈ {0,1} → 0.0 / 1.0
-    return __hiloint2double((int)(x * 0x3FF00000u), 0);
+// x ∈ {0,1} → 0.0 / 1.0 as one IMAD on the FMA pipe: khi = 0x3FF00000 (the
+// high word of 1.0) is a kernel parameter, so ptxas cannot turn the multiply
+// into an ISETP + SEL pair on the ALU pipe.
+__device__ __forceinline__ double one_if(uint32_t x, uint32_t khi) {
+    uint32_t hi;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(hi) : "r"(x), "r"(khi));
+    return __hiloint2double((int)hi, 0);
 }
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 __device__ __forceinline__ double with_tag(double v, uint32_t dev) {
@@ -479,14 +484,14 @@ __device__ __forceinline__ uint32_t cut_bit(uint32_t a, uint32_t b) {   // 1 iff
 }
 // v + [tag(v) ≠ dev]·c for a tagged slot value
 template <int M>
-__device__ __forceinline__ double cut_add_f64(double v, uint32_t dev, double c) {
-    return __fma_rn(c, one_if(cut_bit<M>((uint32_t)__double2loint(v), dev)), v);
+__device__ __forceinline__ double cut_add_f64(double v, uint32_t dev, double c, uint32_t khi) {
+    return __fma_rn(c, one_if(cut_bit<M>((uint32_t)__double2loint(v), dev), khi), v);
 }
 
 template <int M, bool MEM, class Gen>
 __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
                                              const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
-                                             uint32_t K8, uint64_t cap) {
+                                             uint32_t K8, uint64_t cap, uint32_t khi) {
     constexpr double kBig = 1125899906842624.0;   // 2^50
     constexpr bool SM = M > 2;                    // free[] in shared memory
     double prev[kNP], oth[kNP];
@@ -518,7 +523,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint
             // chain step: the only input is the previous step's output
 #pragma unroll
             for (int k = 0; k < kNP; k++) {
-                const double cut = one_if(cut_bit<M>(pdev[k], dev[k]));
+                const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
                 const double same = __dadd_rn(1.0, -cut);
                 const double t = __fma_rn(c0, cut, prev[k]);
                 double s;
@@ -536,10 +541,10 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint
             double r[kNP];
             if (b.x == kFromPrev) {
 #pragma unroll
-                for (int k = 0; k < kNP; k++) r[k] = __fma_rn(c0, one_if(cut_bit<M>(pdev[k], dev[k])), prev[k]);
+                for (int k = 0; k < kNP; k++) r[k] = __fma_rn(c0, one_if(cut_bit<M>(pdev[k], dev[k]), khi), prev[k]);
             } else {
 #pragma unroll
-                for (int k = 0; k < kNP; k++) r[k] = cut_add_f64<M>(ldd(lane + b.x + k * 256), dev[k], c0);
+                for (int k = 0; k < kNP; k++) r[k] = cut_add_f64<M>(ldd(lane + b.x + k * 256), dev[k], c0, khi);
             }
             const uint32_t nx = b.z & 0xFFFFu;
 #pragma unroll 1
@@ -548,18 +553,20 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint
                 x += sizeof(ExtraRec);
                 const double ce = __hiloint2double((int)e.y, (int)e.x);
 #pragma unroll
-                for (int k = 0; k < kNP; k++) r[k] = dmax(r[k], cut_add_f64<M>(ldd(lane + e.z + k * 256), dev[k], ce));
+                for (int k = 0; k < kNP; k++) r[k] = dmax(r[k], cut_add_f64<M>(ldd(lane + e.z + k * 256), dev[k], ce, khi));
             }
 #pragma unroll
             for (int k = 0; k < kNP; k++) {
-                const bool same = cut_bit<M>(pdev[k], dev[k]) == 0;
+                // free[dev] = same ? prev : other, as exact products (FP64 pipe)
+                const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
+                const double same = __dadd_rn(1.0, -cut);
                 double f;
                 if (SM) {
-                    f = same ? prev[k] : ldd(fslot(k, dev[k]));
+                    f = __fma_rn(same, prev[k], __dmul_rn(cut, ldd(fslot(k, dev[k]))));
                     std_(fslot(k, pdev[k]), prev[k]);
                 } else {
-                    f = same ? prev[k] : oth[k];
-                    oth[k] = same ? oth[k] : prev[k];
+                    f = __fma_rn(same, prev[k], __dmul_rn(cut, oth[k]));
+                    oth[k] = __fma_rn(cut, prev[k], __dmul_rn(same, oth[k]));
                 }
                 prev[k] = __dadd_rn(clear_tag(dmax(r[k], f)), cost);
                 pdev[k] = dev[k];
@@ -614,8 +621,8 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint
 template <int M, bool MEM, bool F64, class Gen>
 __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
                                             const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
-                                            uint32_t K8, uint64_t cap) {
-    if constexpr (F64 && M >= 2) schedule_f64<M, MEM>(gen, mk, ops, xr, mem, lane, free_off, K8, cap);
+                                            uint32_t K8, uint64_t cap, uint32_t khi) {
+    if constexpr (F64 && M >= 2) schedule_f64<M, MEM>(gen, mk, ops, xr, mem, lane, free_off, K8, cap, khi);
     else schedule_gen<M, MEM, F64>(gen, mk, ops, xr, mem, lane, free_off, K8, cap);
 }
 
@@ -695,21 +702,21 @@ __global__ void __launch_bounds__(256, PP_MIN_CTAS) search_kernel(const KParams 
         if (GEN == GEN_GRAY) {
             GrayGen<M> g;
             g.init(idx, P.K);
-            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap);
+            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
         } else if (GEN == GEN_RANDOM) {
             RandomGen<M> g;
             g.init(idx, P.seed, P.K);
-            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap);
+            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
         } else if (GEN == GEN_PERTURB) {
             PerturbGen<M> g;
             g.init(idx, P.seed, P.K, P.tau);
-            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap);
+            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
         } else {
             ExplicitGen g;
 #pragma unroll
             for (int k = 0; k < kNP; k++) g.row[k] = P.g_place + (idx[k] - P.begin) * (uint64_t)P.K;
             g.orig = orig;
-            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap);
+            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
         }
 #pragma unroll
         for (int k = 0; k < kNP; k++) {

@@ -73,6 +73,25 @@ __global__ void k_u64max_fsel(uint64_t *out, uint64_t a) {
   uint64_t s = 0; for (int j = 0; j < 8; j++) s += x[j];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
+__global__ void k_i2f64(double *out, uint32_t a) {   // I2F.F64.U32
+  double x[8];
+  uint32_t u[8];
+  for (int j = 0; j < 8; j++) { x[j] = 0; u[j] = threadIdx.x + j; }
+  for (int i = 0; i < N_ITER; i++)
+#pragma unroll
+    for (int j = 0; j < 8; j++) { x[j] += (double)(u[j] & 1u); u[j] += a; }
+  double s = 0; for (int j = 0; j < 8; j++) s += x[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_dfma(double *out, double a) {
+  double x[8];
+  for (int j = 0; j < 8; j++) x[j] = threadIdx.x + j;
+  for (int i = 0; i < N_ITER; i++)
+#pragma unroll
+    for (int j = 0; j < 8; j++) x[j] = __fma_rn(x[j], a, 1.0);
+  double s = 0; for (int j = 0; j < 8; j++) s += x[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
 __global__ void k_alu(uint32_t *out, uint32_t a) {   // LOP3/IADD3 only
   uint32_t x[8];
   for (int j = 0; j < 8; j++) x[j] = threadIdx.x + j;
@@ -114,6 +133,8 @@ int main() {
   run("u64 max (ISETP+SEL)", [&] { k_u64max_sel<<<blocks, thr>>>((uint64_t *)d, 1); }, n, blocks, thr);
   run("u64 max (ISETP+@P MOV)", [&] { k_u64max_pred<<<blocks, thr>>>((uint64_t *)d, 1); }, n, blocks, thr);
   run("u64 max (ISETP+FSEL)", [&] { k_u64max_fsel<<<blocks, thr>>>((uint64_t *)d, 1); }, n, blocks, thr);
+  run("I2F.F64.U32 + DADD + IADD", [&] { k_i2f64<<<blocks, thr>>>((double *)d, 3); }, n, blocks, thr);
+  run("DFMA", [&] { k_dfma<<<blocks, thr>>>((double *)d, 0.5); }, n, blocks, thr);
   run("int32 xor+shift+add (ALU)", [&] { k_alu<<<blocks, thr>>>((uint32_t *)d, 7); }, n, blocks, thr);
   run("int32 IMAD (FMA pipe)", [&] { k_imad<<<blocks, thr>>>((uint32_t *)d, 7); }, n, blocks, thr);
   return 0;
