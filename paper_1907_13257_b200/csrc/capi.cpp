@@ -26,21 +26,21 @@ void note_launch() { g_launches++; }
 
 int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp_dfg **out);
 
-#define PP_DECL_M(m)                                                  \
-    KernelInfo kernel_for_m##m(int gen, bool mem, bool wa, bool f64); \
+#define PP_DECL_M(m)                                                          \
+    KernelInfo kernel_for_m##m(int gen, bool mem, bool wa, bool f64, int np); \
     UpdateFn update_for_m##m(int gen);
 PP_DECL_M(1) PP_DECL_M(2) PP_DECL_M(3) PP_DECL_M(4) PP_DECL_M(5) PP_DECL_M(6) PP_DECL_M(7) PP_DECL_M(8)
 
-KernelInfo kernel_for(int M, int gen, bool mem, bool wa, bool f64) {
+KernelInfo kernel_for(int M, int gen, bool mem, bool wa, bool f64, int np) {
     switch (M) {
-        case 1: return kernel_for_m1(gen, mem, wa, f64);
-        case 2: return kernel_for_m2(gen, mem, wa, f64);
-        case 3: return kernel_for_m3(gen, mem, wa, f64);
-        case 4: return kernel_for_m4(gen, mem, wa, f64);
-        case 5: return kernel_for_m5(gen, mem, wa, f64);
-        case 6: return kernel_for_m6(gen, mem, wa, f64);
-        case 7: return kernel_for_m7(gen, mem, wa, f64);
-        default: return kernel_for_m8(gen, mem, wa, f64);
+        case 1: return kernel_for_m1(gen, mem, wa, f64, np);
+        case 2: return kernel_for_m2(gen, mem, wa, f64, np);
+        case 3: return kernel_for_m3(gen, mem, wa, f64, np);
+        case 4: return kernel_for_m4(gen, mem, wa, f64, np);
+        case 5: return kernel_for_m5(gen, mem, wa, f64, np);
+        case 6: return kernel_for_m6(gen, mem, wa, f64, np);
+        case 7: return kernel_for_m7(gen, mem, wa, f64, np);
+        default: return kernel_for_m8(gen, mem, wa, f64, np);
     }
 }
 UpdateFn update_for(int M, int gen) {
@@ -85,49 +85,81 @@ struct DeviceGuard {
 // ------------------------------------------------------------ launch setup
 struct Launch {
     KernelInfo k;
-    int threads = 0, grid = 0, smem = 0;
+    int threads = 0, grid = 0, smem = 0, np = 0;
     KParams p{};
 };
 
-// Chooses the CTA size (largest of 256/128/64/32 whose per-warp state fits),
-// the dynamic shared memory layout and a grid of (resident CTAs per SM) × SMs.
-static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin, uint64_t end, Launch &L) {
+// Chooses NP (placements per lane), the CTA size and the dynamic shared
+// memory layout, and a grid of (resident CTAs per SM) × SMs.  The per-warp
+// state grows with W·NP, so for DFGs with many live values a smaller NP keeps
+// more warps resident: take the largest NP that keeps ≥ 12 warps per SM (3
+// per scheduler), else the NP with the most resident placements.
+struct Choice {
+    KernelInfo k;
+    int np = 0, threads = 0, smem = 0, ctas = 0;
+    uint32_t region = 0, slots_off = 0;
+};
+
+static int choose(const pp_dfg *g, int M, int gen, bool write_all, int np, Choice &c) {
     const bool mem = g->cap > 0;
-    L.k = kernel_for(M, gen, mem, write_all, g->f64);
+    c.k = kernel_for(M, gen, mem, write_all, g->f64, np);
+    c.np = write_all ? 2 : np;
     const uint32_t nslot = (uint32_t)g->W + 1;                  // live + zero
-    const uint32_t region = (nslot + (M > 2 ? (uint32_t)M : 0u)) * kSlotStride;
-    const uint32_t slots_off = (g->image_bytes + 127) & ~127u;
+    c.region = (nslot + (M > 2 ? (uint32_t)M : 0u)) * kSlotUnit * c.np;
+    c.slots_off = (g->image_bytes + 127) & ~127u;
     cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, L.k.func);
+    cudaError_t e = cudaFuncGetAttributes(&fa, c.k.func);
     if (e != cudaSuccess) return cuda_err(e, "cudaFuncGetAttributes");
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device);
     const size_t max_dyn = (size_t)std::min<int>(optin, kMaxSmemBytes) - fa.sharedSizeBytes - 1024;
-    int threads = 256;
-    size_t smem = 0;
-    for (; threads >= 32; threads >>= 1) {
-        smem = slots_off + (size_t)(threads / 32) * region;
-        if (smem <= max_dyn) break;
+    c.threads = 0;
+    for (int threads = 256; threads >= 32; threads >>= 1) {
+        size_t smem = c.slots_off + (size_t)(threads / 32) * c.region;
+        if (smem <= max_dyn) { c.threads = threads; c.smem = (int)smem; break; }
     }
-    if (threads < 32) {
+    if (!c.threads) return PP_E_TOO_LARGE;
+    e = cudaFuncSetAttribute(c.k.func, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem);
+    if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.ctas, c.k.func, c.threads, c.smem);
+    if (e != cudaSuccess) return cuda_err(e, "occupancy");
+    if (c.ctas < 1) c.ctas = 1;
+    return PP_OK;
+}
+
+static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin, uint64_t end, Launch &L) {
+    Choice best;
+    int best_warps = -1;
+    for (int np : {4, 2, 1}) {
+        Choice c;
+        int rc = choose(g, M, gen, write_all, np, c);
+        if (rc == PP_E_TOO_LARGE) continue;
+        if (rc) return rc;
+        const int warps = c.ctas * c.threads / 32;
+        if (warps >= 12 || write_all) { best = c; best_warps = warps; break; }
+        // otherwise keep the most placements in flight, ties to more warps
+        if (best_warps < 0 || warps * c.np > best_warps * best.np ||
+            (warps * c.np == best_warps * best.np && warps > best_warps)) {
+            best = c;
+            best_warps = warps;
+        }
+    }
+    if (best_warps < 0) {
         set_error("per-lane schedule state does not fit in shared memory");
         return PP_E_TOO_LARGE;
     }
-    e = cudaFuncSetAttribute(L.k.func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.k.func, threads, smem);
-    if (e != cudaSuccess) return cuda_err(e, "occupancy");
-    if (occ < 1) occ = 1;
+    L.k = best.k;
     const uint64_t n = end - begin;
-    const uint64_t tiles = (n + 32 * kNP - 1) / (32 * kNP);
-    const uint64_t wpb = threads / 32;
+    const uint64_t per_warp = 32ull * best.np;
+    const uint64_t tiles = (n + per_warp - 1) / per_warp;
+    const uint64_t wpb = best.threads / 32;
     uint64_t want = (tiles + wpb - 1) / wpb;
-    uint64_t grid = std::min<uint64_t>((uint64_t)occ * g->sm_count, want);
+    uint64_t grid = std::min<uint64_t>((uint64_t)best.ctas * g->sm_count, want);
     grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, kMaxGrid));
-    L.threads = threads;
+    L.threads = best.threads;
     L.grid = (int)grid;
-    L.smem = (int)smem;
+    L.smem = best.smem;
+    L.np = best.np;
     KParams &p = L.p;
     p.g_image = g->d_image;
     p.begin = begin;
@@ -139,10 +171,10 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
     p.off_extra = g->off_extra;
     p.off_mem = g->off_mem;
     p.off_orig = g->off_orig;
-    p.smem_slots_off = slots_off;
-    p.region_bytes = region;
-    p.free_off = nslot * kSlotStride;
-    p.zero_off = (uint32_t)g->W * kSlotStride;
+    p.smem_slots_off = best.slots_off;
+    p.region_bytes = best.region;
+    p.free_off = ((uint32_t)g->W + 1) * kSlotUnit;
+    p.zero_off = (uint32_t)g->W * kSlotUnit;
     p.one_hi = 0x3FF00000u;
     p.g_partials = g->d_partials;
     p.g_ticket = g->d_ticket;

@@ -18,9 +18,9 @@
 //   [u32   × K8 ]    descriptor index of π position p (explicit placements)
 //
 // Per-lane schedule state lives in a per-warp region of shared memory laid out
-// [slot][placement k < kNP][lane] × u64, so a slot's byte offset inside the
-// region is slot·kSlotStride (pre-multiplied in the records) and every access
-// of a warp touches 32 consecutive u64 (conflict-free).  Slots 0..W−1 hold
+// [slot][placement k < NP][lane] × u64, so a slot's byte offset inside the
+// region is slot·256·NP (the records hold slot·256) and every access of a
+// warp touches 32 consecutive u64 (conflict-free).  Slots 0..W−1 hold
 // live finish times (liveness-allocated), slot W is always zero.  An input
 // produced by the immediately preceding step is forwarded in a register
 // (kFromPrev) and a value that no later step reads from a slot is not stored.
@@ -43,8 +43,10 @@
 
 namespace pp {
 
-constexpr int kNP = 4;                          // placements per lane
-constexpr uint32_t kSlotStride = 256u * kNP;    // bytes between consecutive slots
+// Slot offsets in the image are in units of kSlotUnit = 256 bytes (one u64
+// per lane of a warp); a kernel evaluating NP placements per lane (NP ∈ {1,
+// 2, 4}, chosen per launch from W and shared memory) scales them by NP.
+constexpr uint32_t kSlotUnit = 256u;
 
 constexpr uint32_t kFromPrev = 0xFFFFFFFFu;     // OpRec.src_off: previous step's output (register)
 constexpr uint32_t kNoStore = 0xFFFFFFFFu;      // OpRec.out_off: output never read from a slot
@@ -92,8 +94,8 @@ struct KParams {
     uint32_t tau;
     uint32_t smem_slots_off;     // byte offset of the first warp region in smem
     uint32_t region_bytes;       // bytes per warp region
-    uint32_t free_off;           // region offset of free[M] (M ≥ 3)
-    uint32_t zero_off;           // region offset of the always-zero slot
+    uint32_t free_off;           // region offset of free[M] (M ≥ 3), in slot units ×256
+    uint32_t zero_off;           // region offset of the always-zero slot, in slot units ×256
     uint32_t one_hi;             // 0x3FF00000, the high word of 1.0 (opaque to ptxas)
 };
 
@@ -128,7 +130,7 @@ struct KernelInfo {
 };
 
 // search_inst.cu (compiled once per M with -DPP_M): kernel_for_m<M>(...)
-KernelInfo kernel_for(int M, int gen, bool mem, bool write_all, bool f64);
+KernelInfo kernel_for(int M, int gen, bool mem, bool write_all, bool f64, int np);
 UpdateFn update_for(int M, int gen);
 
 }  // namespace pp

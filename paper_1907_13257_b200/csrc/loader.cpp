@@ -188,7 +188,7 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
         expire[last[s]].push_back(sl);
     }
     const int W = nslots;
-    const uint32_t zero_off = (uint32_t)W * kSlotStride;   // slot W always holds 0
+    const uint32_t zero_off = (uint32_t)W * kSlotUnit;   // slot W always holds 0
     if (W + 1 > 4096) return fail(PP_E_TOO_LARGE, "too many live slots");
 
     // ---- arithmetic: exact integer ps in doubles when every time is < 2^49
@@ -208,7 +208,7 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
     // ---- records: first input inlined in the op record, the rest as extras
     std::vector<OpRec> ops(S);
     std::vector<ExtraRec> xr;
-    auto src_off = [&](int v) -> uint32_t { return v < 0 ? zero_off : (uint32_t)slot[v] * kSlotStride; };
+    auto src_off = [&](int v) -> uint32_t { return v < 0 ? zero_off : (uint32_t)slot[v] * kSlotUnit; };
     for (int s = 0; s < S; s++) {
         const bool fwd = s < K8;
         const int p = fwd ? s : S - 1 - s;
@@ -217,7 +217,7 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
         o.cost8 = p < K ? enc(fwd ? d->fwd_ps[pi[p]] : d->bwd_ps[pi[p]]) : enc(0);
         o.c8 = enc(in[0].second);
         o.src_off = fwd_first[s] ? kFromPrev : src_off(in[0].first);
-        o.out_off = slot[s] < 0 ? kNoStore : (uint32_t)slot[s] * kSlotStride;
+        o.out_off = slot[s] < 0 ? kNoStore : (uint32_t)slot[s] * kSlotUnit;
         const uint32_t n_extra = (uint32_t)in.size() - 1;
         if (n_extra > 0xFFFF) return fail(PP_E_TOO_LARGE, "op with more than 65536 inputs");
         o.ctrl = (fwd_first[s] && n_extra == 0) ? 0u : (0x10000u | n_extra);

@@ -2,10 +2,10 @@
 // forward+backward in-order list schedule of each candidate placement, and
 // the (makespan, index) argmin, for sm_100a.
 //
-// Kernel shape (DESIGN.md Â§Kernels): LANE PER PLACEMENT, kNP placements per
-// lane.  A warp evaluates 32Â·kNP candidate placements in lockstep over the
+// Kernel shape (DESIGN.md Â§Kernels): LANE PER PLACEMENT, NP placements per
+// lane.  A warp evaluates 32Â·NP candidate placements in lockstep over the
 // same DFG records, so every record read is a warp-uniform shared-memory
-// broadcast shared by 32Â·kNP placements.  The recurrence (PAPER.md:443â€“453
+// broadcast shared by 32Â·NP placements.  The recurrence (PAPER.md:443â€“453
 // dependency with Î”_e, :465â€“476 one op at a time per device, :497â€“503
 // back-to-back ops + overlapped communication; readings R1, R2):
 //
@@ -62,11 +62,11 @@ struct Bits {
 // yields the device of Ï€ position p = 8g + c for placement k (c is a
 // compile-time constant in the unrolled schedule loop).
 
-template <int M>
+template <int M, int NP>
 struct GrayGen {                           // O5: reflected M-ary Gray code
     static constexpr int b = Bits<M>::b;
     static constexpr int PF = b ? 64 / b : 64;     // fields per register
-    uint64_t lo[kNP], hi[kNP];
+    uint64_t lo[NP], hi[NP];
     __device__ __forceinline__ static void one(uint64_t i, uint32_t K, uint64_t &lo, uint64_t &hi) {
         lo = hi = 0;
         if (M == 1) return;
@@ -109,15 +109,15 @@ struct GrayGen {                           // O5: reflected M-ary Gray code
     }
 };
 
-template <int M>
+template <int M, int NP>
 struct RandomGen {                         // O6 RANDOM: b bits per op, P = 8Â·âŒŠ8/bâŒ‹ ops per word
     static constexpr int b = Bits<M>::b;
     static constexpr int GPW = b ? 8 / b : 8;      // 8-op groups per word
-    uint64_t key[kNP];   // seed + Î³Â·(iÂ·Wd + 1)
-    uint64_t keep[kNP];  // 0 for candidate 0 (all zeros), else ~0
-    uint64_t w[kNP];     // current word
-    uint32_t wg[kNP];    // the current group's 8Â·b bits
-    uint32_t wh[kNP];    // the current half-group's 4Â·b bits
+    uint64_t key[NP];   // seed + Î³Â·(iÂ·Wd + 1)
+    uint64_t keep[NP];  // 0 for candidate 0 (all zeros), else ~0
+    uint64_t w[NP];     // current word
+    uint32_t wg[NP];    // the current group's 8Â·b bits
+    uint32_t wh[NP];    // the current half-group's 4Â·b bits
     uint32_t cur;        // word index held in w (shared by the lane's placements)
     template <int N>
     __device__ __forceinline__ void init(const uint64_t (&i)[N], uint64_t seed, uint32_t K) {
@@ -139,16 +139,16 @@ struct RandomGen {                         // O6 RANDOM: b bits per op, P = 8Â·â
         if (t != cur) {   // warp-uniform
             cur = t;
 #pragma unroll
-            for (int k = 0; k < kNP; k++) w[k] = mix64(key[k] + kGamma * t) & keep[k];
+            for (int k = 0; k < NP; k++) w[k] = mix64(key[k] + kGamma * t) & keep[k];
         }
         const uint32_t sh = 8 * b * (g - t * GPW);
 #pragma unroll
-        for (int k = 0; k < kNP; k++) wg[k] = (uint32_t)(w[k] >> sh);
+        for (int k = 0; k < NP; k++) wg[k] = (uint32_t)(w[k] >> sh);
     }
     // half-group h (ops 8g + 4h .. 8g + 4h + 3)
     __device__ __forceinline__ void sub(uint32_t h) {
 #pragma unroll
-        for (int k = 0; k < kNP; k++) wh[k] = wg[k] >> (4 * b * h);
+        for (int k = 0; k < NP; k++) wh[k] = wg[k] >> (4 * b * h);
     }
     // cc = position within the half-group (compile-time in the schedule loop)
     __device__ __forceinline__ uint32_t dev(int k, uint32_t, uint32_t cc, uint32_t) const {
@@ -158,12 +158,12 @@ struct RandomGen {                         // O6 RANDOM: b bits per op, P = 8Â·â
     }
 };
 
-template <int M>
+template <int M, int NP>
 struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops per word
-    uint64_t key1[kNP], key2[kNP];
-    uint64_t w[kNP], y[kNP];
-    uint32_t uh[kNP], yh[kNP];   // the current half-group's u / y bytes
-    uint32_t tau[kNP];   // 0 for candidate 0 (the base itself)
+    uint64_t key1[NP], key2[NP];
+    uint64_t w[NP], y[NP];
+    uint32_t uh[NP], yh[NP];   // the current half-group's u / y bytes
+    uint32_t tau[NP];   // 0 for candidate 0 (the base itself)
     template <int N>
     __device__ __forceinline__ void init(const uint64_t (&i)[N], uint64_t seed, uint32_t K, uint32_t tau_) {
         const uint64_t Wd = (K + 7) / 8;
@@ -179,14 +179,14 @@ struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops
     __device__ __forceinline__ void refresh(uint32_t g) {
         if (M == 1) return;
 #pragma unroll
-        for (int k = 0; k < kNP; k++) {
+        for (int k = 0; k < NP; k++) {
             w[k] = mix64(key1[k] + kGamma * g);
             if (M > 2) y[k] = mix64(key2[k] + kGamma * g);
         }
     }
     __device__ __forceinline__ void sub(uint32_t h) {
 #pragma unroll
-        for (int k = 0; k < kNP; k++) {
+        for (int k = 0; k < NP; k++) {
             uh[k] = h ? (uint32_t)(w[k] >> 32) : (uint32_t)w[k];
             if (M > 2) yh[k] = h ? (uint32_t)(y[k] >> 32) : (uint32_t)y[k];
         }
@@ -205,8 +205,9 @@ struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops
     }
 };
 
+template <int NP>
 struct ExplicitGen {                       // rows of a [count][K] uint8 array
-    const uint8_t *row[kNP];
+    const uint8_t *row[NP];
     const uint32_t *orig;
     __device__ __forceinline__ void refresh(uint32_t) {}
     __device__ __forceinline__ void sub(uint32_t) {}
@@ -300,25 +301,25 @@ struct MemUse {
     }
 };
 
-// -------------------------------------------------- kNP placements per lane
+// -------------------------------------------------- NP placements per lane
 // lane: shared address of this lane's entry in its warp region (region +
 // 8Â·lane); placement k's copy of a slot is at +kÂ·256.
-template <int M, bool MEM, bool F64, class Gen>
-__device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
+template <int M, int NP, bool MEM, bool F64, class Gen>
+__device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], uint32_t ops, uint32_t xr,
                                             const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
                                             uint32_t K8, uint64_t cap) {
     typedef typename std::conditional<F64, ArithF64, ArithU64>::type A;
     typedef typename A::V V;
-    V prev[kNP], oth[kNP];
-    MemUse<M> mu[kNP];
+    V prev[NP], oth[NP];
+    MemUse<M> mu[NP];
 #pragma unroll
-    for (int k = 0; k < kNP; k++) {
+    for (int k = 0; k < NP; k++) {
         prev[k] = A::from_bits(0);
         oth[k] = A::from_bits(0);
         if (MEM) mu[k].init();
         if (M > 2) {
 #pragma unroll
-            for (int d = 0; d < M; d++) sts64(lane + free_off + d * kSlotStride + k * 256, 0);
+            for (int d = 0; d < M; d++) sts64(lane + free_off * NP + d * NP * 256 + k * 256, 0);
         }
     }
     uint32_t x = xr;
@@ -328,13 +329,13 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[kNP], uint
         const uint4 b = lds128(rec + 16);
         const uint64_t cost = ((uint64_t)a.y << 32) | a.x;
         const uint64_t c0 = ((uint64_t)a.w << 32) | a.z;
-        uint32_t dev[kNP];
+        uint32_t dev[NP];
 #pragma unroll
-        for (int k = 0; k < kNP; k++) dev[k] = gen.dev(k, p, c, b.w);
+        for (int k = 0; k < NP; k++) dev[k] = gen.dev(k, p, c, b.w);
         if (M <= 2 && b.z == 0) {
             // fast path: the only input is the previous step's output (a chain edge)
 #pragma unroll
-            for (int k = 0; k < kNP; k++) {
+            for (int k = 0; k < NP; k++) {
                 V s;
                 if (M == 1) {
                     s = prev[k];
@@ -364,13 +365,13 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[kNP], uint
                 prev[k] = A::finish(s, dev[k], cost);
             }
         } else {
-            V r[kNP];
+            V r[NP];
             if (b.x == kFromPrev) {
 #pragma unroll
-                for (int k = 0; k < kNP; k++) r[k] = cut_add<A, M>(prev[k], dev[k], c0);
+                for (int k = 0; k < NP; k++) r[k] = cut_add<A, M>(prev[k], dev[k], c0);
             } else {
 #pragma unroll
-                for (int k = 0; k < kNP; k++) r[k] = cut_add<A, M>(A::from_bits(lds64(lane + b.x + k * 256)), dev[k], c0);
+                for (int k = 0; k < NP; k++) r[k] = cut_add<A, M>(A::from_bits(lds64(lane + b.x * NP + k * 256)), dev[k], c0);
             }
             const uint32_t nx = b.z & 0xFFFFu;
 #pragma unroll 1
@@ -379,11 +380,11 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[kNP], uint
                 x += sizeof(ExtraRec);
                 const uint64_t ce = ((uint64_t)e.y << 32) | e.x;
 #pragma unroll
-                for (int k = 0; k < kNP; k++)
-                    r[k] = A::vmax(r[k], cut_add<A, M>(A::from_bits(lds64(lane + e.z + k * 256)), dev[k], ce));
+                for (int k = 0; k < NP; k++)
+                    r[k] = A::vmax(r[k], cut_add<A, M>(A::from_bits(lds64(lane + e.z * NP + k * 256)), dev[k], ce));
             }
 #pragma unroll
-            for (int k = 0; k < kNP; k++) {
+            for (int k = 0; k < NP; k++) {
                 V s;
                 if (M == 1) {
                     s = A::vmax(r[k], prev[k]);
@@ -392,7 +393,7 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[kNP], uint
                     s = A::vmax(r[k], same ? prev[k] : oth[k]);
                     oth[k] = same ? oth[k] : prev[k];
                 } else {
-                    const uint32_t fa = lane + free_off + dev[k] * kSlotStride + k * 256;
+                    const uint32_t fa = lane + free_off * NP + dev[k] * NP * 256 + k * 256;
                     s = A::vmax(r[k], A::from_bits(lds64(fa)));
                     prev[k] = A::finish(s, dev[k], cost);
                     sts64(fa, A::to_bits(prev[k]));
@@ -403,12 +404,12 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[kNP], uint
         }
         if (b.y != kNoStore) {
 #pragma unroll
-            for (int k = 0; k < kNP; k++) sts64(lane + b.y + k * 256, A::to_bits(prev[k]));
+            for (int k = 0; k < NP; k++) sts64(lane + b.y * NP + k * 256, A::to_bits(prev[k]));
         }
         if (MEM && fwd) {
             const uint64_t m = mem[p];
 #pragma unroll
-            for (int k = 0; k < kNP; k++) mu[k].add(Dev<M>::canon(dev[k]), m);
+            for (int k = 0; k < NP; k++) mu[k].add(Dev<M>::canon(dev[k]), m);
         }
     };
     const uint32_t G = K8 / 8;
@@ -434,14 +435,14 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[kNP], uint
         }
     }
 #pragma unroll
-    for (int k = 0; k < kNP; k++) {
+    for (int k = 0; k < NP; k++) {
         V v;
         if (M <= 2) {
             v = A::vmax(prev[k], oth[k]);
         } else {
             v = A::from_bits(0);
 #pragma unroll
-            for (int d = 0; d < M; d++) v = A::vmax(v, A::from_bits(lds64(lane + free_off + d * kSlotStride + k * 256)));
+            for (int d = 0; d < M; d++) v = A::vmax(v, A::from_bits(lds64(lane + free_off * NP + d * NP * 256 + k * 256)));
         }
         mk[k] = A::ps(v);
         if (MEM && mu[k].over(cap)) mk[k] = kInfeasible;
@@ -488,27 +489,27 @@ __device__ __forceinline__ double cut_add_f64(double v, uint32_t dev, double c, 
     return __fma_rn(c, one_if(cut_bit<M>((uint32_t)__double2loint(v), dev), khi), v);
 }
 
-template <int M, bool MEM, class Gen>
-__device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
+template <int M, int NP, bool MEM, class Gen>
+__device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint32_t ops, uint32_t xr,
                                              const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
                                              uint32_t K8, uint64_t cap, uint32_t khi) {
     constexpr double kBig = 1125899906842624.0;   // 2^50
     constexpr bool SM = M > 2;                    // free[] in shared memory
-    double prev[kNP], oth[kNP];
-    uint32_t pdev[kNP];
-    MemUse<M> mu[kNP];
+    double prev[NP], oth[NP];
+    uint32_t pdev[NP];
+    MemUse<M> mu[NP];
 #pragma unroll
-    for (int k = 0; k < kNP; k++) {
+    for (int k = 0; k < NP; k++) {
         prev[k] = 0.0;
         oth[k] = 0.0;
         pdev[k] = 0;
         if (MEM) mu[k].init();
         if (SM) {
 #pragma unroll
-            for (int d = 0; d < M; d++) std_(lane + free_off + d * kSlotStride + k * 256, 0.0);
+            for (int d = 0; d < M; d++) std_(lane + free_off * NP + d * NP * 256 + k * 256, 0.0);
         }
     }
-    auto fslot = [&](int k, uint32_t d) { return lane + free_off + d * kSlotStride + k * 256; };
+    auto fslot = [&](int k, uint32_t d) { return lane + free_off * NP + d * NP * 256 + k * 256; };
     uint32_t x = xr;
 
     auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
@@ -516,13 +517,13 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint
         const uint4 b = lds128(rec + 16);
         const double cost = __hiloint2double((int)a.y, (int)a.x);
         const double c0 = __hiloint2double((int)a.w, (int)a.z);
-        uint32_t dev[kNP];
+        uint32_t dev[NP];
 #pragma unroll
-        for (int k = 0; k < kNP; k++) dev[k] = gen.dev(k, p, c, b.w);
+        for (int k = 0; k < NP; k++) dev[k] = gen.dev(k, p, c, b.w);
         if (b.z == 0) {
             // chain step: the only input is the previous step's output
 #pragma unroll
-            for (int k = 0; k < kNP; k++) {
+            for (int k = 0; k < NP; k++) {
                 const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
                 const double same = __dadd_rn(1.0, -cut);
                 const double t = __fma_rn(c0, cut, prev[k]);
@@ -538,13 +539,13 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint
                 pdev[k] = dev[k];
             }
         } else {
-            double r[kNP];
+            double r[NP];
             if (b.x == kFromPrev) {
 #pragma unroll
-                for (int k = 0; k < kNP; k++) r[k] = __fma_rn(c0, one_if(cut_bit<M>(pdev[k], dev[k]), khi), prev[k]);
+                for (int k = 0; k < NP; k++) r[k] = __fma_rn(c0, one_if(cut_bit<M>(pdev[k], dev[k]), khi), prev[k]);
             } else {
 #pragma unroll
-                for (int k = 0; k < kNP; k++) r[k] = cut_add_f64<M>(ldd(lane + b.x + k * 256), dev[k], c0, khi);
+                for (int k = 0; k < NP; k++) r[k] = cut_add_f64<M>(ldd(lane + b.x * NP + k * 256), dev[k], c0, khi);
             }
             const uint32_t nx = b.z & 0xFFFFu;
 #pragma unroll 1
@@ -553,10 +554,10 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint
                 x += sizeof(ExtraRec);
                 const double ce = __hiloint2double((int)e.y, (int)e.x);
 #pragma unroll
-                for (int k = 0; k < kNP; k++) r[k] = dmax(r[k], cut_add_f64<M>(ldd(lane + e.z + k * 256), dev[k], ce, khi));
+                for (int k = 0; k < NP; k++) r[k] = dmax(r[k], cut_add_f64<M>(ldd(lane + e.z * NP + k * 256), dev[k], ce, khi));
             }
 #pragma unroll
-            for (int k = 0; k < kNP; k++) {
+            for (int k = 0; k < NP; k++) {
                 // free[dev] = same ? prev : other, as exact products (FP64 pipe)
                 const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
                 const double same = __dadd_rn(1.0, -cut);
@@ -574,12 +575,12 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint
         }
         if (b.y != kNoStore) {
 #pragma unroll
-            for (int k = 0; k < kNP; k++) std_(lane + b.y + k * 256, with_tag(prev[k], Dev<M>::canon(dev[k])));
+            for (int k = 0; k < NP; k++) std_(lane + b.y * NP + k * 256, with_tag(prev[k], Dev<M>::canon(dev[k])));
         }
         if (MEM && fwd) {
             const uint64_t m = mem[p];
 #pragma unroll
-            for (int k = 0; k < kNP; k++) mu[k].add(Dev<M>::canon(dev[k]), m);
+            for (int k = 0; k < NP; k++) mu[k].add(Dev<M>::canon(dev[k]), m);
         }
     };
     const uint32_t G = K8 / 8;
@@ -605,7 +606,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint
         }
     }
 #pragma unroll
-    for (int k = 0; k < kNP; k++) {
+    for (int k = 0; k < NP; k++) {
         double v = prev[k];
         if (SM) {
 #pragma unroll
@@ -618,12 +619,12 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[kNP], uint
     }
 }
 
-template <int M, bool MEM, bool F64, class Gen>
-__device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[kNP], uint32_t ops, uint32_t xr,
+template <int M, int NP, bool MEM, bool F64, class Gen>
+__device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[NP], uint32_t ops, uint32_t xr,
                                             const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
                                             uint32_t K8, uint64_t cap, uint32_t khi) {
-    if constexpr (F64 && M >= 2) schedule_f64<M, MEM>(gen, mk, ops, xr, mem, lane, free_off, K8, cap, khi);
-    else schedule_gen<M, MEM, F64>(gen, mk, ops, xr, mem, lane, free_off, K8, cap);
+    if constexpr (F64 && M >= 2) schedule_f64<M, NP, MEM>(gen, mk, ops, xr, mem, lane, free_off, K8, cap, khi);
+    else schedule_gen<M, NP, MEM, F64>(gen, mk, ops, xr, mem, lane, free_off, K8, cap);
 }
 
 __device__ __forceinline__ bool lex_less(uint64_t m1, uint64_t i1, uint64_t m2, uint64_t i2) {
@@ -631,7 +632,7 @@ __device__ __forceinline__ bool lex_less(uint64_t m1, uint64_t i1, uint64_t m2, 
 }
 
 // ------------------------------------------------------------------ kernel
-template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64>
+template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64, int NP>
 __global__ void __launch_bounds__(256, PP_MIN_CTAS) search_kernel(const KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t mbar;
@@ -666,7 +667,7 @@ __global__ void __launch_bounds__(256, PP_MIN_CTAS) search_kernel(const KParams 
     const uint32_t smem_base = (uint32_t)__cvta_generic_to_shared(smem);
     const uint32_t lane_region = smem_base + P.smem_slots_off + warp * P.region_bytes + lane * 8;
 #pragma unroll
-    for (int k = 0; k < kNP; k++) sts64(lane_region + P.zero_off + k * 256, 0);
+    for (int k = 0; k < NP; k++) sts64(lane_region + P.zero_off * NP + k * 256, 0);
     {
         uint32_t done = 0;
         while (!done) {
@@ -686,40 +687,40 @@ __global__ void __launch_bounds__(256, PP_MIN_CTAS) search_kernel(const KParams 
     uint64_t best_mk = kInfeasible, best_i = kInfeasible;
     bool have = false;
     const uint64_t n = P.end - P.begin;
-    constexpr uint32_t TILE = 32 * kNP;
+    constexpr uint32_t TILE = 32 * NP;
     const uint64_t ntiles = (n + TILE - 1) / TILE;
     const uint64_t wpb = nthreads >> 5;
     for (uint64_t tile = blockIdx.x * wpb + warp; tile < ntiles; tile += (uint64_t)gridDim.x * wpb) {
-        uint64_t off[kNP], idx[kNP];
-        bool valid[kNP];
+        uint64_t off[NP], idx[NP];
+        bool valid[NP];
 #pragma unroll
-        for (int k = 0; k < kNP; k++) {
+        for (int k = 0; k < NP; k++) {
             off[k] = tile * TILE + k * 32 + lane;
             valid[k] = off[k] < n;
             idx[k] = P.begin + (valid[k] ? off[k] : n - 1);
         }
-        uint64_t mk[kNP];
+        uint64_t mk[NP];
         if (GEN == GEN_GRAY) {
-            GrayGen<M> g;
+            GrayGen<M, NP> g;
             g.init(idx, P.K);
-            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
+            schedule_np<M, NP, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
         } else if (GEN == GEN_RANDOM) {
-            RandomGen<M> g;
+            RandomGen<M, NP> g;
             g.init(idx, P.seed, P.K);
-            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
+            schedule_np<M, NP, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
         } else if (GEN == GEN_PERTURB) {
-            PerturbGen<M> g;
+            PerturbGen<M, NP> g;
             g.init(idx, P.seed, P.K, P.tau);
-            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
+            schedule_np<M, NP, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
         } else {
-            ExplicitGen g;
+            ExplicitGen<NP> g;
 #pragma unroll
-            for (int k = 0; k < kNP; k++) g.row[k] = P.g_place + (idx[k] - P.begin) * (uint64_t)P.K;
+            for (int k = 0; k < NP; k++) g.row[k] = P.g_place + (idx[k] - P.begin) * (uint64_t)P.K;
             g.orig = orig;
-            schedule_np<M, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
+            schedule_np<M, NP, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
         }
 #pragma unroll
-        for (int k = 0; k < kNP; k++) {
+        for (int k = 0; k < NP; k++) {
             if (WRITE_ALL) {
                 if (valid[k]) P.g_makespan[off[k]] = mk[k];
             } else if (valid[k] && (!have || lex_less(mk[k], idx[k], best_mk, best_i))) {
@@ -803,23 +804,21 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
         improve = (U.round == 0) || (mk < s[SC_BEST_MK]);
     }
     __syncthreads();
-    uint64_t ii[kNP];
-#pragma unroll
-    for (int k = 0; k < kNP; k++) ii[k] = idx_s;
+    const uint64_t ii[1] = {idx_s};
     for (uint32_t p = threadIdx.x; p < U.K; p += blockDim.x) {
         uint32_t d;
         if (GEN == GEN_GRAY) {
-            GrayGen<M> g;
+            GrayGen<M, 1> g;
             g.init(ii, U.K);
             d = g.dev(0, p, p % 8, 0);
         } else if (GEN == GEN_RANDOM) {
-            RandomGen<M> g;
+            RandomGen<M, 1> g;
             g.init(ii, U.seed, U.K);
             g.refresh(p / 8);
             g.sub((p / 4) & 1);
             d = g.dev(0, p, p % 4, 0);
         } else {
-            PerturbGen<M> g;
+            PerturbGen<M, 1> g;
             g.init(ii, U.seed, U.K, U.tau);
             g.refresh(p / 8);
             g.sub((p / 4) & 1);
@@ -845,9 +844,9 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
     }
 }
 
-template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64>
+template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64, int NP>
 int launch_search(const KParams &p, int grid, int threads, int smem, void *stream) {
-    search_kernel<M, GEN, MEM, WRITE_ALL, F64><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
+    search_kernel<M, GEN, MEM, WRITE_ALL, F64, NP><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
     return (int)cudaGetLastError();
 }
 
