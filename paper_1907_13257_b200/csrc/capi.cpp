@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -130,13 +131,16 @@ static int choose(const pp_dfg *g, int M, int gen, bool write_all, int np, Choic
 static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin, uint64_t end, Launch &L) {
     Choice best;
     int best_warps = -1;
+    int forced = 0;   // PP_NP=1|2|4 pins NP (tests cover every variant)
+    if (const char *v = getenv("PP_NP")) forced = atoi(v);
     for (int np : {4, 2, 1}) {
+        if (forced && np != forced) continue;
         Choice c;
         int rc = choose(g, M, gen, write_all, np, c);
         if (rc == PP_E_TOO_LARGE) continue;
         if (rc) return rc;
         const int warps = c.ctas * c.threads / 32;
-        if (warps >= 12 || write_all) { best = c; best_warps = warps; break; }
+        if (warps >= 12 || write_all || forced) { best = c; best_warps = warps; break; }
         // otherwise keep the most placements in flight, ties to more warps
         if (best_warps < 0 || warps * c.np > best_warps * best.np ||
             (warps * c.np == best_warps * best.np && warps > best_warps)) {

@@ -272,3 +272,18 @@ def test_nccl_communicator_single_rank(dfgs):
     assert np.array_equal(a.placement, b.placement)
     o = od.search(2, O.GEN_PERTURB, 7, 30_001, rounds=3, tau=8)
     assert a.best_makespan_ps == o.best_makespan_ps and a.best_index == o.best_index
+
+
+@pytest.mark.parametrize("np_", ["1", "2", "4"])
+def test_every_placements_per_lane_variant(dfgs, np_, monkeypatch):
+    """The search kernel is instantiated for NP = 1, 2, 4 placements per lane
+    (chosen per launch); pin each and compare the argmin with the oracle."""
+    monkeypatch.setenv("PP_NP", np_)
+    for name, M, gen in [("gnmt", 2, O.GEN_PERTURB), ("inception_v3", 4, O.GEN_RANDOM), ("toy12", 3, O.GEN_GRAY),
+                         ("biglstm", 8, O.GEN_PERTURB)]:
+        spec, g, od = dfgs[name]
+        count = 729 if name == "toy12" else 9_001
+        base = np.zeros(g.K, dtype=np.uint8)
+        got = pp.u64(g.search_range(M, gen, 77, 24, base, 3, 3 + count))
+        want = od.round(M, gen, 77, 24, base, 3, 3 + count)
+        assert (int(got[0]), int(got[1])) == want, (name, np_)
