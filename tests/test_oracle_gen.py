@@ -76,3 +76,40 @@ def test_perturb_rules(M):
 def test_m1_is_all_zero():
     for g in (O.GEN_GRAY, O.GEN_RANDOM, O.GEN_PERTURB):
         assert not O.gen(20, 1, g, 5, 128, None, 3).any()
+
+
+# ---------------------------------------------------------------------------
+# Layout pins: choose the seed so that the generator's word is exactly a
+# PUBLISHED SplitMix64 output (state 1234567: outputs 6457827717110365317,
+# 3203168211198807973, 9817491932198370423 for the 1st, 2nd, 3rd call).  The
+# expected placement then follows from the literal's bits/bytes, independently
+# of the oracle's code.  word(i, t) = mix(seed + γ·(i·Wd + t + 1)); with
+# Wd = 1 and (i, t) = (1, 0) the state is seed + 2γ, i.e. the 2nd output.
+SM64_2ND = 3203168211198807973
+SM64_3RD = 9817491932198370423
+C1 = 0xD1B54A32D192ED03
+
+
+def test_random_layout_pinned_by_published_vector():
+    K, M = 60, 2                      # b = 1, P = 64 ops per word, Wd = 1
+    d = O.gen(K, M, O.GEN_RANDOM, 1234567, 0, None, 1)
+    assert [int(x) for x in d] == [(SM64_2ND >> j) & 1 for j in range(K)]
+    K, M = 30, 4                      # b = 2, P = 32, Wd = 1: 2-bit fields
+    d = O.gen(K, M, O.GEN_RANDOM, 1234567, 0, None, 1)
+    assert [int(x) for x in d] == [(SM64_2ND >> (2 * j)) & 3 for j in range(K)]
+    K, M = 16, 8                      # b = 3, P = 16 (48 bits used), Wd = 1
+    d = O.gen(K, M, O.GEN_RANDOM, 1234567, 0, None, 1)
+    assert [int(x) for x in d] == [(SM64_2ND >> (3 * j)) & 7 for j in range(K)]
+    # Wd = 1 and (i, t) = (2, 0): state seed + 3γ, the 3rd output
+    d = O.gen(60, 2, O.GEN_RANDOM, 1234567, 0, None, 2)
+    assert [int(x) for x in d] == [(SM64_3RD >> j) & 1 for j in range(60)]
+
+
+@pytest.mark.parametrize("tau", [0, 77, 128, 200, 256])
+def test_perturb_layout_pinned_by_published_vector(tau):
+    K, M = 8, 2                       # 8 ops per word, Wd = 1
+    seed_r = 1234567 ^ C1             # so that the u-stream seed is 1234567
+    base = np.array([0, 1, 1, 0, 1, 0, 0, 1], dtype=np.uint8)
+    d = O.gen(K, M, O.GEN_PERTURB, seed_r, tau, base, 1)
+    u = [(SM64_2ND >> (8 * j)) & 0xFF for j in range(8)]
+    assert [int(x) for x in d] == [1 - int(base[j]) if u[j] < tau else int(base[j]) for j in range(8)]
