@@ -19,8 +19,10 @@
  *   or_schedule                pinned (K1–K7, brute-force longest path, invariants)
  *   or_gen (GRAY)              pinned (Gray property: one digit changes per step,
  *                              bijection onto [0,M)^K; M=2 equals i^(i>>1))
- *   or_gen (RANDOM, PERTURB)   pinned (SplitMix64 published test vector of the
- *                              finaliser; distribution/flip-rate properties)
+ *   or_gen (RANDOM, PERTURB)   pinned (seeds chosen so the generator word IS a
+ *                              published SplitMix64 output: the expected bits /
+ *                              bytes of the placement come from that literal;
+ *                              distribution and flip-rate properties)
  *   or_round / or_search       pinned (K2, K3, K8, exhaustive == brute force)
  *   or_ar                      pinned (K9 closed form)
  *   or_epochs / or_cell        pinned (K10–K12 paper ratios)
