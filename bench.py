@@ -41,8 +41,19 @@ WORKLOADS = {"inception_v3": "Inception-V3-shaped (synth.inception_v3, batch 64)
              "toy12": "toy-12 (SURVEY 8(d) config 1)"}
 
 
+HW_GRAPHS = {"cube_mesh": "8 devices, DGX-1-style hybrid cube-mesh (synth.hw.hybrid_cube_mesh)",
+             "switch": "8 devices on one switch (synth.hw.switch)",
+             "ring": "8-device ring (synth.hw.ring)",
+             "two_nodes": "2 nodes x 4 devices, switch per node, one network link (synth.hw.two_nodes)"}
+
+
 def workload(args):
-    return getattr(synth, args.workload)()
+    spec = getattr(synth, args.workload)()
+    if args.hw != "none":   # general hardware graph
+        from synth import hw as H
+        spec["hw"] = {"cube_mesh": H.hybrid_cube_mesh, "switch": lambda: H.switch(8), "ring": lambda: H.ring(8),
+                      "two_nodes": lambda: H.two_nodes(4)}[args.hw]()
+    return spec
 
 
 def scenario(args, t1, grad):
@@ -195,12 +206,14 @@ def run_reference(args):
 def config_dict(args, spec, per_step=None):
     gen = (f"PERTURB tau={args.tau}/256, {args.rounds} rounds x {args.count:.0e}" if args.gen == "perturb"
            else f"RANDOM {args.count:.0e}").replace("+0", "")
-    return {"workload": f"{args.workload}_shaped_M{args.M}_{args.gen}_{args.count * args.rounds:.0e}".replace("+0", ""),
+    hw = f"_hw-{args.hw}" if args.hw != "none" else ""
+    return {"workload": f"{args.workload}_shaped_M{args.M}_{args.gen}_{args.count * args.rounds:.0e}{hw}".replace("+0", ""),
             "dfg": WORKLOADS[args.workload], "K": len(spec["fwd_ps"]),
             "E": len(spec["edge_src"]), "M": args.M, "generator": gen + " (SplitMix64)", "seed": SEED,
             "candidates_per_step": per_step or args.count * args.rounds,
             "projection": f"M in {{1,{args.M}}}, N=1..{args.nmax}, EQ5, ring AR on",
-            "l2": "flushed between timed steps (256 MiB write); inputs live on-chip"}
+            "l2": "flushed between timed steps (256 MiB write); inputs live on-chip",
+            **({"hardware_graph": HW_GRAPHS[args.hw]} if args.hw != "none" else {})}
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -301,7 +314,7 @@ def run_pp(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": config_dict(args, spec),
+            "config": {**config_dict(args, spec), "image_bytes": g.image_bytes, "live_slots": g.W},
             "gpu_launches": int(launches),
             "roofline": {"bound": "alu", "achieved": achieved_ops / 1e12, "peak": pk["int32_ops_per_s"] / 1e12,
                          "unit": "Tops/s (int32)", "frac": achieved_ops / pk["int32_ops_per_s"],
@@ -344,6 +357,8 @@ def main():
     ap.add_argument("--gen", default="perturb", choices=["perturb", "random"])
     ap.add_argument("--tau", type=int, default=8)
     ap.add_argument("--nmax", type=int, default=1024)
+    ap.add_argument("--hw", default="none", choices=["none", *HW_GRAPHS],
+                    help="evaluate on a general hardware graph instead of the uniform link")
     ap.add_argument("--ref-sample", type=int, default=200_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -82,6 +82,24 @@ typedef struct {
     uint64_t dev_mem_cap_bytes;  /* Mem(n); 0 = unlimited (R7)   */
 } pp_link_desc;
 
+/* The general hardware graph (Table 2
+ * PAPER.md:379–392): device nodes 0..num_devices−1, router nodes
+ * num_devices..num_devices+num_routers−1, bidirectional links with bandwidth
+ * B(l) > 0 B/s and latency L(l) ps.  A cut edge e from device a to device b
+ * costs the delay of its delay-shortest route for its payload
+ * (PAPER.md:455–462 Δ_e = Σ_l C_el·(D(e)/B(l) + L(l))):
+ *   c(e, a, b) = min over paths a → b of Σ_hops (⌈D(e)·10^12 / B⌉ + L).
+ * A search with M devices uses devices 0..M−1 (M ≤ num_devices).            */
+typedef struct {
+    int32_t         num_devices;      /* 1..8                                       */
+    int32_t         num_routers;      /* ≥ 0                                        */
+    int32_t         num_links;
+    const int32_t  *link_a, *link_b;  /* [num_links] node ids, a ≠ b                 */
+    const uint64_t *link_bw_Bps;      /* [num_links] B(l) > 0                        */
+    const uint64_t *link_lat_ps;      /* [num_links] L(l)                            */
+    uint64_t        dev_mem_cap_bytes;/* Mem(n), 0 = unlimited                        */
+} pp_hw_desc;
+
 typedef struct {
     int32_t  num_ops, num_edges;
     int32_t  num_slots;          /* W: live finish-time slots per placement         */
@@ -97,6 +115,12 @@ typedef struct {
  * PP_E_CUDA.  On success *out owns device memory until pp_free_dfg.         */
 int  pp_load_dfg(const pp_dfg_desc *desc, const pp_link_desc *link, int cuda_device,
                  pp_dfg **out);
+/* As pp_load_dfg on a general hardware graph.  Device pairs whose cost on
+ * every edge (both directions) agree share a cost class; the image holds one
+ * cost row per input and class.  Needs every time bound < 2^49 ps (tagged-f64
+ * arithmetic) else PP_E_RANGE; devices must be connected else PP_E_INVALID;
+ * PP_E_TOO_LARGE when the rows do not fit in the 96 KB image.              */
+int  pp_load_dfg_hw(const pp_dfg_desc *desc, const pp_hw_desc *hw, int cuda_device, pp_dfg **out);
 void pp_free_dfg(pp_dfg *dfg);
 int  pp_dfg_get_info(const pp_dfg *dfg, pp_dfg_info *out);
 /* host ptr pi_out[K]: pi_out[p] = descriptor index of the op at π position p */

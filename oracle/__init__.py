@@ -45,6 +45,13 @@ class _Input(C.Structure):
                 ("dev_mem_cap_bytes", C.c_uint64)]
 
 
+class _Hw(C.Structure):
+    _fields_ = [("num_devices", C.c_int32), ("num_routers", C.c_int32), ("num_links", C.c_int32),
+                ("link_a", C.POINTER(C.c_int32)), ("link_b", C.POINTER(C.c_int32)),
+                ("link_bw_Bps", C.POINTER(C.c_uint64)), ("link_lat_ps", C.POINTER(C.c_uint64)),
+                ("dev_mem_cap_bytes", C.c_uint64)]
+
+
 class _Result(C.Structure):
     _fields_ = [("best_makespan_ps", C.c_uint64), ("best_index", C.c_uint64),
                 ("best_round", C.c_uint64), ("t1_ps", C.c_uint64), ("evaluated", C.c_uint64)]
@@ -89,6 +96,10 @@ def lib():
         P = C.POINTER
         L.or_prepare.argtypes = [P(_Input), P(C.c_void_p), C.c_char_p, C.c_int]
         L.or_prepare.restype = C.c_int
+        L.or_prepare_hw.argtypes = [P(_Input), P(_Hw), P(C.c_void_p), C.c_char_p, C.c_int]
+        L.or_prepare_hw.restype = C.c_int
+        L.or_hw_edge_cost.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.or_hw_edge_cost.restype = C.c_uint64
         L.or_free.argtypes = [C.c_void_p]
         L.or_num_ops.argtypes = [C.c_void_p]
         L.or_get_pi.argtypes = [C.c_void_p, P(C.c_int32)]
@@ -146,9 +157,9 @@ class SearchResult:
 class Dfg:
     """Prepared DFG (π, adjacency, edge costs).  Arrays in descriptor order."""
 
-    def __init__(self, fwd_ps, bwd_ps, edge_src, edge_dst, edge_fwd_bytes, link_bw_Bps,
-                 link_lat_ps, edge_bwd_bytes=None, op_id=None, mem_bytes=None,
-                 param_bytes=None, dev_mem_cap_bytes=0):
+    def __init__(self, fwd_ps, bwd_ps, edge_src, edge_dst, edge_fwd_bytes, link_bw_Bps=1,
+                 link_lat_ps=0, edge_bwd_bytes=None, op_id=None, mem_bytes=None,
+                 param_bytes=None, dev_mem_cap_bytes=0, hw=None):
         self._keep = []
         fwd = _u64(fwd_ps); bwd = _u64(bwd_ps)
         K = len(fwd)
@@ -166,7 +177,17 @@ class Dfg:
                      int(link_bw_Bps), int(link_lat_ps), int(dev_mem_cap_bytes))
         h = C.c_void_p()
         err = C.create_string_buffer(512)
-        rc = lib().or_prepare(C.byref(inp), C.byref(h), err, 512)
+        if hw is None:
+            rc = lib().or_prepare(C.byref(inp), C.byref(h), err, 512)
+        else:
+            la = np.ascontiguousarray(np.asarray(hw["link_a"], dtype=np.int32))
+            lb = np.ascontiguousarray(np.asarray(hw["link_b"], dtype=np.int32))
+            bw = _u64(hw["link_bw_Bps"]); lat = _u64(hw["link_lat_ps"])
+            self._keep += [la, lb, bw, lat]
+            h_ = _Hw(int(hw["num_devices"]), int(hw.get("num_routers", 0)), len(la), _ptr(la, C.c_int32),
+                     _ptr(lb, C.c_int32), _ptr(bw, C.c_uint64), _ptr(lat, C.c_uint64),
+                     int(hw.get("dev_mem_cap_bytes", 0)))
+            rc = lib().or_prepare_hw(C.byref(inp), C.byref(h_), C.byref(h), err, 512)
         if rc:
             raise OracleError(rc, err.value.decode())
         self._h = h
@@ -177,7 +198,7 @@ class Dfg:
     def from_spec(cls, spec: dict) -> "Dfg":
         keys = ["fwd_ps", "bwd_ps", "edge_src", "edge_dst", "edge_fwd_bytes", "link_bw_Bps",
                 "link_lat_ps", "edge_bwd_bytes", "op_id", "mem_bytes", "param_bytes",
-                "dev_mem_cap_bytes"]
+                "dev_mem_cap_bytes", "hw"]
         return cls(**{k: spec[k] for k in keys if k in spec and spec[k] is not None})
 
     def __del__(self):
@@ -190,6 +211,10 @@ class Dfg:
         out = np.zeros(self.K, dtype=np.int32)
         lib().or_get_pi(self._h, out.ctypes.data_as(C.POINTER(C.c_int32)))
         return out
+
+    def hw_edge_cost(self, e, a, b, bwd=False) -> int:
+        """c(e, a, b) of the hardware graph (0 when a == b)."""
+        return int(lib().or_hw_edge_cost(self._h, e, a, b, 1 if bwd else 0))
 
     @property
     def t1(self) -> int:

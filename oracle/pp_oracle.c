@@ -75,7 +75,21 @@ typedef struct {
     uint64_t cap;
     uint64_t t1;
     uint64_t grad_bytes;
+    /* general hardware graph (NEXT f2): per-edge cost for every ordered
+     * device pair, cfm[(eid·nd + a)·nd + b]; adjacency lists carry edge ids */
+    int nd;                 /* 0 = one uniform hop (R4) */
+    int **in_eid, **out_eid;
+    uint64_t *cfm, *cbm;
 } or_ctx;
+
+/* Hardware graph of PAPER.md:352 (§6): devices 0..nd−1, routers nd..nd+R−1,
+ * bidirectional links with bandwidth B(l) > 0 and latency L(l).             */
+typedef struct {
+    int32_t num_devices, num_routers, num_links;
+    const int32_t *link_a, *link_b;
+    const uint64_t *link_bw_Bps, *link_lat_ps;
+    uint64_t dev_mem_cap_bytes;
+} or_hw;
 
 static void set_err(char *err, int errlen, const char *msg) {
     if (err && errlen > 0) { strncpy(err, msg, (size_t)errlen - 1); err[errlen - 1] = 0; }
@@ -100,6 +114,8 @@ void or_free(or_ctx *c) {
         if (c->out_dst) free(c->out_dst[p]);
         if (c->out_cb) free(c->out_cb[p]);
     }
+    if (c->in_eid) for (int p = 0; p < c->K; p++) { free(c->in_eid[p]); free(c->out_eid[p]); }
+    free(c->in_eid); free(c->out_eid); free(c->cfm); free(c->cbm);
     free(c->in_src); free(c->in_cf); free(c->out_dst); free(c->out_cb);
     free(c->in_cnt); free(c->out_cnt);
     free(c->id); free(c->pi); free(c->pos); free(c->df); free(c->db); free(c->mem);
@@ -225,6 +241,104 @@ int or_prepare(const or_input *in, or_ctx **out, char *err, int errlen) {
     return OR_OK;
 }
 
+/* NEXT f2 — the general hardware graph (Δ_e = Σ_l C_el·(D(e)/B(l)
+ * + L(l))).  Reading: a transfer uses the delay-shortest
+ * route for its payload (with no link contention, R5, this is
+ * what the ILP optimum picks), each hop charged ⌈D·10^12/B(l)⌉ + L(l) ps:
+ *   c(e, a, b) = min over paths a → b of Σ_hops (⌈D(e)·10^12/B⌉ + L).
+ * Plain Dijkstra (O(V^2)) per edge, per direction and per source device.     */
+static u128 dijkstra_cost(const or_hw *hw, uint64_t bytes, int src, int dst) {
+    int V = hw->num_devices + hw->num_routers;
+    u128 *dist = malloc(sizeof(u128) * (size_t)V);
+    char *done = calloc((size_t)V, 1);
+    const u128 INF = ~(u128)0;
+    for (int v = 0; v < V; v++) dist[v] = INF;
+    dist[src] = 0;
+    for (int it = 0; it < V; it++) {
+        int u = -1;
+        for (int v = 0; v < V; v++) if (!done[v] && dist[v] != INF && (u < 0 || dist[v] < dist[u])) u = v;
+        if (u < 0) break;
+        done[u] = 1;
+        for (int l = 0; l < hw->num_links; l++) {
+            int a = hw->link_a[l], b = hw->link_b[l], v;
+            if (a == u) v = b; else if (b == u) v = a; else continue;
+            u128 w = ((u128)bytes * 1000000000000ULL + hw->link_bw_Bps[l] - 1) / hw->link_bw_Bps[l] + hw->link_lat_ps[l];
+            if (dist[u] + w < dist[v]) dist[v] = dist[u] + w;
+        }
+    }
+    u128 r = dist[dst];
+    free(dist); free(done);
+    return r;
+}
+
+int or_prepare_hw(const or_input *in, const or_hw *hw, or_ctx **out, char *err, int errlen) {
+    *out = NULL;
+    if (!hw || hw->num_devices < 1 || hw->num_devices > 8 || hw->num_routers < 0 || hw->num_links < 0) {
+        set_err(err, errlen, "invalid hardware graph sizes"); return OR_E_INVALID;
+    }
+    int V = hw->num_devices + hw->num_routers;
+    for (int l = 0; l < hw->num_links; l++) {
+        if (hw->link_a[l] < 0 || hw->link_a[l] >= V || hw->link_b[l] < 0 || hw->link_b[l] >= V ||
+            hw->link_a[l] == hw->link_b[l] || hw->link_bw_Bps[l] == 0) {
+            set_err(err, errlen, "invalid link"); return OR_E_INVALID;
+        }
+    }
+    /* the DFG part, with a dummy uniform link (costs replaced below) */
+    or_input in2 = *in;
+    in2.link_bw_Bps = 1000000000000ULL;
+    in2.link_lat_ps = 0;
+    in2.dev_mem_cap_bytes = hw->dev_mem_cap_bytes;
+    int rc = or_prepare(&in2, out, err, errlen);
+    if (rc) return rc;
+    or_ctx *c = *out;
+    int nd = hw->num_devices, E = c->E, K = c->K;
+    for (int a = 0; a < nd; a++)
+        for (int b = 0; b < nd; b++)
+            if (a != b && dijkstra_cost(hw, 0, a, b) == ~(u128)0) {
+                set_err(err, errlen, "devices not connected"); or_free(c); *out = NULL; return OR_E_INVALID;
+            }
+    c->nd = nd;
+    c->cfm = calloc((size_t)E * nd * nd + 1, 8);
+    c->cbm = calloc((size_t)E * nd * nd + 1, 8);
+    u128 bound = c->t1;
+    for (int e = 0; e < E; e++) {
+        uint64_t bf = in->edge_fwd_bytes[e], bb = in->edge_bwd_bytes ? in->edge_bwd_bytes[e] : bf;
+        u128 mf = 0, mb = 0;
+        for (int a = 0; a < nd; a++)
+            for (int b = 0; b < nd; b++) {
+                if (a == b) continue;
+                u128 f = dijkstra_cost(hw, bf, a, b), g = dijkstra_cost(hw, bb, a, b);
+                if ((f >> 64) || (g >> 64)) { set_err(err, errlen, "edge cost overflow"); or_free(c); *out = NULL; return OR_E_RANGE; }
+                c->cfm[((size_t)e * nd + a) * nd + b] = (uint64_t)f;
+                c->cbm[((size_t)e * nd + a) * nd + b] = (uint64_t)g;
+                if (f > mf) mf = f;
+                if (g > mb) mb = g;
+            }
+        bound += mf + mb;
+    }
+    if (bound >> 61) { set_err(err, errlen, "time bound >= 2^61 ps"); or_free(c); *out = NULL; return OR_E_RANGE; }
+    /* adjacency lists with edge ids, in the same order as in_src / out_dst */
+    c->in_eid = calloc((size_t)K, sizeof(int *));
+    c->out_eid = calloc((size_t)K, sizeof(int *));
+    int *ic = calloc((size_t)K, sizeof(int)), *oc = calloc((size_t)K, sizeof(int));
+    for (int p = 0; p < K; p++) {
+        c->in_eid[p] = malloc(sizeof(int) * (size_t)(c->in_cnt[p] + 1));
+        c->out_eid[p] = malloc(sizeof(int) * (size_t)(c->out_cnt[p] + 1));
+    }
+    for (int e = 0; e < E; e++) {
+        int u = c->pos[in->edge_src[e]], v = c->pos[in->edge_dst[e]];
+        c->in_eid[v][ic[v]++] = e;
+        c->out_eid[u][oc[u]++] = e;
+    }
+    free(ic); free(oc);
+    return OR_OK;
+}
+
+uint64_t or_hw_edge_cost(const or_ctx *c, int e, int a, int b, int bwd) {
+    if (!c->nd || a == b) return 0;
+    return (bwd ? c->cbm : c->cfm)[((size_t)e * c->nd + a) * c->nd + b];
+}
+
 int or_num_ops(const or_ctx *c) { return c->K; }
 void or_get_pi(const or_ctx *c, int32_t *pi_out) { for (int p = 0; p < c->K; p++) pi_out[p] = c->pi[p]; }
 /* O4 / R8: T_1 = Σ_k (Δf(k)+Δb(k)), the all-on-one-device makespan (PAPER.md:501 assumption 1). */
@@ -247,7 +361,8 @@ uint64_t or_schedule_ex(const or_ctx *c, int M, const uint8_t *d,
         uint64_t r = 0;
         for (int i = 0; i < c->in_cnt[p]; i++) {
             int u = c->in_src[p][i];
-            uint64_t t = fin[u] + (d[u] != d[p] ? c->in_cf[p][i] : 0);
+            uint64_t cost = c->nd ? c->cfm[((size_t)c->in_eid[p][i] * c->nd + d[u]) * c->nd + d[p]] : c->in_cf[p][i];
+            uint64_t t = fin[u] + (d[u] != d[p] ? cost : 0);
             if (t > r) r = t;
         }
         uint64_t s = r > free_t[d[p]] ? r : free_t[d[p]];
@@ -259,7 +374,8 @@ uint64_t or_schedule_ex(const or_ctx *c, int M, const uint8_t *d,
         uint64_t r = (c->out_cnt[p] == 0) ? fin[p] : 0;  /* a sink waits for its own forward (R1) */
         for (int i = 0; i < c->out_cnt[p]; i++) {
             int w = c->out_dst[p][i];
-            uint64_t t = finb[w] + (d[w] != d[p] ? c->out_cb[p][i] : 0);
+            uint64_t cost = c->nd ? c->cbm[((size_t)c->out_eid[p][i] * c->nd + d[w]) * c->nd + d[p]] : c->out_cb[p][i];
+            uint64_t t = finb[w] + (d[w] != d[p] ? cost : 0);
             if (t > r) r = t;
         }
         uint64_t s = r > free_t[d[p]] ? r : free_t[d[p]];
@@ -287,7 +403,7 @@ uint64_t or_schedule(const or_ctx *c, int M, const uint8_t *d_pi) {
 
 /* placement given in original (descriptor) op order */
 int or_makespan_orig(const or_ctx *c, int M, const uint8_t *d_orig, uint64_t *out) {
-    if (M < 1 || M > 8) return OR_E_INVALID;
+    if (M < 1 || M > 8 || (c->nd && M > c->nd)) return OR_E_INVALID;
     uint8_t *d = malloc((size_t)c->K);
     for (int p = 0; p < c->K; p++) {
         d[p] = d_orig[c->pi[p]];
@@ -405,6 +521,7 @@ int or_search(const or_ctx *c, int M, int gen, uint64_t seed, uint64_t count,
               or_result *res, uint8_t *placement_orig) {
     int K = c->K;
     if (M < 1 || M > 8 || count < 1 || rounds < 1 || gen < 0 || gen > 2 || tau > 256) return OR_E_INVALID;
+    if (c->nd && M > c->nd) return OR_E_INVALID;   /* devices 0..M−1 of the hardware graph */
     if (gen != OR_GEN_PERTURB && rounds != 1) return OR_E_INVALID;
     if (gen == OR_GEN_GRAY) {
         u128 space = 1;

@@ -25,23 +25,23 @@ static uint64_t g_timing_n = 0;
 void set_error(const std::string &msg) { g_err = msg; }
 void note_launch() { g_launches++; }
 
-int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp_dfg **out);
+int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *hw, int cuda_device, pp_dfg **out);
 
-#define PP_DECL_M(m)                                                          \
-    KernelInfo kernel_for_m##m(int gen, bool mem, bool wa, bool f64, int np); \
+#define PP_DECL_M(m)                                                                   \
+    KernelInfo kernel_for_m##m(int gen, bool mem, bool wa, bool f64, int np, bool hw); \
     UpdateFn update_for_m##m(int gen);
 PP_DECL_M(1) PP_DECL_M(2) PP_DECL_M(3) PP_DECL_M(4) PP_DECL_M(5) PP_DECL_M(6) PP_DECL_M(7) PP_DECL_M(8)
 
-KernelInfo kernel_for(int M, int gen, bool mem, bool wa, bool f64, int np) {
+KernelInfo kernel_for(int M, int gen, bool mem, bool wa, bool f64, int np, bool hw) {
     switch (M) {
-        case 1: return kernel_for_m1(gen, mem, wa, f64, np);
-        case 2: return kernel_for_m2(gen, mem, wa, f64, np);
-        case 3: return kernel_for_m3(gen, mem, wa, f64, np);
-        case 4: return kernel_for_m4(gen, mem, wa, f64, np);
-        case 5: return kernel_for_m5(gen, mem, wa, f64, np);
-        case 6: return kernel_for_m6(gen, mem, wa, f64, np);
-        case 7: return kernel_for_m7(gen, mem, wa, f64, np);
-        default: return kernel_for_m8(gen, mem, wa, f64, np);
+        case 1: return kernel_for_m1(gen, mem, wa, f64, np, hw);
+        case 2: return kernel_for_m2(gen, mem, wa, f64, np, hw);
+        case 3: return kernel_for_m3(gen, mem, wa, f64, np, hw);
+        case 4: return kernel_for_m4(gen, mem, wa, f64, np, hw);
+        case 5: return kernel_for_m5(gen, mem, wa, f64, np, hw);
+        case 6: return kernel_for_m6(gen, mem, wa, f64, np, hw);
+        case 7: return kernel_for_m7(gen, mem, wa, f64, np, hw);
+        default: return kernel_for_m8(gen, mem, wa, f64, np, hw);
     }
 }
 UpdateFn update_for(int M, int gen) {
@@ -103,7 +103,7 @@ struct Choice {
 
 static int choose(const pp_dfg *g, int M, int gen, bool write_all, int np, Choice &c) {
     const bool mem = g->cap > 0;
-    c.k = kernel_for(M, gen, mem, write_all, g->f64, np);
+    c.k = kernel_for(M, gen, mem, write_all, g->f64, np, g->hw);
     c.np = write_all ? 2 : np;
     const uint32_t nslot = (uint32_t)g->W + 1;                  // live + zero
     c.region = (nslot + (M > 2 ? (uint32_t)M : 0u)) * kSlotUnit * c.np;
@@ -180,6 +180,7 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
     p.free_off = ((uint32_t)g->W + 1) * kSlotUnit;
     p.zero_off = (uint32_t)g->W * kSlotUnit;
     p.one_hi = 0x3FF00000u;
+    p.off_cls = g->off_cls;
     p.g_partials = g->d_partials;
     p.g_ticket = g->d_ticket;
     p.g_out = g->d_scalars + SC_LOCAL_MK;
@@ -196,6 +197,7 @@ static int run(Launch &L, void *stream) {
 static int check_gen_args(const pp_dfg *g, int M, int gen, uint32_t tau, uint64_t end) {
     if (!g) { set_error("dfg is NULL"); return PP_E_INVALID; }
     if (M < 1 || M > 8) { set_error("M must be in [1,8]"); return PP_E_INVALID; }
+    if (g->hw && M > g->nd) { set_error("M exceeds the hardware graph's devices"); return PP_E_INVALID; }
     if (gen < 0 || gen > 2) { set_error("unknown generator"); return PP_E_INVALID; }
     if (tau > 256) { set_error("flip_thresh must be in [0,256]"); return PP_E_INVALID; }
     if (gen == GEN_GRAY) {
@@ -268,7 +270,14 @@ void pp_get_kernel_timing(double *total_ms, uint64_t *n) {
 
 int pp_load_dfg(const pp_dfg_desc *desc, const pp_link_desc *link, int cuda_device, pp_dfg **out) {
     g_err.clear();
-    return load_dfg(desc, link, cuda_device, out);
+    if (!link) { set_error("link is NULL"); return PP_E_INVALID; }
+    return load_dfg(desc, link, nullptr, cuda_device, out);
+}
+
+int pp_load_dfg_hw(const pp_dfg_desc *desc, const pp_hw_desc *hw, int cuda_device, pp_dfg **out) {
+    g_err.clear();
+    if (!hw) { set_error("hw is NULL"); return PP_E_INVALID; }
+    return load_dfg(desc, nullptr, hw, cuda_device, out);
 }
 
 int pp_dfg_get_info(const pp_dfg *g, pp_dfg_info *out) {
@@ -290,7 +299,7 @@ int pp_dfg_get_pi(const pp_dfg *g, int32_t *pi_out) {
 
 int pp_eval_placements(const pp_dfg *g, int M, const uint8_t *d_placements, uint64_t count,
                        uint64_t *d_makespan, void *stream) {
-    if (!g || M < 1 || M > 8 || (count && (!d_placements || !d_makespan))) {
+    if (!g || M < 1 || M > 8 || (g->hw && M > g->nd) || (count && (!d_placements || !d_makespan))) {
         set_error("invalid arguments");
         return PP_E_INVALID;
     }

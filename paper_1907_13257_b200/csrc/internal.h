@@ -16,6 +16,10 @@
 //   [ExtraRec × NX]  the remaining input edges, consumed in step order.
 //   [u64   × K8 ]    M(k) by π position (read only when a memory cap is set)
 //   [u32   × K8 ]    descriptor index of π position p (explicit placements)
+//   [u8    × 64 ]    hardware graph only: cost class of device pair (a, b)
+//   [u64 × rows·C]   hardware graph only: per-input cost rows, one f64-encoded
+//                    cost per class (class 0 = same device, unused); the
+//                    records' cost fields then hold the row's byte offset
 //
 // Per-lane schedule state lives in a per-warp region of shared memory laid out
 // [slot][placement k < NP][lane] × u64, so a slot's byte offset inside the
@@ -97,6 +101,7 @@ struct KParams {
     uint32_t free_off;           // region offset of free[M] (M ≥ 3), in slot units ×256
     uint32_t zero_off;           // region offset of the always-zero slot, in slot units ×256
     uint32_t one_hi;             // 0x3FF00000, the high word of 1.0 (opaque to ptxas)
+    uint32_t off_cls;            // hardware graph: image offset of cls[a·8 + b]
 };
 
 // Device scalar slots of pp_dfg::d_scalars (u64).
@@ -130,7 +135,7 @@ struct KernelInfo {
 };
 
 // search_inst.cu (compiled once per M with -DPP_M): kernel_for_m<M>(...)
-KernelInfo kernel_for(int M, int gen, bool mem, bool write_all, bool f64, int np);
+KernelInfo kernel_for(int M, int gen, bool mem, bool write_all, bool f64, int np, bool hw);
 UpdateFn update_for(int M, int gen);
 
 }  // namespace pp
@@ -139,6 +144,9 @@ struct pp_dfg {
     int device = 0;
     int K = 0, K8 = 0, E = 0, W = 0;
     bool f64 = false;            // tagged-f64 arithmetic (bound < 2^49) else tagged-u64
+    bool hw = false;             // general hardware graph: class-cost rows (pp_load_dfg_hw)
+    int nd = 0;                  // hardware-graph devices
+    uint32_t off_cls = 0;        // image offset of the 8×8 class table
     uint64_t t1 = 0, grad_bytes = 0, cap = 0;
     std::vector<int32_t> pi;     // π position → descriptor index
     std::vector<int32_t> pos;    // descriptor index → π position

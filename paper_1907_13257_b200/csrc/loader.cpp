@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <queue>
 #include <unordered_set>
 
@@ -68,15 +69,56 @@ static int topo_order(int K, const std::vector<int64_t> &id, const std::vector<i
     return fail(PP_E_CYCLE, msg);
 }
 
-int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp_dfg **out) {
+// Delay-shortest route cost from device a to every node for a payload
+// (general hardware graph, pp_hw_desc): binary-heap Dijkstra, u128.
+static void route_costs(const pp_hw_desc *hw, uint64_t bytes, int src, std::vector<u128> &dist) {
+    const int V = hw->num_devices + hw->num_routers;
+    const u128 INF = ~(u128)0;
+    dist.assign(V, INF);
+    typedef std::pair<u128, int> Item;
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
+    dist[src] = 0;
+    heap.push(Item(0, src));
+    while (!heap.empty()) {
+        Item it = heap.top();
+        heap.pop();
+        if (it.first != dist[it.second]) continue;
+        const int u = it.second;
+        for (int l = 0; l < hw->num_links; l++) {
+            int v;
+            if (hw->link_a[l] == u) v = hw->link_b[l];
+            else if (hw->link_b[l] == u) v = hw->link_a[l];
+            else continue;
+            const u128 w = ((u128)bytes * 1000000000000ull + hw->link_bw_Bps[l] - 1) / hw->link_bw_Bps[l] +
+                           hw->link_lat_ps[l];
+            if (it.first + w < dist[v]) {
+                dist[v] = it.first + w;
+                heap.push(Item(dist[v], v));
+            }
+        }
+    }
+}
+
+int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *hw, int cuda_device,
+             pp_dfg **out) {
     if (!out) return fail(PP_E_INVALID, "out is NULL");
     *out = nullptr;
-    if (!d || !link) return fail(PP_E_INVALID, "desc or link is NULL");
+    if (!d || (!link && !hw)) return fail(PP_E_INVALID, "desc or link is NULL");
+    if (hw) {
+        if (hw->num_devices < 1 || hw->num_devices > 8 || hw->num_routers < 0 || hw->num_links < 0 ||
+            (hw->num_links > 0 && (!hw->link_a || !hw->link_b || !hw->link_bw_Bps || !hw->link_lat_ps)))
+            return fail(PP_E_INVALID, "invalid hardware graph sizes");
+        const int V = hw->num_devices + hw->num_routers;
+        for (int l = 0; l < hw->num_links; l++)
+            if (hw->link_a[l] < 0 || hw->link_a[l] >= V || hw->link_b[l] < 0 || hw->link_b[l] >= V ||
+                hw->link_a[l] == hw->link_b[l] || hw->link_bw_Bps[l] == 0)
+                return fail(PP_E_INVALID, "invalid link " + std::to_string(l));
+    }
     const int K = d->num_ops, E = d->num_edges;
     if (K < 1 || E < 0 || !d->fwd_ps || !d->bwd_ps ||
         (E > 0 && (!d->edge_src || !d->edge_dst || !d->edge_fwd_bytes)))
         return fail(PP_E_INVALID, "invalid sizes or null arrays");
-    if (link->link_bw_Bps == 0) return fail(PP_E_INVALID, "link bandwidth must be > 0");
+    if (!hw && link->link_bw_Bps == 0) return fail(PP_E_INVALID, "link bandwidth must be > 0");
     if (K > 65535) return fail(PP_E_TOO_LARGE, "more than 65535 ops");
 
     std::vector<int64_t> id(K);
@@ -105,17 +147,68 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
     u128 bound = 0;
     for (int k = 0; k < K; k++) bound += (u128)d->fwd_ps[k] + d->bwd_ps[k];
     const u128 t1 = bound;
-    for (int e = 0; e < E; e++) {
-        uint64_t bf = d->edge_fwd_bytes[e];
-        uint64_t bb = d->edge_bwd_bytes ? d->edge_bwd_bytes[e] : bf;
-        u128 qf = ((u128)bf * 1000000000000ull + link->link_bw_Bps - 1) / link->link_bw_Bps + link->link_lat_ps;
-        u128 qb = ((u128)bb * 1000000000000ull + link->link_bw_Bps - 1) / link->link_bw_Bps + link->link_lat_ps;
-        bound += qf + qb;
-        if ((qf >> 64) || (qb >> 64) || (bound >> 61)) return fail(PP_E_RANGE, "time bound >= 2^61 ps");
-        cf[e] = (uint64_t)qf;
-        cb[e] = (uint64_t)qb;
+    // hardware graph: cost of every ordered device pair, classes of pairs
+    const int nd = hw ? hw->num_devices : 0;
+    std::vector<uint64_t> hcf, hcb;           // [e][a][b]
+    std::vector<int> cls(64, 0);              // class of (a, b); 0 for a == b
+    int ncls = 1;
+    if (hw) {
+        hcf.assign((size_t)E * nd * nd, 0);
+        hcb.assign((size_t)E * nd * nd, 0);
+        std::vector<u128> dist;
+        for (int a = 0; a < nd; a++) {
+            route_costs(hw, 0, a, dist);
+            for (int b = 0; b < nd; b++)
+                if (dist[b] == ~(u128)0) return fail(PP_E_INVALID, "devices not connected");
+        }
+        for (int e = 0; e < E; e++) {
+            uint64_t bf = d->edge_fwd_bytes[e];
+            uint64_t bb = d->edge_bwd_bytes ? d->edge_bwd_bytes[e] : bf;
+            u128 mf = 0, mb = 0;
+            for (int dir = 0; dir < 2; dir++)
+                for (int a = 0; a < nd; a++) {
+                    route_costs(hw, dir ? bb : bf, a, dist);
+                    for (int b = 0; b < nd; b++) {
+                        if (a == b) continue;
+                        if (dist[b] >> 64) return fail(PP_E_RANGE, "edge cost overflow");
+                        (dir ? hcb : hcf)[((size_t)e * nd + a) * nd + b] = (uint64_t)dist[b];
+                        u128 &m = dir ? mb : mf;
+                        if (dist[b] > m) m = dist[b];
+                    }
+                }
+            bound += mf + mb;
+            if (bound >> 61) return fail(PP_E_RANGE, "time bound >= 2^61 ps");
+        }
+        // pairs with equal costs on every edge and direction share a class
+        std::vector<std::vector<uint64_t>> reps;
+        for (int a = 0; a < nd; a++)
+            for (int b = 0; b < nd; b++) {
+                if (a == b) continue;
+                std::vector<uint64_t> v(2 * (size_t)E);
+                for (int e = 0; e < E; e++) {
+                    v[2 * e] = hcf[((size_t)e * nd + a) * nd + b];
+                    v[2 * e + 1] = hcb[((size_t)e * nd + a) * nd + b];
+                }
+                size_t c = 0;
+                while (c < reps.size() && reps[c] != v) c++;
+                if (c == reps.size()) reps.push_back(v);
+                cls[a * 8 + b] = (int)c + 1;
+            }
+        ncls = (int)reps.size() + 1;
+    } else {
+        for (int e = 0; e < E; e++) {
+            uint64_t bf = d->edge_fwd_bytes[e];
+            uint64_t bb = d->edge_bwd_bytes ? d->edge_bwd_bytes[e] : bf;
+            u128 qf = ((u128)bf * 1000000000000ull + link->link_bw_Bps - 1) / link->link_bw_Bps + link->link_lat_ps;
+            u128 qb = ((u128)bb * 1000000000000ull + link->link_bw_Bps - 1) / link->link_bw_Bps + link->link_lat_ps;
+            bound += qf + qb;
+            if ((qf >> 64) || (qb >> 64) || (bound >> 61)) return fail(PP_E_RANGE, "time bound >= 2^61 ps");
+            cf[e] = (uint64_t)qf;
+            cb[e] = (uint64_t)qb;
+        }
     }
     if (bound >> 61) return fail(PP_E_RANGE, "time bound >= 2^61 ps");
+    if (hw && (bound >> 49)) return fail(PP_E_RANGE, "hardware-graph mode needs every time < 2^49 ps");
 
     // adjacency by π position
     std::vector<std::vector<int>> in_e(K), out_e(K);
@@ -129,19 +222,20 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
     // finish time of p = s, or backward finish time of p = 2K8−1−s); −1 = zero.
     const int K8 = (K + 7) / 8 * 8;
     const int S = 2 * K8;
-    std::vector<std::vector<std::pair<int, uint64_t>>> inputs(S);   // (value id, cost ps)
+    // (value id, edge code): code = 2·e + [backward], −1 for a zero-cost input
+    std::vector<std::vector<std::pair<int, int64_t>>> inputs(S);
     for (int s = 0; s < S; s++) {
         const bool fwd = s < K8;
         const int p = fwd ? s : S - 1 - s;
         auto &in = inputs[s];
         if (p >= K) {
-            in.push_back({-1, 0});                       // pad
+            in.push_back({-1, -1});                      // pad
         } else if (fwd) {
-            for (int e : in_e[p]) in.push_back({pos[src[e]], cf[e]});
-            if (in.empty()) in.push_back({-1, 0});
+            for (int e : in_e[p]) in.push_back({pos[src[e]], 2 * (int64_t)e});
+            if (in.empty()) in.push_back({-1, -1});
         } else {
-            for (int e : out_e[p]) in.push_back({S - 1 - pos[dst[e]], cb[e]});
-            if (out_e[p].empty()) in.push_back({p, 0});   // sink: waits for its own forward (R1)
+            for (int e : out_e[p]) in.push_back({S - 1 - pos[dst[e]], 2 * (int64_t)e + 1});
+            if (out_e[p].empty()) in.push_back({p, -1});  // sink: waits for its own forward (R1)
         }
     }
     // register forwarding: an input produced by the previous step goes first
@@ -197,6 +291,7 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
     if (const char *a = getenv("PP_ARITH")) {
         if (!strcmp(a, "int64")) f64 = false;
     }
+    if (hw) f64 = true;   // the class-cost rows are f64-encoded
     auto enc = [&](uint64_t ps) -> uint64_t {
         if (!f64) return 8ull * ps;
         double x = (double)ps;   // exact: ps < 2^49
@@ -205,9 +300,41 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
         return bits;
     };
 
-    // ---- records: first input inlined in the op record, the rest as extras
+    // ---- records: first input inlined in the op record, the rest as extras.
+    // Uniform link: the record holds the encoded cost.  Hardware graph: it
+    // holds the byte offset of the input's cost row (one entry per class).
     std::vector<OpRec> ops(S);
     std::vector<ExtraRec> xr;
+    std::vector<uint64_t> rows;                 // hardware graph: ncls entries per distinct input
+    std::map<int64_t, uint32_t> row_of;                  // edge code -> row index (memo)
+    std::map<std::vector<uint64_t>, uint32_t> row_idx;   // row contents -> row index (dedupe)
+    auto cost_field = [&](int64_t code) -> uint64_t {
+        if (!hw) {
+            if (code < 0) return enc(0);
+            return enc((code & 1) ? cb[code >> 1] : cf[code >> 1]);
+        }
+        auto it = row_of.find(code);
+        if (it != row_of.end()) return it->second;   // patched to a byte offset below
+        std::vector<uint64_t> row(ncls, enc(0));
+        if (code >= 0) {
+            const int e = (int)(code >> 1);
+            const auto &h = (code & 1) ? hcb : hcf;
+            for (int a = 0; a < nd; a++)
+                for (int b = 0; b < nd; b++)   // any pair of a class has the same cost
+                    if (a != b) row[cls[a * 8 + b]] = enc(h[((size_t)e * nd + a) * nd + b]);
+        }
+        auto r = row_idx.find(row);
+        uint32_t idx;
+        if (r != row_idx.end()) {
+            idx = r->second;
+        } else {   // edges with equal payloads share one row
+            idx = (uint32_t)(rows.size() / ncls);
+            rows.insert(rows.end(), row.begin(), row.end());
+            row_idx.emplace(std::move(row), idx);
+        }
+        row_of.emplace(code, idx);
+        return idx;
+    };
     auto src_off = [&](int v) -> uint32_t { return v < 0 ? zero_off : (uint32_t)slot[v] * kSlotUnit; };
     for (int s = 0; s < S; s++) {
         const bool fwd = s < K8;
@@ -215,20 +342,27 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
         const auto &in = inputs[s];
         OpRec &o = ops[s];
         o.cost8 = p < K ? enc(fwd ? d->fwd_ps[pi[p]] : d->bwd_ps[pi[p]]) : enc(0);
-        o.c8 = enc(in[0].second);
+        o.c8 = cost_field(in[0].second);
         o.src_off = fwd_first[s] ? kFromPrev : src_off(in[0].first);
         o.out_off = slot[s] < 0 ? kNoStore : (uint32_t)slot[s] * kSlotUnit;
         const uint32_t n_extra = (uint32_t)in.size() - 1;
         if (n_extra > 0xFFFF) return fail(PP_E_TOO_LARGE, "op with more than 65536 inputs");
         o.ctrl = (fwd_first[s] && n_extra == 0) ? 0u : (0x10000u | n_extra);
         o.base = 0;
-        for (size_t q = 1; q < in.size(); q++) xr.push_back(ExtraRec{enc(in[q].second), src_off(in[q].first), 0});
+        for (size_t q = 1; q < in.size(); q++) xr.push_back(ExtraRec{cost_field(in[q].second), src_off(in[q].first), 0});
     }
     size_t off_extra = sizeof(OpRec) * S;
     size_t off_mem = off_extra + sizeof(ExtraRec) * xr.size();
     size_t off_orig = off_mem + 8ull * K8;
-    size_t bytes = off_orig + 4ull * K8;
+    size_t off_cls = (off_orig + 4ull * K8 + 15) & ~size_t(15);
+    size_t off_rows = off_cls + (hw ? 64 : 0);
+    size_t bytes = off_rows + 8ull * rows.size();
     bytes = (bytes + 15) & ~size_t(15);
+    if (hw) {   // row indices -> byte offsets
+        const uint64_t row_bytes = 8ull * ncls;
+        for (auto &o : ops) o.c8 = off_rows + o.c8 * row_bytes;
+        for (auto &x : xr) x.c8 = off_rows + x.c8 * row_bytes;
+    }
     if (bytes > (size_t)kMaxImageBytes) return fail(PP_E_TOO_LARGE, "DFG image exceeds 96 KB of shared memory");
 
     pp_dfg *g = new pp_dfg();
@@ -239,7 +373,10 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
     g->W = W;
     g->f64 = f64;
     g->t1 = (uint64_t)t1;
-    g->cap = link->dev_mem_cap_bytes;
+    g->cap = hw ? hw->dev_mem_cap_bytes : link->dev_mem_cap_bytes;
+    g->hw = hw != nullptr;
+    g->nd = nd;
+    g->off_cls = (uint32_t)off_cls;
     g->grad_bytes = 0;
     if (d->param_bytes)
         for (int k = 0; k < K; k++) g->grad_bytes += d->param_bytes[k];
@@ -253,6 +390,10 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, int cuda_device, pp
         memcpy(g->image.data() + off_mem + 8ull * p, &m, 8);
         uint32_t o = p < K ? (uint32_t)pi[p] : 0u;
         memcpy(g->image.data() + off_orig + 4ull * p, &o, 4);
+    }
+    if (hw) {
+        for (int i = 0; i < 64; i++) g->image[off_cls + i] = (uint8_t)cls[i];
+        memcpy(g->image.data() + off_rows, rows.data(), 8 * rows.size());
     }
     g->off_extra = (uint32_t)off_extra;
     g->off_mem = (uint32_t)off_mem;

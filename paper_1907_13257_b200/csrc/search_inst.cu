@@ -11,40 +11,48 @@
 
 namespace pp {
 
+template <int GEN, bool MEM, bool WA, bool F64, int NP, bool HW>
+static KernelInfo info2() {
+    return KernelInfo{&launch_search<PP_M, GEN, MEM, WA, F64, NP, HW>,
+                      reinterpret_cast<const void *>(&search_kernel<PP_M, GEN, MEM, WA, F64, NP, HW>)};
+}
+
+// the hardware-graph variant exists for the tagged-f64 arithmetic and M ≥ 2
 template <int GEN, bool MEM, bool WA, bool F64, int NP>
-static KernelInfo info1() {
-    return KernelInfo{&launch_search<PP_M, GEN, MEM, WA, F64, NP>,
-                      reinterpret_cast<const void *>(&search_kernel<PP_M, GEN, MEM, WA, F64, NP>)};
+static KernelInfo info1(bool hw) {
+    constexpr bool kHw = F64 && PP_M >= 2;
+    if (kHw && hw) return info2<GEN, MEM, WA, F64, NP, kHw>();
+    return info2<GEN, MEM, WA, F64, NP, false>();
 }
 
 // placements per lane: 1, 2 or 4 for the argmin (search) kernels; the
 // write-all (per-candidate output) kernels are built for NP = 2 only
 template <int GEN, bool MEM, bool WA, bool F64>
-static KernelInfo info_np(int np) {
-    if (WA) return info1<GEN, MEM, WA, F64, 2>();
-    if (np >= 4) return info1<GEN, MEM, WA, F64, 4>();
-    if (np == 2) return info1<GEN, MEM, WA, F64, 2>();
-    return info1<GEN, MEM, WA, F64, 1>();
+static KernelInfo info_np(int np, bool hw) {
+    if (WA) return info1<GEN, MEM, WA, F64, 2>(hw);
+    if (np >= 4) return info1<GEN, MEM, WA, F64, 4>(hw);
+    if (np == 2) return info1<GEN, MEM, WA, F64, 2>(hw);
+    return info1<GEN, MEM, WA, F64, 1>(hw);
 }
 
 template <int GEN, bool MEM, bool WA>
-static KernelInfo info_f(bool f64, int np) {
-    return f64 ? info_np<GEN, MEM, WA, true>(np) : info_np<GEN, MEM, WA, false>(np);
+static KernelInfo info_f(bool f64, int np, bool hw) {
+    return f64 ? info_np<GEN, MEM, WA, true>(np, hw) : info_np<GEN, MEM, WA, false>(np, hw);
 }
 
-KernelInfo PP_CAT(kernel_for_m, PP_M)(int gen, bool mem, bool wa, bool f64, int np) {
+template <int GEN>
+static KernelInfo info_gen(bool mem, bool wa, bool f64, int np, bool hw) {
+    if (mem) return wa ? info_f<GEN, true, true>(f64, np, hw) : info_f<GEN, true, false>(f64, np, hw);
+    return wa ? info_f<GEN, false, true>(f64, np, hw) : info_f<GEN, false, false>(f64, np, hw);
+}
+
+KernelInfo PP_CAT(kernel_for_m, PP_M)(int gen, bool mem, bool wa, bool f64, int np, bool hw) {
     switch (gen) {
-        case GEN_GRAY:
-            return mem ? (wa ? info_f<GEN_GRAY, true, true>(f64, np) : info_f<GEN_GRAY, true, false>(f64, np))
-                       : (wa ? info_f<GEN_GRAY, false, true>(f64, np) : info_f<GEN_GRAY, false, false>(f64, np));
-        case GEN_RANDOM:
-            return mem ? (wa ? info_f<GEN_RANDOM, true, true>(f64, np) : info_f<GEN_RANDOM, true, false>(f64, np))
-                       : (wa ? info_f<GEN_RANDOM, false, true>(f64, np) : info_f<GEN_RANDOM, false, false>(f64, np));
-        case GEN_PERTURB:
-            return mem ? (wa ? info_f<GEN_PERTURB, true, true>(f64, np) : info_f<GEN_PERTURB, true, false>(f64, np))
-                       : (wa ? info_f<GEN_PERTURB, false, true>(f64, np) : info_f<GEN_PERTURB, false, false>(f64, np));
+        case GEN_GRAY: return info_gen<GEN_GRAY>(mem, wa, f64, np, hw);
+        case GEN_RANDOM: return info_gen<GEN_RANDOM>(mem, wa, f64, np, hw);
+        case GEN_PERTURB: return info_gen<GEN_PERTURB>(mem, wa, f64, np, hw);
         default:
-            return mem ? info_f<GEN_EXPLICIT, true, true>(f64, np) : info_f<GEN_EXPLICIT, false, true>(f64, np);
+            return mem ? info_f<GEN_EXPLICIT, true, true>(f64, np, hw) : info_f<GEN_EXPLICIT, false, true>(f64, np, hw);
     }
 }
 

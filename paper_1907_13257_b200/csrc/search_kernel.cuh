@@ -477,6 +477,11 @@ __device__ __forceinline__ double clear_tag(double v) {
     return __hiloint2double(__double2hiint(v), __double2loint(v) & ~7);
 }
 __device__ __forceinline__ double ldd(uint32_t a) { return __longlong_as_double((long long)lds64(a)); }
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ void std_(uint32_t a, double v) { sts64(a, (uint64_t)__double_as_longlong(v)); }
 
 template <int M>
@@ -489,10 +494,13 @@ __device__ __forceinline__ double cut_add_f64(double v, uint32_t dev, double c, 
     return __fma_rn(c, one_if(cut_bit<M>((uint32_t)__double2loint(v), dev), khi), v);
 }
 
-template <int M, int NP, bool MEM, class Gen>
+// Hardware graph (HW): a record's cost field is the image offset of its cost
+// row; the transfer a → b costs row[cls[a][b]], class 0 (a = b) costing 0, so
+// an input is simply v + row[cls[tag(v)][dev]] (no cut flag needed).
+template <int M, int NP, bool MEM, bool HW, class Gen>
 __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint32_t ops, uint32_t xr,
                                              const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
-                                             uint32_t K8, uint64_t cap, uint32_t khi) {
+                                             uint32_t K8, uint64_t cap, uint32_t khi, uint32_t cls) {
     constexpr double kBig = 1125899906842624.0;   // 2^50
     constexpr bool SM = M > 2;                    // free[] in shared memory
     double prev[NP], oth[NP];
@@ -510,6 +518,9 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
         }
     }
     auto fslot = [&](int k, uint32_t d) { return lane + free_off * NP + d * NP * 256 + k * 256; };
+    auto hwc = [&](uint32_t row, uint32_t a, uint32_t b) {   // cost of a transfer a → b
+        return ldd(ops + row + 8 * lds8(cls + Dev<M>::canon(a) * 8 + Dev<M>::canon(b)));
+    };
     uint32_t x = xr;
 
     auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
@@ -526,7 +537,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
             for (int k = 0; k < NP; k++) {
                 const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
                 const double same = __dadd_rn(1.0, -cut);
-                const double t = __fma_rn(c0, cut, prev[k]);
+                const double t = HW ? __dadd_rn(prev[k], hwc(a.z, pdev[k], dev[k])) : __fma_rn(c0, cut, prev[k]);
                 double s;
                 if (SM) {
                     s = dmax(t, __fma_rn(same, -kBig, ldd(fslot(k, dev[k]))));
@@ -542,10 +553,16 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
             double r[NP];
             if (b.x == kFromPrev) {
 #pragma unroll
-                for (int k = 0; k < NP; k++) r[k] = __fma_rn(c0, one_if(cut_bit<M>(pdev[k], dev[k]), khi), prev[k]);
+                for (int k = 0; k < NP; k++)
+                    r[k] = HW ? __dadd_rn(prev[k], hwc(a.z, pdev[k], dev[k]))
+                              : __fma_rn(c0, one_if(cut_bit<M>(pdev[k], dev[k]), khi), prev[k]);
             } else {
 #pragma unroll
-                for (int k = 0; k < NP; k++) r[k] = cut_add_f64<M>(ldd(lane + b.x * NP + k * 256), dev[k], c0, khi);
+                for (int k = 0; k < NP; k++) {
+                    const double v = ldd(lane + b.x * NP + k * 256);
+                    r[k] = HW ? __dadd_rn(v, hwc(a.z, (uint32_t)__double2loint(v) & 7u, dev[k]))
+                              : cut_add_f64<M>(v, dev[k], c0, khi);
+                }
             }
             const uint32_t nx = b.z & 0xFFFFu;
 #pragma unroll 1
@@ -554,7 +571,11 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
                 x += sizeof(ExtraRec);
                 const double ce = __hiloint2double((int)e.y, (int)e.x);
 #pragma unroll
-                for (int k = 0; k < NP; k++) r[k] = dmax(r[k], cut_add_f64<M>(ldd(lane + e.z * NP + k * 256), dev[k], ce, khi));
+                for (int k = 0; k < NP; k++) {
+                    const double v = ldd(lane + e.z * NP + k * 256);
+                    r[k] = dmax(r[k], HW ? __dadd_rn(v, hwc(e.x, (uint32_t)__double2loint(v) & 7u, dev[k]))
+                                         : cut_add_f64<M>(v, dev[k], ce, khi));
+                }
             }
 #pragma unroll
             for (int k = 0; k < NP; k++) {
@@ -619,11 +640,11 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
     }
 }
 
-template <int M, int NP, bool MEM, bool F64, class Gen>
+template <int M, int NP, bool MEM, bool F64, bool HW, class Gen>
 __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[NP], uint32_t ops, uint32_t xr,
                                             const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
-                                            uint32_t K8, uint64_t cap, uint32_t khi) {
-    if constexpr (F64 && M >= 2) schedule_f64<M, NP, MEM>(gen, mk, ops, xr, mem, lane, free_off, K8, cap, khi);
+                                            uint32_t K8, uint64_t cap, uint32_t khi, uint32_t cls) {
+    if constexpr (F64 && M >= 2) schedule_f64<M, NP, MEM, HW>(gen, mk, ops, xr, mem, lane, free_off, K8, cap, khi, cls);
     else schedule_gen<M, NP, MEM, F64>(gen, mk, ops, xr, mem, lane, free_off, K8, cap);
 }
 
@@ -632,7 +653,7 @@ __device__ __forceinline__ bool lex_less(uint64_t m1, uint64_t i1, uint64_t m2, 
 }
 
 // ------------------------------------------------------------------ kernel
-template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64, int NP>
+template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64, int NP, bool HW>
 __global__ void __launch_bounds__(256, PP_MIN_CTAS) search_kernel(const KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t mbar;
@@ -703,21 +724,25 @@ __global__ void __launch_bounds__(256, PP_MIN_CTAS) search_kernel(const KParams 
         if (GEN == GEN_GRAY) {
             GrayGen<M, NP> g;
             g.init(idx, P.K);
-            schedule_np<M, NP, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
+            schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
+                                              smem_base + P.off_cls);
         } else if (GEN == GEN_RANDOM) {
             RandomGen<M, NP> g;
             g.init(idx, P.seed, P.K);
-            schedule_np<M, NP, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
+            schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
+                                              smem_base + P.off_cls);
         } else if (GEN == GEN_PERTURB) {
             PerturbGen<M, NP> g;
             g.init(idx, P.seed, P.K, P.tau);
-            schedule_np<M, NP, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
+            schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
+                                              smem_base + P.off_cls);
         } else {
             ExplicitGen<NP> g;
 #pragma unroll
             for (int k = 0; k < NP; k++) g.row[k] = P.g_place + (idx[k] - P.begin) * (uint64_t)P.K;
             g.orig = orig;
-            schedule_np<M, NP, MEM, F64>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi);
+            schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
+                                              smem_base + P.off_cls);
         }
 #pragma unroll
         for (int k = 0; k < NP; k++) {
@@ -844,9 +869,9 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
     }
 }
 
-template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64, int NP>
+template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64, int NP, bool HW>
 int launch_search(const KParams &p, int grid, int threads, int smem, void *stream) {
-    search_kernel<M, GEN, MEM, WRITE_ALL, F64, NP><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
+    search_kernel<M, GEN, MEM, WRITE_ALL, F64, NP, HW><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
     return (int)cudaGetLastError();
 }
 

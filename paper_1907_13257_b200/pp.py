@@ -44,6 +44,12 @@ class LinkDesc(C.Structure):
     _fields_ = [("link_bw_Bps", C.c_uint64), ("link_lat_ps", C.c_uint64), ("dev_mem_cap_bytes", C.c_uint64)]
 
 
+class HwDesc(C.Structure):
+    _fields_ = [("num_devices", C.c_int32), ("num_routers", C.c_int32), ("num_links", C.c_int32),
+                ("link_a", P(C.c_int32)), ("link_b", P(C.c_int32)), ("link_bw_Bps", P(C.c_uint64)),
+                ("link_lat_ps", P(C.c_uint64)), ("dev_mem_cap_bytes", C.c_uint64)]
+
+
 class DfgInfo(C.Structure):
     _fields_ = [("num_ops", C.c_int32), ("num_edges", C.c_int32), ("num_slots", C.c_int32),
                 ("image_bytes", C.c_int32), ("t1_ps", C.c_uint64), ("grad_bytes", C.c_uint64)]
@@ -84,6 +90,7 @@ class CrossoverC(C.Structure):
 # against include/pp.h
 SIGNATURES = {
     "pp_load_dfg": ([P(DfgDesc), P(LinkDesc), C.c_int, P(C.c_void_p)], C.c_int),
+    "pp_load_dfg_hw": ([P(DfgDesc), P(HwDesc), C.c_int, P(C.c_void_p)], C.c_int),
     "pp_free_dfg": ([C.c_void_p], None),
     "pp_dfg_get_info": ([C.c_void_p, P(DfgInfo)], C.c_int),
     "pp_dfg_get_pi": ([C.c_void_p, P(C.c_int32)], C.c_int),
@@ -199,9 +206,19 @@ class Dfg:
                        _ptr(a["bwd"], C.c_uint64), _ptr(a["mem"], C.c_uint64), _ptr(a["par"], C.c_uint64),
                        _ptr(a["src"], C.c_int32), _ptr(a["dst"], C.c_int32), _ptr(a["bf"], C.c_uint64),
                        _ptr(a["bb"], C.c_uint64))
-        link = LinkDesc(int(spec["link_bw_Bps"]), int(spec["link_lat_ps"]), int(spec.get("dev_mem_cap_bytes") or 0))
         h = C.c_void_p()
-        _check(lib().pp_load_dfg(C.byref(desc), C.byref(link), device, C.byref(h)))
+        hw = spec.get("hw")
+        if hw is None:
+            link = LinkDesc(int(spec["link_bw_Bps"]), int(spec["link_lat_ps"]), int(spec.get("dev_mem_cap_bytes") or 0))
+            _check(lib().pp_load_dfg(C.byref(desc), C.byref(link), device, C.byref(h)))
+        else:   # general hardware graph
+            a.update(la=np.ascontiguousarray(np.asarray(hw["link_a"], dtype=np.int32)),
+                     lb=np.ascontiguousarray(np.asarray(hw["link_b"], dtype=np.int32)),
+                     hbw=_u64(hw["link_bw_Bps"]), hlat=_u64(hw["link_lat_ps"]))
+            hd = HwDesc(int(hw["num_devices"]), int(hw.get("num_routers", 0)), len(a["la"]),
+                        _ptr(a["la"], C.c_int32), _ptr(a["lb"], C.c_int32), _ptr(a["hbw"], C.c_uint64),
+                        _ptr(a["hlat"], C.c_uint64), int(hw.get("dev_mem_cap_bytes", 0)))
+            _check(lib().pp_load_dfg_hw(C.byref(desc), C.byref(hd), device, C.byref(h)))
         self._h = h
         self.device = device
         info = DfgInfo()

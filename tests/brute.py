@@ -51,20 +51,57 @@ def _cost(nbytes, bw, lat):
     return -(-nbytes * 10**12 // bw) + lat
 
 
+def route_delays(hw, nbytes):
+    """All-pairs delay of the cheapest route for a payload of `nbytes` on the
+    hardware graph (PAPER.md:352 nodes N ∪ R and links L; Δ_e of PAPER.md:455–462
+    summed over the route's links), by Floyd–Warshall over device and router
+    nodes — a different algorithm from the oracle's Dijkstra.  Returns
+    d[a][b] for devices a, b (None if unreachable)."""
+    V = hw["num_devices"] + hw.get("num_routers", 0)
+    INF = None
+    d = [[0 if i == j else INF for j in range(V)] for i in range(V)]
+    for a, b, bw, lat in zip(hw["link_a"], hw["link_b"], hw["link_bw_Bps"], hw["link_lat_ps"]):
+        c = _cost(nbytes, bw, lat)
+        for x, y in ((a, b), (b, a)):
+            if d[x][y] is None or c < d[x][y]:
+                d[x][y] = c
+    for k in range(V):
+        for i in range(V):
+            if d[i][k] is None:
+                continue
+            for j in range(V):
+                if d[k][j] is not None and (d[i][j] is None or d[i][k] + d[k][j] < d[i][j]):
+                    d[i][j] = d[i][k] + d[k][j]
+    nd = hw["num_devices"]
+    return [row[:nd] for row in d[:nd]]
+
+
 def longest_path_makespan(spec, M, placement):
     K = len(spec["fwd_ps"])
     ids = spec.get("op_id") or list(range(K))
     src, dst = spec["edge_src"], spec["edge_dst"]
     bf = spec["edge_fwd_bytes"]
     bb = spec.get("edge_bwd_bytes") or bf
-    bw, lat = spec["link_bw_Bps"], spec["link_lat_ps"]
+    hw = spec.get("hw")
+    if hw is None:
+        bw, lat = spec["link_bw_Bps"], spec["link_lat_ps"]
+
+        def cost(nbytes, a, b):
+            return _cost(nbytes, bw, lat) if a != b else 0
+    else:
+        memo = {}
+
+        def cost(nbytes, a, b):
+            if nbytes not in memo:
+                memo[nbytes] = route_delays(hw, nbytes)
+            return memo[nbytes][a][b]
     order = kahn_by_id(K, ids, src, dst)
     seq = [("F", k) for k in order] + [("B", k) for k in reversed(order)]
     preds = {n: [] for n in seq}
     for e, (u, v) in enumerate(zip(src, dst)):
-        cut = placement[u] != placement[v]
-        preds[("F", v)].append((("F", u), _cost(bf[e], bw, lat) if cut else 0))
-        preds[("B", u)].append((("B", v), _cost(bb[e], bw, lat) if cut else 0))
+        a, b = placement[u], placement[v]
+        preds[("F", v)].append((("F", u), cost(bf[e], a, b)))
+        preds[("B", u)].append((("B", v), cost(bb[e], b, a)))
     for k in range(K):
         preds[("B", k)].append((("F", k), 0))
     last = {}
@@ -85,7 +122,7 @@ def longest_path_makespan(spec, M, placement):
         return s + w[n]
 
     mk = max(finish(n) for n in seq)
-    cap = spec.get("dev_mem_cap_bytes") or 0
+    cap = (hw or spec).get("dev_mem_cap_bytes") or 0
     if cap:
         mem = spec.get("mem_bytes") or [0] * K
         for m in range(M):
