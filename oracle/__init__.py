@@ -112,6 +112,12 @@ def lib():
         L.or_schedule_ex.argtypes = [C.c_void_p, C.c_int, P(C.c_uint8), P(C.c_uint64), P(C.c_uint64)]
         L.or_schedule_ex.restype = C.c_uint64
         L.or_makespan_orig.argtypes = [C.c_void_p, C.c_int, P(C.c_uint8), P(C.c_uint64)]
+        L.or_exact.argtypes = [C.c_void_p, C.c_int, P(C.c_uint8)]
+        L.or_exact.restype = C.c_uint64
+        L.or_makespan_exact_orig.argtypes = [C.c_void_p, C.c_int, P(C.c_uint8), P(C.c_uint64)]
+        L.or_round_exact.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32, P(C.c_uint8),
+                                     C.c_uint64, C.c_uint64]
+        L.or_round_exact.restype = _Best
         L.or_mix.argtypes = [C.c_uint64]; L.or_mix.restype = C.c_uint64
         L.or_gen.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint32, P(C.c_uint8),
                              C.c_uint64, P(C.c_uint8)]
@@ -232,6 +238,26 @@ class Dfg:
         if rc:
             raise OracleError(rc)
         return int(out.value)
+
+    def makespan_exact(self, M: int, placement) -> int:
+        """NEXT f1: the makespan-optimal schedule of a placement in descriptor order."""
+        d = np.ascontiguousarray(np.asarray(placement, dtype=np.uint8))
+        out = C.c_uint64()
+        rc = lib().or_makespan_exact_orig(self._h, M, d.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(out))
+        if rc:
+            raise OracleError(rc)
+        return int(out.value)
+
+    def exact_pi(self, M: int, d_pi) -> int:
+        d = np.ascontiguousarray(np.asarray(d_pi, dtype=np.uint8))
+        return int(lib().or_exact(self._h, M, d.ctypes.data_as(C.POINTER(C.c_uint8))))
+
+    def round_exact(self, M, gen, seed_r, tau, base_pi, begin, end):
+        base = np.ascontiguousarray(np.asarray(base_pi if base_pi is not None else np.zeros(self.K),
+                                               dtype=np.uint8))
+        r = lib().or_round_exact(self._h, M, gen, seed_r, tau, base.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                 begin, end)
+        return int(r.makespan), int(r.index)
 
     def makespan_pi(self, M: int, d_pi) -> int:
         d = np.ascontiguousarray(np.asarray(d_pi, dtype=np.uint8))

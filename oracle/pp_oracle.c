@@ -27,6 +27,11 @@
  *   or_ar                      pinned (K9 closed form)
  *   or_epochs / or_cell        pinned (K10–K12 paper ratios)
  *   or_crossover               pinned (K10–K14 paper statements)
+ *   or_prepare_hw              pinned (SPEC route examples, closed forms on
+ *                              ring/switch/two-node graphs, Floyd–Warshall)
+ *   or_exact / or_round_exact  pinned (SPEC exact_schedule examples, a hand
+ *                              case where in-order issue loses, brute force
+ *                              over per-device orders, exact ≤ in-order)
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -414,6 +419,125 @@ int or_makespan_orig(const or_ctx *c, int M, const uint8_t *d_orig, uint64_t *ou
     return OR_OK;
 }
 
+/* ------------------------------------------- NEXT f1: the exact schedule */
+/* The makespan-optimal schedule of a FIXED placement: DLPlacer "minimizes
+ * per step training time by ... determining the execution start time of each
+ * vertex on a device" (§6) subject to the dependency constraint
+ * (PAPER.md:443–453), the non-overlap constraint and the
+ * back-to-back assumption; SPEC.md:161–169 exact_schedule.
+ *
+ * Nodes: F_p (forward of π position p) and B_p (its backward), on device d[p].
+ * Arcs (R1): F_u → F_v with c_f(e) when cut, B_v → B_u with c_b(e) when cut,
+ * F_p → B_p.  Reading R22: a schedule is a linear extension σ of the arcs;
+ * each node starts at max(data ready, finish of the node before it on its
+ * device in σ).  Every feasible schedule's per-device orders are induced by
+ * some σ, whose schedule is no later, so the optimum is
+ *     exact = min over all linear extensions σ of makespan(σ).
+ * Enumerated by depth-first search over σ.  A branch stops when its partial
+ * makespan (max finish so far) is already ≥ the best complete σ: extending σ
+ * never lowers a finish time already fixed.  Exponential: small DFGs only.   */
+typedef struct {
+    const or_ctx *c;
+    const uint8_t *d;
+    int K;
+    uint64_t *fin;        /* [2K] finish time of each scheduled node            */
+    uint8_t *done;        /* [2K]                                              */
+    uint64_t free_t[8];
+    uint64_t best;
+} or_ex;
+
+/* data-ready time of node n if all its predecessors are done; 0 with *ok=0 otherwise */
+static uint64_t ex_ready(const or_ex *x, int n, int *ok) {
+    const or_ctx *c = x->c;
+    const uint8_t *d = x->d;
+    int K = x->K;
+    uint64_t r = 0;
+    *ok = 1;
+    if (n < K) {                                   /* F_p: forward in-edges */
+        int p = n;
+        for (int i = 0; i < c->in_cnt[p]; i++) {
+            int u = c->in_src[p][i];
+            if (!x->done[u]) { *ok = 0; return 0; }
+            uint64_t cost = c->nd ? c->cfm[((size_t)c->in_eid[p][i] * c->nd + d[u]) * c->nd + d[p]] : c->in_cf[p][i];
+            uint64_t t = x->fin[u] + (d[u] != d[p] ? cost : 0);
+            if (t > r) r = t;
+        }
+    } else {                                       /* B_p: own forward + gradients */
+        int p = n - K;
+        if (!x->done[p]) { *ok = 0; return 0; }
+        r = x->fin[p];
+        for (int i = 0; i < c->out_cnt[p]; i++) {
+            int w = c->out_dst[p][i];
+            if (!x->done[K + w]) { *ok = 0; return 0; }
+            uint64_t cost = c->nd ? c->cbm[((size_t)c->out_eid[p][i] * c->nd + d[w]) * c->nd + d[p]] : c->out_cb[p][i];
+            uint64_t t = x->fin[K + w] + (d[w] != d[p] ? cost : 0);
+            if (t > r) r = t;
+        }
+    }
+    return r;
+}
+
+static void ex_dfs(or_ex *x, int placed, uint64_t partial) {
+    int K = x->K;
+    if (placed == 2 * K) {
+        if (partial < x->best) x->best = partial;
+        return;
+    }
+    for (int n = 0; n < 2 * K; n++) {
+        if (x->done[n]) continue;
+        int ok;
+        uint64_t r = ex_ready(x, n, &ok);
+        if (!ok) continue;
+        int p = n < K ? n : n - K;
+        int dev = x->d[p];
+        uint64_t s = r > x->free_t[dev] ? r : x->free_t[dev];
+        uint64_t f = s + (n < K ? x->c->df[p] : x->c->db[p]);
+        uint64_t np = f > partial ? f : partial;
+        if (np >= x->best) continue;               /* cannot beat the best σ */
+        uint64_t saved = x->free_t[dev];
+        x->fin[n] = f;
+        x->done[n] = 1;
+        x->free_t[dev] = f;
+        ex_dfs(x, placed + 1, np);
+        x->free_t[dev] = saved;
+        x->done[n] = 0;
+    }
+}
+
+/* exact makespan of placement d (by π position); OR_INFEASIBLE_MAKESPAN when
+ * the memory cap is violated (R7)                          */
+uint64_t or_exact(const or_ctx *c, int M, const uint8_t *d) {
+    int K = c->K;
+    if (c->cap > 0) {
+        for (int m = 0; m < M; m++) {
+            u128 used = 0;
+            for (int p = 0; p < K; p++) if (d[p] == m) used += c->mem[p];
+            if (used > c->cap) return OR_INFEASIBLE_MAKESPAN;
+        }
+    }
+    or_ex x;
+    memset(&x, 0, sizeof x);
+    x.c = c; x.d = d; x.K = K;
+    x.fin = calloc((size_t)(2 * K) + 1, 8);
+    x.done = calloc((size_t)(2 * K) + 1, 1);
+    x.best = UINT64_MAX;
+    ex_dfs(&x, 0, 0);
+    free(x.fin); free(x.done);
+    return x.best;
+}
+
+int or_makespan_exact_orig(const or_ctx *c, int M, const uint8_t *d_orig, uint64_t *out) {
+    if (M < 1 || M > 8 || (c->nd && M > c->nd)) return OR_E_INVALID;
+    uint8_t *d = malloc((size_t)c->K + 1);
+    for (int p = 0; p < c->K; p++) {
+        d[p] = d_orig[c->pi[p]];
+        if (d[p] >= M) { free(d); return OR_E_INVALID; }
+    }
+    *out = or_exact(c, M, d);
+    free(d);
+    return OR_OK;
+}
+
 /* ------------------------------------------------------- O5 / O6 generators */
 #define OR_GEN_GRAY 0
 #define OR_GEN_RANDOM 1
@@ -499,6 +623,23 @@ or_best or_round(const or_ctx *c, int M, int gen, uint64_t seed_r, uint32_t tau,
     for (uint64_t i = begin; i < end; i++) {
         or_gen(c->K, M, gen, seed_r, tau, base, i, d);
         uint64_t mk = or_schedule(c, M, d);
+        if (mk < best.makespan || (mk == best.makespan && i < best.index)) {
+            best.makespan = mk; best.index = i;
+        }
+    }
+    free(d);
+    return best;
+}
+
+/* argmin over candidates [begin, end) of the EXACT makespan (NEXT f1),
+ * lexicographic (makespan, index) as in O7                                   */
+or_best or_round_exact(const or_ctx *c, int M, int gen, uint64_t seed_r, uint32_t tau,
+                       const uint8_t *base, uint64_t begin, uint64_t end) {
+    or_best best = { UINT64_MAX, UINT64_MAX };
+    uint8_t *d = malloc((size_t)c->K + 1);
+    for (uint64_t i = begin; i < end; i++) {
+        or_gen(c->K, M, gen, seed_r, tau, base, i, d);
+        uint64_t mk = or_exact(c, M, d);
         if (mk < best.makespan || (mk == best.makespan && i < best.index)) {
             best.makespan = mk; best.index = i;
         }

@@ -131,6 +131,70 @@ def longest_path_makespan(spec, M, placement):
     return mk
 
 
+def exact_makespan(spec, M, placement):
+    """Makespan-optimal schedule of a fixed placement (NEXT f1), by the
+    disjunctive-graph formulation: choose an order of the nodes on every
+    device (all permutations, per device), add the consecutive-order arcs to
+    the precedence arcs of the augmented DAG; if the result is acyclic its
+    longest path is that choice's makespan.  Minimum over every choice.  A
+    different formulation from the oracle's enumeration of linear extensions."""
+    K = len(spec["fwd_ps"])
+    src, dst = spec["edge_src"], spec["edge_dst"]
+    bf = spec["edge_fwd_bytes"]
+    bb = spec.get("edge_bwd_bytes") or bf
+    hw = spec.get("hw")
+    cap = (hw or spec).get("dev_mem_cap_bytes") or 0
+    if cap:
+        mem = spec.get("mem_bytes") or [0] * K
+        for m in range(M):
+            if sum(mem[k] for k in range(K) if placement[k] == m) > cap:
+                return (1 << 64) - 1
+    if hw is None:
+        bw, lat = spec["link_bw_Bps"], spec["link_lat_ps"]
+
+        def cost(nbytes, a, b):
+            return _cost(nbytes, bw, lat) if a != b else 0
+    else:
+        def cost(nbytes, a, b):
+            return route_delays(hw, nbytes)[a][b]
+    nodes = [("F", k) for k in range(K)] + [("B", k) for k in range(K)]
+    w = {("F", k): spec["fwd_ps"][k] for k in range(K)}
+    w.update({("B", k): spec["bwd_ps"][k] for k in range(K)})
+    arcs = []
+    for e, (u, v) in enumerate(zip(src, dst)):
+        a, b = placement[u], placement[v]
+        arcs.append((("F", u), ("F", v), cost(bf[e], a, b)))
+        arcs.append((("B", v), ("B", u), cost(bb[e], b, a)))
+    arcs += [(("F", k), ("B", k), 0) for k in range(K)]
+    per_dev = [[n for n in nodes if placement[n[1]] == m] for m in range(M)]
+    best = None
+    for orders in itertools.product(*[itertools.permutations(g) for g in per_dev]):
+        extra = [(o[i], o[i + 1], 0) for o in orders for i in range(len(o) - 1)]
+        preds = {n: [] for n in nodes}
+        for a, b, c in arcs + extra:
+            preds[b].append((a, c))
+        fin, state, ok = {}, {}, [True]
+
+        def visit(n):
+            if state.get(n) == 2:
+                return fin[n]
+            if state.get(n) == 1:
+                ok[0] = False
+                return 0
+            state[n] = 1
+            s = 0
+            for p, c in preds[n]:
+                s = max(s, visit(p) + c)
+            state[n] = 2
+            fin[n] = s + w[n]
+            return fin[n]
+
+        mk = max(visit(n) for n in nodes)
+        if ok[0] and (best is None or mk < best):
+            best = mk
+    return best
+
+
 def reflected_gray(M, K):
     """Textbook recursive reflected M-ary Gray list; tuple index j = digit j
     (digit 0 changes fastest)."""
