@@ -183,6 +183,36 @@ int pp_search_range(const pp_dfg *dfg, int M, int gen, uint64_t seed_r, uint32_t
                     const uint8_t *d_base_pi, uint64_t begin, uint64_t end, uint64_t *d_best,
                     void *cuda_stream);
 
+/* ------------------------------------------- exact schedule (§8(f) f1) --
+ * The makespan-OPTIMAL schedule of each placement instead of the in-order
+ * list schedule: DLPlacer "minimizes per step training time by ...
+ * determining the execution start time of each vertex on a device"
+ * (§6) under the dependency and non-overlap
+ * constraints; SPEC.md:161–169 exact_schedule.  Per-device
+ * execution order is free (reading R22); the result is ≤ the
+ * in-order makespan of the same placement.  Branch and bound on the GPU, one
+ * warp per placement; exponential in the worst case, so it needs
+ * 2K ≤ 64 nodes (K ≤ 32 ops) else PP_E_TOO_LARGE.
+ *   node_limit   branch-and-bound nodes per placement before giving up
+ *                (0 ⇒ 2^24).  A placement that hits it gets the best
+ *                makespan found so far (an upper bound) and d_exact[i] = 0.
+ *   d_exact      device ptr uint8 [count], optional (NULL): 1 = optimal.
+ * Placements and generators as in pp_eval_placements / pp_eval_generated;
+ * memory-infeasible placements give PP_INFEASIBLE_MAKESPAN.  Asynchronous.  */
+int pp_eval_exact(const pp_dfg *dfg, int M, const uint8_t *d_placements, uint64_t count,
+                  uint64_t node_limit, uint64_t *d_makespan, uint8_t *d_exact, void *cuda_stream);
+int pp_eval_exact_generated(const pp_dfg *dfg, int M, int gen, uint64_t seed_r, uint32_t flip_thresh,
+                            const uint8_t *d_base_pi, uint64_t begin, uint64_t count, uint64_t node_limit,
+                            uint64_t *d_makespan, uint8_t *d_exact, void *cuda_stream);
+/* Lexicographically smallest (exact makespan, index) over candidates
+ * [begin, end) of one round.  Placements whose bound already exceeds the
+ * best makespan found so far are abandoned early (they cannot win).
+ * d_best: device ptr uint64[3] = {makespan, index, number of placements that
+ * hit node_limit (0 ⇒ the result is exact)}.  Asynchronous.                 */
+int pp_search_exact(const pp_dfg *dfg, int M, int gen, uint64_t seed_r, uint32_t flip_thresh,
+                    const uint8_t *d_base_pi, uint64_t begin, uint64_t end, uint64_t node_limit,
+                    uint64_t *d_best, void *cuda_stream);
+
 /* Full search: per round the candidates are sharded over
  * the ranks of `comm` (contiguous slices, see pp_rank_slice), each GPU takes
  * its slice's argmin, one NCCL min all-reduce of the packed key

@@ -433,9 +433,12 @@ int or_makespan_orig(const or_ctx *c, int M, const uint8_t *d_orig, uint64_t *ou
  * device in σ).  Every feasible schedule's per-device orders are induced by
  * some σ, whose schedule is no later, so the optimum is
  *     exact = min over all linear extensions σ of makespan(σ).
- * Enumerated by depth-first search over σ.  A branch stops when its partial
- * makespan (max finish so far) is already ≥ the best complete σ: extending σ
- * never lowers a finish time already fixed.  Exponential: small DFGs only.   */
+ * Enumerated by depth-first search over σ.  A branch stops when it cannot
+ * beat the best complete σ: (a) its partial makespan (max finish so far) is
+ * already ≥ best — extending σ never lowers a finish time already fixed; or
+ * (b) some device's free time plus the work still to run on it is ≥ best —
+ * every remaining node of that device starts after its free time and they
+ * run one at a time.  Exponential: small DFGs only.      */
 typedef struct {
     const or_ctx *c;
     const uint8_t *d;
@@ -443,6 +446,8 @@ typedef struct {
     uint64_t *fin;        /* [2K] finish time of each scheduled node            */
     uint8_t *done;        /* [2K]                                              */
     uint64_t free_t[8];
+    uint64_t left[8];     /* work not yet scheduled, per device */
+    int M;
     uint64_t best;
 } or_ex;
 
@@ -493,12 +498,18 @@ static void ex_dfs(or_ex *x, int placed, uint64_t partial) {
         uint64_t s = r > x->free_t[dev] ? r : x->free_t[dev];
         uint64_t f = s + (n < K ? x->c->df[p] : x->c->db[p]);
         uint64_t np = f > partial ? f : partial;
-        if (np >= x->best) continue;               /* cannot beat the best σ */
+        if (np >= x->best) continue;               /* (a) */
+        uint64_t dur = n < K ? x->c->df[p] : x->c->db[p];
         uint64_t saved = x->free_t[dev];
         x->fin[n] = f;
         x->done[n] = 1;
         x->free_t[dev] = f;
-        ex_dfs(x, placed + 1, np);
+        x->left[dev] -= dur;
+        int hopeless = 0;                          /* (b) */
+        for (int m = 0; m < x->M; m++)
+            if (x->free_t[m] + x->left[m] >= x->best) hopeless = 1;
+        if (!hopeless) ex_dfs(x, placed + 1, np);
+        x->left[dev] += dur;
         x->free_t[dev] = saved;
         x->done[n] = 0;
     }
@@ -517,7 +528,8 @@ uint64_t or_exact(const or_ctx *c, int M, const uint8_t *d) {
     }
     or_ex x;
     memset(&x, 0, sizeof x);
-    x.c = c; x.d = d; x.K = K;
+    x.c = c; x.d = d; x.K = K; x.M = M;
+    for (int p = 0; p < K; p++) x.left[d[p]] += c->df[p] + c->db[p];
     x.fin = calloc((size_t)(2 * K) + 1, 8);
     x.done = calloc((size_t)(2 * K) + 1, 1);
     x.best = UINT64_MAX;

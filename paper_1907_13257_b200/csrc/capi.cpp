@@ -29,7 +29,8 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
 
 #define PP_DECL_M(m)                                                                   \
     KernelInfo kernel_for_m##m(int gen, bool mem, bool wa, bool f64, int np, bool hw); \
-    UpdateFn update_for_m##m(int gen);
+    UpdateFn update_for_m##m(int gen);                                                 \
+    XKernelInfo exact_for_m##m(int gen);
 PP_DECL_M(1) PP_DECL_M(2) PP_DECL_M(3) PP_DECL_M(4) PP_DECL_M(5) PP_DECL_M(6) PP_DECL_M(7) PP_DECL_M(8)
 
 KernelInfo kernel_for(int M, int gen, bool mem, bool wa, bool f64, int np, bool hw) {
@@ -54,6 +55,19 @@ UpdateFn update_for(int M, int gen) {
         case 6: return update_for_m6(gen);
         case 7: return update_for_m7(gen);
         default: return update_for_m8(gen);
+    }
+}
+
+XKernelInfo exact_kernel_for(int M, int gen) {
+    switch (M) {
+        case 1: return exact_for_m1(gen);
+        case 2: return exact_for_m2(gen);
+        case 3: return exact_for_m3(gen);
+        case 4: return exact_for_m4(gen);
+        case 5: return exact_for_m5(gen);
+        case 6: return exact_for_m6(gen);
+        case 7: return exact_for_m7(gen);
+        default: return exact_for_m8(gen);
     }
 }
 
@@ -358,6 +372,106 @@ int pp_search_range(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
     L.p.tau = tau;
     L.p.g_out = d_best;
     return run(L, stream);
+}
+
+// ------------------------------------------------ exact schedule (NEXT f1)
+static constexpr uint64_t kDefaultNodeLimit = 1ull << 24;
+
+static int run_exact(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t tau, const uint8_t *d_base_pi,
+                     const uint8_t *d_place, uint64_t begin, uint64_t end, uint64_t node_limit,
+                     uint64_t *d_makespan, uint8_t *d_exact, uint64_t *d_best, void *stream) {
+    if (!g->x_bytes) {
+        set_error("exact schedule needs 2K <= 64 nodes (K <= 32) and an image that fits");
+        return PP_E_TOO_LARGE;
+    }
+    DeviceGuard dg(g->device);
+    if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
+    const XKernelInfo k = exact_kernel_for(M, gen);
+    const int threads = 256;
+    const int ws_off = (int)((g->x_bytes + 15) & ~15u);
+    const int smem = ws_off + (threads / 32) * (int)sizeof(XWarp);
+    cudaError_t ce;
+    if ((ce = cudaFuncSetAttribute(k.func, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess)
+        return cuda_err(ce, "exact kernel attribute");
+    int per_sm = 0;
+    if ((ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.func, threads, smem)) != cudaSuccess)
+        return cuda_err(ce, "exact kernel occupancy");
+    if (per_sm < 1) { set_error("exact kernel does not fit on an SM"); return PP_E_TOO_LARGE; }
+    const uint64_t warps_needed = end - begin;
+    uint64_t grid = (uint64_t)per_sm * (uint64_t)g->sm_count;
+    const uint64_t by_work = (warps_needed + threads / 32 - 1) / (threads / 32);
+    if (by_work < grid) grid = by_work;
+    if (grid > (uint64_t)kMaxGrid) grid = kMaxGrid;
+    if (grid < 1) grid = 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((ce = cudaMemsetAsync(g->d_xwork, 0, 4 * sizeof(unsigned long long), st)) != cudaSuccess ||
+        (ce = cudaMemsetAsync(g->d_xwork + 1, 0xFF, sizeof(unsigned long long), st)) != cudaSuccess)
+        return cuda_err(ce, "exact work counters");
+    XParams p{};
+    p.g_ximage = g->d_ximage;
+    p.g_place = d_place;
+    p.g_base = d_base_pi;
+    p.g_makespan = d_makespan;
+    p.g_exact = d_exact;
+    p.g_partials = g->d_partials;
+    p.g_ticket = g->d_ticket;
+    p.g_out = d_best;
+    p.g_work = g->d_xwork;
+    p.begin = begin;
+    p.end = end;
+    p.seed = seed_r;
+    p.cap = g->cap;
+    p.node_limit = node_limit ? node_limit : kDefaultNodeLimit;
+    p.x_bytes = g->x_bytes;
+    p.N = g->xN;
+    p.K = (uint32_t)g->K;
+    p.xcls = g->xcls;
+    p.tau = tau;
+    p.off_pred = g->x_off_pred;
+    p.off_rows = g->x_off_rows;
+    p.off_cls = g->x_off_cls;
+    p.off_mem = g->x_off_mem;
+    p.off_orig = g->x_off_orig;
+    p.ws_off = (uint32_t)ws_off;
+    p.search = d_best ? 1 : 0;
+    int rc = k.launch(p, (int)grid, threads, smem, stream);
+    g_launches++;
+    if (rc) return cuda_err((cudaError_t)rc, "exact kernel launch");
+    return PP_OK;
+}
+
+int pp_eval_exact(const pp_dfg *g, int M, const uint8_t *d_placements, uint64_t count, uint64_t node_limit,
+                  uint64_t *d_makespan, uint8_t *d_exact, void *stream) {
+    if (!g || M < 1 || M > 8 || (g->hw && M > g->nd) || (count && (!d_placements || !d_makespan))) {
+        set_error("invalid arguments");
+        return PP_E_INVALID;
+    }
+    if (count == 0) return PP_OK;
+    return run_exact(g, M, GEN_EXPLICIT, 0, 0, nullptr, d_placements, 0, count, node_limit, d_makespan, d_exact,
+                     nullptr, stream);
+}
+
+int pp_eval_exact_generated(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t tau,
+                            const uint8_t *d_base_pi, uint64_t begin, uint64_t count, uint64_t node_limit,
+                            uint64_t *d_makespan, uint8_t *d_exact, void *stream) {
+    int rc = check_gen_args(g, M, gen, tau, begin + count);
+    if (rc) return rc;
+    if (count == 0) return PP_OK;
+    if (!d_makespan || (gen == GEN_PERTURB && !d_base_pi)) { set_error("NULL device buffer"); return PP_E_INVALID; }
+    return run_exact(g, M, gen, seed_r, tau, d_base_pi, nullptr, begin, begin + count, node_limit, d_makespan,
+                     d_exact, nullptr, stream);
+}
+
+int pp_search_exact(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t tau, const uint8_t *d_base_pi,
+                    uint64_t begin, uint64_t end, uint64_t node_limit, uint64_t *d_best, void *stream) {
+    int rc = check_gen_args(g, M, gen, tau, end);
+    if (rc) return rc;
+    if (end <= begin || !d_best || (gen == GEN_PERTURB && !d_base_pi)) {
+        set_error("invalid range or NULL buffer");
+        return PP_E_INVALID;
+    }
+    return run_exact(g, M, gen, seed_r, tau, d_base_pi, nullptr, begin, end, node_limit, nullptr, nullptr, d_best,
+                     stream);
 }
 
 void pp_rank_slice(uint64_t count, int rank, int world, uint64_t *begin, uint64_t *end) {

@@ -104,6 +104,74 @@ struct KParams {
     uint32_t off_cls;            // hardware graph: image offset of cls[a·8 + b]
 };
 
+// ---- exact-schedule image, built when
+// N = 2K ≤ 64 nodes:
+//   [XNode × N]        node n < K: forward of π position n; n ≥ K: backward of
+//                      π position n − K.  N-node order F_0..F_{K−1},
+//                      B_{K−1}..B_0 is topological.
+//   [XPred × NA]       predecessor arcs, contiguous per node
+//   [u64 × nrows·xcls] arc cost (ps) per device-pair class; row 0 is all zero
+//                      (the F_p → B_p arc and zero-cost inputs)
+//   [u8 × 64]          class of the ordered device pair (a, b), 0 iff a = b
+//   [u64 × K]          M(k) by π position
+//   [u8 × K]           descriptor index of π position p
+struct XNode {
+    uint64_t dur;         // Δf or Δb
+    uint64_t tail0;       // longest path from the node to the end with zero communication
+    uint64_t predmask;    // bit q set iff node q is a predecessor
+    uint16_t pred_begin;  // first XPred
+    uint8_t npred;        // number of XPred
+    uint8_t pos;          // π position (its device is the placement's device of pos)
+    uint32_t pad;
+};
+static_assert(sizeof(XNode) == 32, "XNode is 32 B");
+struct XPred {
+    uint8_t node;         // predecessor node
+    uint8_t pad;
+    uint16_t row;         // cost row
+};
+constexpr int kMaxExactNodes = 64;
+
+// per-warp branch-and-bound state of the exact kernel (shared memory)
+struct XWarp {
+    uint64_t fin[kMaxExactNodes];
+    uint64_t cand[kMaxExactNodes + 1];
+    uint64_t oldfree[kMaxExactNodes + 1];
+    uint64_t oldpm[kMaxExactNodes + 1];
+    uint64_t head[kMaxExactNodes];     // longest path to the node's start (this placement's delays)
+    uint64_t tail[kMaxExactNodes];     // longest path from the node's start to the end
+    uint64_t ebuf[kMaxExactNodes];     // per-expand lower bound on each unscheduled node's start
+    uint64_t freeT[8];
+    uint64_t rem[8];
+    uint8_t chosen[kMaxExactNodes + 1];
+    uint8_t ystar[kMaxExactNodes + 1];
+    uint8_t dev[kMaxExactNodes];       // by π position
+    uint8_t pad[14];
+};
+
+struct XParams {
+    const uint8_t *g_ximage;
+    const uint8_t *g_place;      // explicit placements [count][K] (descriptor order)
+    const uint8_t *g_base;       // PERTURB base, π order
+    uint64_t *g_makespan;        // per-candidate output [end − begin] (or null in search mode)
+    uint8_t *g_exact;            // per-candidate 1 = exact, 0 = node limit hit (optional)
+    uint64_t *g_partials;        // search mode: [grid][2] per-CTA argmin
+    unsigned *g_ticket;
+    uint64_t *g_out;             // search mode: {makespan, index, unresolved}
+    unsigned long long *g_work;  // [0] next candidate, [1] incumbent makespan, [2] unresolved count
+    uint64_t begin, end, seed, cap, node_limit;
+    uint32_t x_bytes, N, K, xcls, tau;
+    uint32_t off_pred, off_rows, off_cls, off_mem, off_orig;
+    uint32_t ws_off;             // smem offset of the first per-warp state block
+    int search;                  // 1: argmin with incumbent pruning
+};
+typedef int (*XLaunchFn)(const XParams &, int grid, int threads, int smem, void *stream);
+struct XKernelInfo {
+    XLaunchFn launch;
+    const void *func;
+};
+XKernelInfo exact_kernel_for(int M, int gen);
+
 // Device scalar slots of pp_dfg::d_scalars (u64).
 enum ScalarSlot : int {
     SC_LOCAL_MK = 0, SC_LOCAL_IDX = 1,       // this GPU's argmin of the round
@@ -153,6 +221,12 @@ struct pp_dfg {
     std::vector<uint8_t> image;  // host copy of the image
     uint32_t off_extra = 0, off_mem = 0, off_orig = 0, image_bytes = 0;
     uint32_t base_bytes = 0;     // K rounded up to 16
+    // exact-schedule image (empty when 2K > 64)
+    std::vector<uint8_t> ximage;
+    uint32_t xN = 0, xcls = 0, x_bytes = 0;
+    uint32_t x_off_pred = 0, x_off_rows = 0, x_off_cls = 0, x_off_mem = 0, x_off_orig = 0;
+    uint8_t *d_ximage = nullptr;
+    unsigned long long *d_xwork = nullptr;   // [4]
     // device memory
     uint8_t *d_image = nullptr;
     uint8_t *d_base = nullptr;        // [base_bytes] PERTURB base (π order)

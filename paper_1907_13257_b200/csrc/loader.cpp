@@ -401,6 +401,98 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     g->image_bytes = (uint32_t)bytes;
     g->base_bytes = (uint32_t)((K + 15) & ~15);
 
+    // ---- exact-schedule image (NEXT f1): plain u64 costs per device-pair class
+    if (2 * K <= kMaxExactNodes) {
+        const int N = 2 * K;
+        const int xcls = hw ? ncls : 2;
+        std::vector<uint8_t> xc(64, 0);
+        for (int a = 0; a < 8; a++)
+            for (int b = 0; b < 8; b++) xc[a * 8 + b] = hw ? (uint8_t)cls[a * 8 + b] : (uint8_t)(a != b);
+        std::vector<uint64_t> xrows(xcls, 0);                  // row 0: all zero
+        std::map<std::vector<uint64_t>, uint16_t> xrow_idx;
+        xrow_idx.emplace(std::vector<uint64_t>(xcls, 0), 0);
+        bool ok = true;
+        auto xrow = [&](int e, bool bwd) -> uint16_t {
+            std::vector<uint64_t> r(xcls, 0);
+            if (hw) {
+                const auto &h = bwd ? hcb : hcf;
+                for (int a = 0; a < nd; a++)
+                    for (int b = 0; b < nd; b++)
+                        if (a != b) r[cls[a * 8 + b]] = h[((size_t)e * nd + a) * nd + b];
+            } else {
+                r[1] = bwd ? cb[e] : cf[e];
+            }
+            auto it = xrow_idx.find(r);
+            if (it != xrow_idx.end()) return it->second;
+            const size_t idx = xrows.size() / xcls;
+            if (idx > 0xFFFF) { ok = false; return 0; }
+            xrows.insert(xrows.end(), r.begin(), r.end());
+            xrow_idx.emplace(r, (uint16_t)idx);
+            return (uint16_t)idx;
+        };
+        std::vector<XNode> xn(N);
+        std::vector<XPred> xp;
+        std::vector<std::vector<int>> succ(N);
+        for (int n = 0; n < N; n++) {
+            const bool f = n < K;
+            const int p = f ? n : n - K;
+            XNode &x = xn[n];
+            memset(&x, 0, sizeof x);
+            x.dur = f ? d->fwd_ps[pi[p]] : d->bwd_ps[pi[p]];
+            x.pos = (uint8_t)p;
+            x.pred_begin = (uint16_t)xp.size();
+            auto arc = [&](int q, uint16_t row) {
+                xp.push_back(XPred{(uint8_t)q, 0, row});
+                x.predmask |= 1ull << q;
+                succ[q].push_back(n);
+            };
+            if (f) {
+                for (int e : in_e[p]) arc(pos[src[e]], xrow(e, false));
+            } else {
+                arc(p, 0);                                      // own forward (R1)
+                for (int e : out_e[p]) arc(K + pos[dst[e]], xrow(e, true));
+            }
+            const size_t np = xp.size() - x.pred_begin;
+            if (np > 255 || xp.size() > 0xFFFF) ok = false;
+            x.npred = (uint8_t)np;
+        }
+        // tail0 over the reverse of the topological order F_0..F_{K−1}, B_{K−1}..B_0
+        for (int t = N - 1; t >= 0; t--) {
+            const int n = t < K ? t : N - 1 - (t - K);
+            uint64_t m = 0;
+            for (int s2 : succ[n]) m = std::max(m, xn[s2].tail0);
+            xn[n].tail0 = xn[n].dur + m;
+        }
+        if (ok) {
+            size_t o = sizeof(XNode) * N;
+            g->x_off_pred = (uint32_t)o;
+            o = (o + sizeof(XPred) * xp.size() + 7) & ~size_t(7);
+            g->x_off_rows = (uint32_t)o;
+            o += 8 * xrows.size();
+            g->x_off_cls = (uint32_t)o;
+            o += 64;
+            g->x_off_mem = (uint32_t)o;
+            o += 8ull * K;
+            g->x_off_orig = (uint32_t)o;
+            o = (o + K + 15) & ~size_t(15);
+            if (o <= (size_t)kMaxImageBytes) {
+                g->ximage.assign(o, 0);
+                memcpy(g->ximage.data(), xn.data(), sizeof(XNode) * N);
+                if (!xp.empty()) memcpy(g->ximage.data() + g->x_off_pred, xp.data(), sizeof(XPred) * xp.size());
+                memcpy(g->ximage.data() + g->x_off_rows, xrows.data(), 8 * xrows.size());
+                memcpy(g->ximage.data() + g->x_off_cls, xc.data(), 64);
+                for (int p = 0; p < K; p++) {
+                    uint64_t m = d->mem_bytes ? d->mem_bytes[pi[p]] : 0;
+                    memcpy(g->ximage.data() + g->x_off_mem + 8ull * p, &m, 8);
+                    g->ximage[g->x_off_orig + p] = (uint8_t)pi[p];
+                }
+                g->xN = (uint32_t)N;
+                g->xcls = (uint32_t)xcls;
+                g->x_bytes = (uint32_t)o;
+            }
+        }
+    }
+
     // ---- device side
     int prev = 0;
     cudaGetDevice(&prev);
@@ -418,6 +510,13 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
         (ce = cudaMalloc(&g->d_partials, sizeof(uint64_t) * 2 * kMaxGrid)) != cudaSuccess ||
         (ce = cudaMalloc(&g->d_ticket, sizeof(unsigned) * 4)) != cudaSuccess ||
         (ce = cudaMalloc(&g->d_scalars, sizeof(uint64_t) * scal)) != cudaSuccess) {
+        pp_free_dfg(g);
+        return cuda_fail(ce);
+    }
+    if (g->x_bytes &&
+        ((ce = cudaMalloc(&g->d_ximage, g->x_bytes)) != cudaSuccess ||
+         (ce = cudaMalloc(&g->d_xwork, sizeof(unsigned long long) * 4)) != cudaSuccess ||
+         (ce = cudaMemcpy(g->d_ximage, g->ximage.data(), g->x_bytes, cudaMemcpyHostToDevice)) != cudaSuccess)) {
         pp_free_dfg(g);
         return cuda_fail(ce);
     }
@@ -447,6 +546,8 @@ extern "C" void pp_free_dfg(pp_dfg *g) {
     if (g->d_partials) cudaFree(g->d_partials);
     if (g->d_ticket) cudaFree(g->d_ticket);
     if (g->d_scalars) cudaFree(g->d_scalars);
+    if (g->d_ximage) cudaFree(g->d_ximage);
+    if (g->d_xwork) cudaFree(g->d_xwork);
     cudaSetDevice(prev);
     delete g;
 }

@@ -1,5 +1,6 @@
 // search_inst.cu — instantiates the search/eval kernels for one device count
 // M (compiled once per M ∈ [1,8] with -DPP_M=M, in parallel).
+#include "exact_kernel.cuh"
 #include "search_kernel.cuh"
 
 #ifndef PP_M
@@ -61,6 +62,20 @@ UpdateFn PP_CAT(update_for_m, PP_M)(int gen) {
         case GEN_GRAY: return &launch_update<PP_M, GEN_GRAY>;
         case GEN_RANDOM: return &launch_update<PP_M, GEN_RANDOM>;
         default: return &launch_update<PP_M, GEN_PERTURB>;
+    }
+}
+
+template <int GEN>
+static XKernelInfo xinfo() {
+    return XKernelInfo{&launch_exact<PP_M, GEN>, reinterpret_cast<const void *>(&exact_kernel<PP_M, GEN>)};
+}
+
+XKernelInfo PP_CAT(exact_for_m, PP_M)(int gen) {
+    switch (gen) {
+        case GEN_GRAY: return xinfo<GEN_GRAY>();
+        case GEN_RANDOM: return xinfo<GEN_RANDOM>();
+        case GEN_PERTURB: return xinfo<GEN_PERTURB>();
+        default: return xinfo<GEN_EXPLICIT>();
     }
 }
 

@@ -99,6 +99,12 @@ SIGNATURES = {
                            C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
     "pp_search_range": ([C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint64,
                          C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
+    "pp_eval_exact": ([C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                       C.c_void_p], C.c_int),
+    "pp_eval_exact_generated": ([C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint64,
+                                 C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "pp_search_exact": ([C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint64,
+                         C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
     "pp_search_best": ([C.c_void_p, C.c_int, P(SearchDesc), C.c_void_p, C.c_void_p, P(SearchResultC)], C.c_int),
     "pp_comm_get_unique_id": ([P(C.c_uint8)], C.c_int),
     "pp_comm_init": ([P(C.c_uint8), C.c_int, C.c_int, C.c_int, P(C.c_void_p)], C.c_int),
@@ -279,6 +285,49 @@ class Dfg:
         _check(lib().pp_search_range(self._h, M, gen, seed_r, tau, _dptr(b), begin, end, _dptr(out),
                                      _stream(stream)))
         return out
+
+    # ------------------------------------------- exact schedule (§8(f) f1)
+    def eval_exact(self, M, placements, node_limit=0, out=None, exact=None, stream=None):
+        """Makespan-optimal schedule of each placement (uint8 CUDA tensor
+        [count, K], descriptor order).  Returns (makespans int64 tensor,
+        exact-flag uint8 tensor)."""
+        import torch
+        _require_cuda(placements, ("uint8",))
+        count = placements.shape[0]
+        if placements.dim() != 2 or placements.shape[1] != self.K:
+            raise PPError(-1, "placements must be [count, K]")
+        if out is None:
+            out = torch.empty(count, dtype=torch.int64, device=placements.device)
+        if exact is None:
+            exact = torch.empty(count, dtype=torch.uint8, device=placements.device)
+        _check(lib().pp_eval_exact(self._h, M, _dptr(placements), count, node_limit, _dptr(out), _dptr(exact),
+                                   _stream(stream)))
+        return out, exact
+
+    def eval_exact_generated(self, M, gen, seed_r, tau, base_pi, begin, count, node_limit=0, stream=None):
+        import torch
+        dev = torch.device("cuda", self.device)
+        out = torch.empty(count, dtype=torch.int64, device=dev)
+        exact = torch.empty(count, dtype=torch.uint8, device=dev)
+        b = None
+        if gen == GEN_PERTURB:
+            b = torch.as_tensor(np.asarray(base_pi, dtype=np.uint8), device=dev)
+        _check(lib().pp_eval_exact_generated(self._h, M, gen, seed_r, tau, _dptr(b), begin, count, node_limit,
+                                             _dptr(out), _dptr(exact), _stream(stream)))
+        return out, exact
+
+    def search_exact(self, M, gen, seed_r, tau, base_pi, begin, end, node_limit=0, stream=None):
+        """(exact makespan, index, unresolved) of the argmin over [begin, end)."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        out = torch.empty(3, dtype=torch.int64, device=dev)
+        b = None
+        if gen == GEN_PERTURB:
+            b = torch.as_tensor(np.asarray(base_pi, dtype=np.uint8), device=dev)
+        _check(lib().pp_search_exact(self._h, M, gen, seed_r, tau, _dptr(b), begin, end, node_limit, _dptr(out),
+                                     _stream(stream)))
+        r = u64(out)
+        return int(r[0]), int(r[1]), int(r[2])
 
     def search_best(self, M, gen, seed, count, rounds=1, tau=0, base=None, comm=None, stream=None):
         b = None
