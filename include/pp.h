@@ -213,6 +213,17 @@ int pp_search_exact(const pp_dfg *dfg, int M, int gen, uint64_t seed_r, uint32_t
                     const uint8_t *d_base_pi, uint64_t begin, uint64_t end, uint64_t node_limit,
                     uint64_t *d_best, void *cuda_stream);
 
+/* ----------------------------------------- EFT base seed (§8(f) f4) --
+ * The earliest-finish-time greedy placement (SPEC.md:245–253
+ * heuristic_place; reading R23): forward ops in π order, each
+ * on the device where it would finish first given the ops already placed and
+ * the incoming transfer delays (ties → smaller device), skipping devices
+ * whose memory would exceed the cap.  A good PERTURB base
+ * (pp_search_desc.base).  placement: host ptr uint8 [K], descriptor order.
+ * Synchronises cuda_stream.  Errors: PP_E_INVALID, PP_E_INFEASIBLE (an op
+ * fits on no device), PP_E_CUDA.                                            */
+int pp_eft_place(const pp_dfg *dfg, int M, uint8_t *placement, void *cuda_stream);
+
 /* Full search: per round the candidates are sharded over
  * the ranks of `comm` (contiguous slices, see pp_rank_slice), each GPU takes
  * its slice's argmin, one NCCL min all-reduce of the packed key

@@ -118,6 +118,7 @@ def lib():
         L.or_round_exact.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32, P(C.c_uint8),
                                      C.c_uint64, C.c_uint64]
         L.or_round_exact.restype = _Best
+        L.or_eft_orig.argtypes = [C.c_void_p, C.c_int, P(C.c_uint8)]
         L.or_mix.argtypes = [C.c_uint64]; L.or_mix.restype = C.c_uint64
         L.or_gen.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint32, P(C.c_uint8),
                              C.c_uint64, P(C.c_uint8)]
@@ -247,6 +248,14 @@ class Dfg:
         if rc:
             raise OracleError(rc)
         return int(out.value)
+
+    def eft(self, M: int) -> np.ndarray:
+        """NEXT f4: the EFT-greedy placement (descriptor order)."""
+        d = np.zeros(self.K, dtype=np.uint8)
+        rc = lib().or_eft_orig(self._h, M, d.ctypes.data_as(C.POINTER(C.c_uint8)))
+        if rc:
+            raise OracleError(rc)
+        return d
 
     def exact_pi(self, M: int, d_pi) -> int:
         d = np.ascontiguousarray(np.asarray(d_pi, dtype=np.uint8))

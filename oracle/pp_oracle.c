@@ -29,6 +29,9 @@
  *   or_crossover               pinned (K10–K14 paper statements)
  *   or_prepare_hw              pinned (SPEC route examples, closed forms on
  *                              ring/switch/two-node graphs, Floyd–Warshall)
+ *   or_eft                     pinned (SPEC heuristic_place examples, closed
+ *                              forms: round-robin of equal independent ops,
+ *                              chain kept whole, diamond → (0,0,1,1))
  *   or_exact / or_round_exact  pinned (SPEC exact_schedule examples, a hand
  *                              case where in-order issue loses, brute force
  *                              over per-device orders, exact ≤ in-order)
@@ -548,6 +551,56 @@ int or_makespan_exact_orig(const or_ctx *c, int M, const uint8_t *d_orig, uint64
     *out = or_exact(c, M, d);
     free(d);
     return OR_OK;
+}
+
+/* ----------------------------------------- NEXT f4: EFT-greedy base seed */
+/* SPEC.md:245–253 heuristic_place: "earliest-finish-time greedy in
+ * topological order: each vertex assigned to the device minimizing its
+ * completion time given current partial schedule and incoming-edge
+ * communication delays; memory-feasible".  Reading R23: the forward pass in
+ * π order decides (the backward ops follow their forward op's device);
+ * ties go to the smallest device; a device whose memory would exceed the cap
+ * is skipped; no feasible device => OR_E_INFEASIBLE.
+ * d_out receives the placement by π position.                                */
+int or_eft(const or_ctx *c, int M, uint8_t *d_out) {
+    int K = c->K;
+    if (M < 1 || M > 8 || (c->nd && M > c->nd)) return OR_E_INVALID;
+    uint64_t *fin = calloc((size_t)K + 1, 8);
+    uint64_t free_t[8] = {0};
+    u128 used[8] = {0};
+    for (int p = 0; p < K; p++) {
+        int best_m = -1;
+        uint64_t best_f = 0;
+        for (int m = 0; m < M; m++) {
+            if (c->cap > 0 && used[m] + c->mem[p] > c->cap) continue;
+            uint64_t r = 0;
+            for (int i = 0; i < c->in_cnt[p]; i++) {
+                int u = c->in_src[p][i];
+                uint64_t cost = c->nd ? c->cfm[((size_t)c->in_eid[p][i] * c->nd + d_out[u]) * c->nd + m]
+                                      : c->in_cf[p][i];
+                uint64_t t = fin[u] + (d_out[u] != m ? cost : 0);
+                if (t > r) r = t;
+            }
+            uint64_t st = r > free_t[m] ? r : free_t[m];
+            uint64_t f = st + c->df[p];
+            if (best_m < 0 || f < best_f) { best_m = m; best_f = f; }
+        }
+        if (best_m < 0) { free(fin); return OR_E_INFEASIBLE; }
+        d_out[p] = (uint8_t)best_m;
+        fin[p] = best_f;
+        free_t[best_m] = best_f;
+        used[best_m] += c->mem[p];
+    }
+    free(fin);
+    return OR_OK;
+}
+
+int or_eft_orig(const or_ctx *c, int M, uint8_t *d_orig) {
+    uint8_t *d = malloc((size_t)c->K + 1);
+    int rc = or_eft(c, M, d);
+    if (rc == OR_OK) for (int p = 0; p < c->K; p++) d_orig[c->pi[p]] = d[p];
+    free(d);
+    return rc;
 }
 
 /* ------------------------------------------------------- O5 / O6 generators */

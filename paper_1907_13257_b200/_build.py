@@ -40,6 +40,7 @@ def _sources():
     for m in range(1, 9):
         jobs.append(("search_inst.cu", f"search_m{m}.o", [f"-DPP_M={m}"]))
     jobs.append(("projection.cu", "projection.o", []))
+    jobs.append(("eft.cu", "eft.o", []))
     jobs.append(("loader.cpp", "loader.o", []))
     jobs.append(("capi.cpp", "capi.o", ["-I", _nccl_include()]))
     return jobs

@@ -71,6 +71,8 @@ XKernelInfo exact_kernel_for(int M, int gen) {
     }
 }
 
+int launch_eft(const pp_dfg *g, int M, uint8_t *d_out, int *d_status, void *stream);
+
 struct ProjParams;
 struct CrossParams;
 int launch_pack_key(uint64_t *s, int rank, void *stream);
@@ -472,6 +474,35 @@ int pp_search_exact(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
     }
     return run_exact(g, M, gen, seed_r, tau, d_base_pi, nullptr, begin, end, node_limit, nullptr, nullptr, d_best,
                      stream);
+}
+
+// ------------------------------------------------- EFT base seed (NEXT f4)
+int pp_eft_place(const pp_dfg *g, int M, uint8_t *placement, void *stream) {
+    if (!g || M < 1 || M > 8 || (g->hw && M > g->nd) || !placement) {
+        set_error("invalid arguments");
+        return PP_E_INVALID;
+    }
+    DeviceGuard dg(g->device);
+    if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    // scratch: the placement in d_winner, the status in the ticket slot 2
+    int *d_status = reinterpret_cast<int *>(g->d_ticket + 2);
+    int rc = launch_eft(g, M, g->d_winner, d_status, stream);
+    g_launches++;
+    if (rc) return cuda_err((cudaError_t)rc, "EFT kernel launch");
+    std::vector<uint8_t> pl(g->K);
+    int status = 0;
+    cudaError_t ce;
+    if ((ce = cudaMemcpyAsync(pl.data(), g->d_winner, g->K, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (ce = cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (ce = cudaStreamSynchronize(st)) != cudaSuccess)
+        return cuda_err(ce, "EFT result");
+    if (status) {
+        set_error("no memory-feasible device for some op");
+        return PP_E_INFEASIBLE;
+    }
+    for (int p = 0; p < g->K; p++) placement[g->pi[p]] = pl[p];
+    return PP_OK;
 }
 
 void pp_rank_slice(uint64_t count, int rank, int world, uint64_t *begin, uint64_t *end) {

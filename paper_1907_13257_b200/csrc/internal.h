@@ -132,6 +132,23 @@ struct XPred {
 };
 constexpr int kMaxExactNodes = 64;
 
+// ---- EFT image, any K:
+//   [GOp × K]          forward op of π position p
+//   [GArc × NA]        its forward in-arcs
+//   [u64 × nrows·gcls] cost rows (as in the exact image; row 0 all zero)
+//   [u8 × 64]          class of the ordered device pair
+struct GOp {
+    uint64_t fwd;         // Δf
+    uint64_t mem;         // M(k)
+    uint32_t in_begin, in_cnt;
+    uint64_t pad;
+};
+static_assert(sizeof(GOp) == 32, "GOp is 32 B");
+struct GArc {
+    uint32_t u;           // producer's π position
+    uint32_t row;         // cost row
+};
+
 // per-warp branch-and-bound state of the exact kernel (shared memory)
 struct XWarp {
     uint64_t fin[kMaxExactNodes];
@@ -226,6 +243,10 @@ struct pp_dfg {
     uint32_t xN = 0, xcls = 0, x_bytes = 0;
     uint32_t x_off_pred = 0, x_off_rows = 0, x_off_cls = 0, x_off_mem = 0, x_off_orig = 0;
     uint8_t *d_ximage = nullptr;
+    // EFT image
+    std::vector<uint8_t> gimage;
+    uint32_t g_off_arc = 0, g_off_rows = 0, g_off_cls = 0, g_bytes = 0, gcls = 0;
+    uint8_t *d_gimage = nullptr;
     unsigned long long *d_xwork = nullptr;   // [4]
     // device memory
     uint8_t *d_image = nullptr;

@@ -401,35 +401,60 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     g->image_bytes = (uint32_t)bytes;
     g->base_bytes = (uint32_t)((K + 15) & ~15);
 
-    // ---- exact-schedule image (NEXT f1): plain u64 costs per device-pair class
+    // ---- cost rows shared by the exact-schedule and EFT images: plain u64 ps
+    // per device-pair class, deduplicated by content; row 0 is all zero
+    const int xcls = hw ? ncls : 2;
+    std::vector<uint8_t> xc(64, 0);
+    for (int a = 0; a < 8; a++)
+        for (int b = 0; b < 8; b++) xc[a * 8 + b] = hw ? (uint8_t)cls[a * 8 + b] : (uint8_t)(a != b);
+    std::vector<uint64_t> xrows(xcls, 0);
+    std::map<std::vector<uint64_t>, uint32_t> xrow_idx;
+    xrow_idx.emplace(std::vector<uint64_t>(xcls, 0), 0u);
+    auto xrow = [&](int e, bool bwd) -> uint32_t {
+        std::vector<uint64_t> r(xcls, 0);
+        if (hw) {
+            const auto &h = bwd ? hcb : hcf;
+            for (int a = 0; a < nd; a++)
+                for (int b = 0; b < nd; b++)
+                    if (a != b) r[cls[a * 8 + b]] = h[((size_t)e * nd + a) * nd + b];
+        } else {
+            r[1] = bwd ? cb[e] : cf[e];
+        }
+        auto it = xrow_idx.find(r);
+        if (it != xrow_idx.end()) return it->second;
+        const uint32_t idx = (uint32_t)(xrows.size() / xcls);
+        xrows.insert(xrows.end(), r.begin(), r.end());
+        xrow_idx.emplace(r, idx);
+        return idx;
+    };
+
+    // ---- EFT image (NEXT f4): forward in-arcs by π position, any K
+    {
+        std::vector<GOp> go(K);
+        std::vector<GArc> ga;
+        for (int p = 0; p < K; p++) {
+            GOp &o = go[p];
+            memset(&o, 0, sizeof o);
+            o.fwd = d->fwd_ps[pi[p]];
+            o.mem = d->mem_bytes ? d->mem_bytes[pi[p]] : 0;
+            o.in_begin = (uint32_t)ga.size();
+            for (int e : in_e[p]) ga.push_back(GArc{(uint32_t)pos[src[e]], xrow(e, false)});
+            o.in_cnt = (uint32_t)(ga.size() - o.in_begin);
+        }
+        size_t o = sizeof(GOp) * K;
+        g->g_off_arc = (uint32_t)o;
+        o = (o + sizeof(GArc) * ga.size() + 7) & ~size_t(7);
+        g->g_off_rows = (uint32_t)o;
+        // rows are appended after the exact image is built (it may add rows)
+        g->gimage.assign(o, 0);
+        memcpy(g->gimage.data(), go.data(), sizeof(GOp) * K);
+        if (!ga.empty()) memcpy(g->gimage.data() + g->g_off_arc, ga.data(), sizeof(GArc) * ga.size());
+    }
+
+    // ---- exact-schedule image (NEXT f1)
     if (2 * K <= kMaxExactNodes) {
         const int N = 2 * K;
-        const int xcls = hw ? ncls : 2;
-        std::vector<uint8_t> xc(64, 0);
-        for (int a = 0; a < 8; a++)
-            for (int b = 0; b < 8; b++) xc[a * 8 + b] = hw ? (uint8_t)cls[a * 8 + b] : (uint8_t)(a != b);
-        std::vector<uint64_t> xrows(xcls, 0);                  // row 0: all zero
-        std::map<std::vector<uint64_t>, uint16_t> xrow_idx;
-        xrow_idx.emplace(std::vector<uint64_t>(xcls, 0), 0);
         bool ok = true;
-        auto xrow = [&](int e, bool bwd) -> uint16_t {
-            std::vector<uint64_t> r(xcls, 0);
-            if (hw) {
-                const auto &h = bwd ? hcb : hcf;
-                for (int a = 0; a < nd; a++)
-                    for (int b = 0; b < nd; b++)
-                        if (a != b) r[cls[a * 8 + b]] = h[((size_t)e * nd + a) * nd + b];
-            } else {
-                r[1] = bwd ? cb[e] : cf[e];
-            }
-            auto it = xrow_idx.find(r);
-            if (it != xrow_idx.end()) return it->second;
-            const size_t idx = xrows.size() / xcls;
-            if (idx > 0xFFFF) { ok = false; return 0; }
-            xrows.insert(xrows.end(), r.begin(), r.end());
-            xrow_idx.emplace(r, (uint16_t)idx);
-            return (uint16_t)idx;
-        };
         std::vector<XNode> xn(N);
         std::vector<XPred> xp;
         std::vector<std::vector<int>> succ(N);
@@ -441,8 +466,9 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
             x.dur = f ? d->fwd_ps[pi[p]] : d->bwd_ps[pi[p]];
             x.pos = (uint8_t)p;
             x.pred_begin = (uint16_t)xp.size();
-            auto arc = [&](int q, uint16_t row) {
-                xp.push_back(XPred{(uint8_t)q, 0, row});
+            auto arc = [&](int q, uint32_t row) {
+                if (row > 0xFFFF) ok = false;
+                xp.push_back(XPred{(uint8_t)q, 0, (uint16_t)row});
                 x.predmask |= 1ull << q;
                 succ[q].push_back(n);
             };
@@ -493,6 +519,18 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
         }
     }
 
+    {   // EFT image: rows and class table
+        size_t o = g->g_off_rows;
+        g->gimage.resize(o + 8 * xrows.size());
+        memcpy(g->gimage.data() + o, xrows.data(), 8 * xrows.size());
+        o += 8 * xrows.size();
+        g->g_off_cls = (uint32_t)o;
+        g->gimage.resize((o + 64 + 15) & ~size_t(15), 0);
+        memcpy(g->gimage.data() + o, xc.data(), 64);
+        g->gcls = (uint32_t)xcls;
+        g->g_bytes = (uint32_t)g->gimage.size();
+    }
+
     // ---- device side
     int prev = 0;
     cudaGetDevice(&prev);
@@ -510,6 +548,11 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
         (ce = cudaMalloc(&g->d_partials, sizeof(uint64_t) * 2 * kMaxGrid)) != cudaSuccess ||
         (ce = cudaMalloc(&g->d_ticket, sizeof(unsigned) * 4)) != cudaSuccess ||
         (ce = cudaMalloc(&g->d_scalars, sizeof(uint64_t) * scal)) != cudaSuccess) {
+        pp_free_dfg(g);
+        return cuda_fail(ce);
+    }
+    if ((ce = cudaMalloc(&g->d_gimage, g->g_bytes)) != cudaSuccess ||
+        (ce = cudaMemcpy(g->d_gimage, g->gimage.data(), g->g_bytes, cudaMemcpyHostToDevice)) != cudaSuccess) {
         pp_free_dfg(g);
         return cuda_fail(ce);
     }
@@ -548,6 +591,7 @@ extern "C" void pp_free_dfg(pp_dfg *g) {
     if (g->d_scalars) cudaFree(g->d_scalars);
     if (g->d_ximage) cudaFree(g->d_ximage);
     if (g->d_xwork) cudaFree(g->d_xwork);
+    if (g->d_gimage) cudaFree(g->d_gimage);
     cudaSetDevice(prev);
     delete g;
 }

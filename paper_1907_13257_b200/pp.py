@@ -105,6 +105,7 @@ SIGNATURES = {
                                  C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "pp_search_exact": ([C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint64,
                          C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
+    "pp_eft_place": ([C.c_void_p, C.c_int, P(C.c_uint8), C.c_void_p], C.c_int),
     "pp_search_best": ([C.c_void_p, C.c_int, P(SearchDesc), C.c_void_p, C.c_void_p, P(SearchResultC)], C.c_int),
     "pp_comm_get_unique_id": ([P(C.c_uint8)], C.c_int),
     "pp_comm_init": ([P(C.c_uint8), C.c_int, C.c_int, C.c_int, P(C.c_void_p)], C.c_int),
@@ -285,6 +286,12 @@ class Dfg:
         _check(lib().pp_search_range(self._h, M, gen, seed_r, tau, _dptr(b), begin, end, _dptr(out),
                                      _stream(stream)))
         return out
+
+    def eft_place(self, M, stream=None) -> np.ndarray:
+        """EFT-greedy placement (descriptor order), computed on the GPU."""
+        pl = np.zeros(self.K, dtype=np.uint8)
+        _check(lib().pp_eft_place(self._h, M, _ptr(pl, C.c_uint8), _stream(stream)))
+        return pl
 
     # ------------------------------------------- exact schedule (§8(f) f1)
     def eval_exact(self, M, placements, node_limit=0, out=None, exact=None, stream=None):
