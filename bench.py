@@ -148,18 +148,19 @@ def measured_clock():
 
 
 # ------------------------------------------------------------ oracle arm
-def cpu_oracle_sample(spec, M, gen_name, tau, n_target_s=12.0):
+def cpu_oracle_sample(spec, M, gen_name, tau, base_kind, n_target_s=12.0):
     """The CPU oracle (oracle/) as it stands, single thread, on a bounded
     prefix of round 0 of the same candidate stream (placements/s, n, s)."""
     import oracle as O
     gen = O.GEN_PERTURB if gen_name == "perturb" else O.GEN_RANDOM
     od = O.Dfg.from_spec(spec)
+    base_pi = od.eft(M)[od.pi] if (gen == O.GEN_PERTURB and base_kind == "eft") else None
     t = time.perf_counter()
-    od.round(M, gen, SEED, tau, None, 0, 20_000)
+    od.round(M, gen, SEED, tau, base_pi, 0, 20_000)
     rate = 20_000 / (time.perf_counter() - t)
     count = max(20_000, int(rate * n_target_s))
     t = time.perf_counter()
-    od.round(M, gen, SEED, tau, None, 0, count)
+    od.round(M, gen, SEED, tau, base_pi, 0, count)
     dt = time.perf_counter() - t
     return count / dt, count, dt
 
@@ -179,7 +180,8 @@ def run_reference(args):
     for s in range(args.warmup + args.steps):
         t = time.perf_counter()
         od = O.Dfg.from_spec(spec)
-        r = od.search(args.M, gen, SEED, per_round, rounds=rounds, tau=args.tau)
+        base = od.eft(args.M) if (gen == O.GEN_PERTURB and args.base == "eft") else None
+        r = od.search(args.M, gen, SEED, per_round, rounds=rounds, tau=args.tau, base=base)
         sc = scenario(args, od.t1, od.grad_bytes)
         cells = O.Scenario.from_spec(sc).project([1, args.M], [od.t1, r.best_makespan_ps], args.nmax)
         x = O.crossover(cells, [1, args.M], args.nmax)
@@ -211,6 +213,8 @@ def config_dict(args, spec, per_step=None):
             "dfg": WORKLOADS[args.workload], "K": len(spec["fwd_ps"]),
             "E": len(spec["edge_src"]), "M": args.M, "generator": gen + " (SplitMix64)", "seed": SEED,
             "candidates_per_step": per_step or args.count * args.rounds,
+            "base": ("EFT greedy placement (pp_eft_place, SURVEY 8(f) f4)" if args.base == "eft" and args.gen == "perturb"
+                     else "all ops on device 0"),
             "projection": f"M in {{1,{args.M}}}, N=1..{args.nmax}, EQ5, ring AR on",
             "l2": "flushed between timed steps (256 MiB write); inputs live on-chip",
             **({"hardware_graph": HW_GRAPHS[args.hw]} if args.hw != "none" else {})}
@@ -245,8 +249,12 @@ def run_pp(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    use_eft = GEN == pp.GEN_PERTURB and args.base == "eft"
+
     def step():
-        r = g.search_best(M, GEN, SEED, args.count, rounds=args.rounds, tau=args.tau, comm=comm, stream=stream)
+        base = g.eft_place(M, stream=stream) if use_eft else None      # SURVEY §8(f) f4 base seed
+        r = g.search_best(M, GEN, SEED, args.count, rounds=args.rounds, tau=args.tau, base=base, comm=comm,
+                          stream=stream)
         cells = pp.project_e2e(sc, [1, M], [g.t1, r.best_makespan_ps], args.nmax, device=local, stream=stream)
         x = pp.crossover(cells, [1, M], args.nmax, best_m=False, stream=stream)
         return r, x
@@ -287,7 +295,9 @@ def run_pp(args):
         t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         g2 = pp.Dfg(spec, device=local)                        # H2D of the DFG image
-        r2 = g2.search_best(M, GEN, SEED, args.count, rounds=args.rounds, tau=args.tau, comm=comm, stream=stream)
+        base2 = g2.eft_place(M, stream=stream) if use_eft else None
+        r2 = g2.search_best(M, GEN, SEED, args.count, rounds=args.rounds, tau=args.tau, base=base2, comm=comm,
+                            stream=stream)
         cells2 = pp.project_e2e(sc, [1, M], [g2.t1, r2.best_makespan_ps], args.nmax, device=local, stream=stream)
         x2 = pp.crossover(cells2, [1, M], args.nmax, best_m=False, stream=stream)
         t1.record(stream)
@@ -295,6 +305,8 @@ def run_pp(args):
         e2e_ms.append(t0.elapsed_time(t1))
         h2d = g2.image_bytes + ((g2.K + 15) // 16) * 16           # image + base upload
         d2h = 24 + ((g2.K + 15) // 16) * 16 + 4 + 76             # result, placement, range flag, crossover
+        if use_eft:
+            d2h += g2.K + 4                                      # EFT placement + status
         g2.close()
     e2 = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -331,7 +343,7 @@ def run_pp(args):
                        "n_star_vs_best_dp": x.n_star_vs_best_dp},
         }
         if world == 1 and not args.no_cpu_baseline:
-            rate, n, dt = cpu_oracle_sample(spec, M, args.gen, args.tau)
+            rate, n, dt = cpu_oracle_sample(spec, M, args.gen, args.tau, args.base)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                                     "sample": f"first {n} {args.gen.upper()} candidates of round 0 of the same "
                                               f"stream, {dt:.1f} s, single thread (nproc={os.cpu_count()})"}
@@ -357,6 +369,7 @@ def main():
     ap.add_argument("--gen", default="perturb", choices=["perturb", "random"])
     ap.add_argument("--tau", type=int, default=8)
     ap.add_argument("--nmax", type=int, default=1024)
+    ap.add_argument("--base", default="eft", choices=["eft", "zero"], help="PERTURB starting placement")
     ap.add_argument("--hw", default="none", choices=["none", *HW_GRAPHS],
                     help="evaluate on a general hardware graph instead of the uniform link")
     ap.add_argument("--ref-sample", type=int, default=200_000)

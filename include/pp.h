@@ -264,7 +264,14 @@ int      pp_key_rank(uint64_t key);
  *   AR(W) = 0 if W = 1 else ⌈2(W−1)·S_grad·10^12/(W·BW)⌉ + 2(W−1)·α with the
  *   intra tier if N ≤ node_size else the inter tier (R10;
  *   a tier with BW = 0 is "SE ≡ 1"),
- *   T = ⌊(T_1 + AR)·T_M / T_1⌋ (EQ5, SU^M·SE_W of Eq. 5, R11) or T_M + AR (TIME). */
+ *   T = ⌊(T_1 + AR)·T_M / T_1⌋ (EQ5, SU^M·SE_W of Eq. 5, R11) or T_M + AR (TIME).
+ * Gradient-accumulation axis (PAPER.md:251 delayed
+ * gradient update; R25): with factors a ∈ accum[], a cell accumulates a
+ * mini-batches per step: G = W·B·a, T = ⌊(a·T_1 + AR)·T_M / T_1⌋ (EQ5) or
+ * a·T_M + AR (TIME); the cell keeps the a with the least C (ties → earlier in
+ * accum[]) in pp_cell.accum.  Placement-aware all-reduce (R24): with
+ * shard_bytes, hybrid M all-reduces each device's shard over its W peers in
+ * parallel, AR = max_d AR(W, S_d) (pp_shard_bytes gives S_d of a placement). */
 typedef struct {
     uint64_t        dataset_items;   /* D ≥ 1                                   */
     uint32_t        mini_batch;      /* B ≥ 1                                   */
@@ -276,13 +283,23 @@ typedef struct {
     uint32_t        node_size;       /* 0 ⇒ 8                                   */
     uint32_t        ar_mode;         /* 0 = EQ5 (default), 1 = TIME             */
     uint64_t        t1_ps;           /* T_1 > 0                                 */
+    uint32_t        n_accum;         /* 0 ⇒ a = 1 only; else ≤ 32 factors       */
+    uint32_t        _pad;
+    const uint32_t *accum;           /* host ptr [n_accum], each ≥ 1            */
+    const uint64_t *shard_bytes;     /* host ptr [nM][8] (row m: S_d of Ms[m]'s
+                                        placement, d < Ms[m]) or NULL ⇒ every
+                                        device all-reduces grad_bytes       */
 } pp_scenario;
 
 typedef struct {
     uint64_t C_lo, C_hi;             /* C as u128 (ps × µ-epochs)               */
     uint64_t step_ps, steps, uepochs;
-    uint32_t feasible, _pad;
+    uint32_t feasible, accum;        /* accum: the chosen a (0 if infeasible)   */
 } pp_cell;
+
+/* S_d = Σ param_bytes of the ops placed on device d (R24).  placement: host
+ * ptr uint8 [K] descriptor order, values < M; out: host ptr uint64 [8].     */
+int pp_shard_bytes(const pp_dfg *dfg, int M, const uint8_t *placement, uint64_t *out);
 
 /* Ms, T_M_ps: host ptrs [nM] (nM ∈ [1,8], each M ≥ 1, T_M > 0);
  * d_cells: device ptr pp_cell [nM][N_max], cell (m, N) at m·N_max + N−1;

@@ -67,13 +67,15 @@ class _Scenario(C.Structure):
                 ("grad_bytes", C.c_uint64),
                 ("bw_intra_Bps", C.c_uint64), ("lat_intra_ps", C.c_uint64),
                 ("bw_inter_Bps", C.c_uint64), ("lat_inter_ps", C.c_uint64),
-                ("node_size", C.c_uint32), ("ar_mode", C.c_uint32), ("t1_ps", C.c_uint64)]
+                ("node_size", C.c_uint32), ("ar_mode", C.c_uint32), ("t1_ps", C.c_uint64),
+                ("n_accum", C.c_uint32), ("_pad", C.c_uint32), ("accum", C.POINTER(C.c_uint32)),
+                ("shard_bytes", C.POINTER(C.c_uint64))]
 
 
 class Cell(C.Structure):
     _fields_ = [("C_lo", C.c_uint64), ("C_hi", C.c_uint64), ("step_ps", C.c_uint64),
                 ("steps", C.c_uint64), ("uepochs", C.c_uint64), ("feasible", C.c_uint32),
-                ("_pad", C.c_uint32)]
+                ("accum", C.c_uint32)]
 
     @property
     def C(self) -> int:
@@ -119,6 +121,7 @@ def lib():
                                      C.c_uint64, C.c_uint64]
         L.or_round_exact.restype = _Best
         L.or_eft_orig.argtypes = [C.c_void_p, C.c_int, P(C.c_uint8)]
+        L.or_shard_bytes.argtypes = [C.c_void_p, C.c_int, P(C.c_uint8), P(C.c_uint64)]
         L.or_mix.argtypes = [C.c_uint64]; L.or_mix.restype = C.c_uint64
         L.or_gen.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint32, P(C.c_uint8),
                              C.c_uint64, P(C.c_uint8)]
@@ -249,6 +252,16 @@ class Dfg:
             raise OracleError(rc)
         return int(out.value)
 
+    def shard_bytes(self, M: int, placement) -> list:
+        """NEXT f4: per-device gradient shard of a placement (descriptor order)."""
+        d = np.ascontiguousarray(np.asarray(placement, dtype=np.uint8))
+        out = np.zeros(8, dtype=np.uint64)
+        rc = lib().or_shard_bytes(self._h, M, d.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                  out.ctypes.data_as(C.POINTER(C.c_uint64)))
+        if rc:
+            raise OracleError(rc)
+        return [int(x) for x in out]
+
     def eft(self, M: int) -> np.ndarray:
         """NEXT f4: the EFT-greedy placement (descriptor order)."""
         d = np.zeros(self.K, dtype=np.uint8)
@@ -332,12 +345,18 @@ class Scenario:
 
     def __init__(self, dataset_items, mini_batch, knot_G, knot_uepochs, grad_bytes, t1_ps,
                  bw_intra_Bps=0, lat_intra_ps=0, bw_inter_Bps=0, lat_inter_ps=0, node_size=8,
-                 ar_mode=0):
+                 ar_mode=0, accum=None, shard_bytes=None):
+        """accum: accumulation factors offered per cell (NEXT f4); shard_bytes:
+        [nM][8] per-device gradient shards of each M's placement, or None."""
         self.kG = _u64(knot_G); self.kE = _u64(knot_uepochs)
+        self.acc = np.ascontiguousarray(np.asarray(accum, dtype=np.uint32)) if accum is not None else None
+        self.sh = _u64(np.asarray(shard_bytes, dtype=np.uint64).reshape(-1)) if shard_bytes is not None else None
         self.s = _Scenario(int(dataset_items), int(mini_batch), len(self.kG),
                            _ptr(self.kG, C.c_uint64), _ptr(self.kE, C.c_uint64), int(grad_bytes),
                            int(bw_intra_Bps), int(lat_intra_ps), int(bw_inter_Bps), int(lat_inter_ps),
-                           int(node_size), int(ar_mode), int(t1_ps))
+                           int(node_size), int(ar_mode), int(t1_ps),
+                           len(self.acc) if self.acc is not None else 0, 0,
+                           _ptr(self.acc, C.c_uint32), _ptr(self.sh, C.c_uint64))
 
     @classmethod
     def from_spec(cls, spec: dict) -> "Scenario":

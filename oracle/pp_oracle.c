@@ -76,7 +76,7 @@ typedef struct {
     int *pi;            /* pi[p]  = original index of the op at π position p */
     int *pos;           /* pos[k] = π position of original op k            */
     /* everything below is indexed by π position */
-    uint64_t *df, *db, *mem;
+    uint64_t *df, *db, *mem, *param;
     /* adjacency lists by π position: in-edges and out-edges */
     int *in_cnt, **in_src;  uint64_t **in_cf;
     int *out_cnt, **out_dst; uint64_t **out_cb;
@@ -126,7 +126,7 @@ void or_free(or_ctx *c) {
     free(c->in_eid); free(c->out_eid); free(c->cfm); free(c->cbm);
     free(c->in_src); free(c->in_cf); free(c->out_dst); free(c->out_cb);
     free(c->in_cnt); free(c->out_cnt);
-    free(c->id); free(c->pi); free(c->pos); free(c->df); free(c->db); free(c->mem);
+    free(c->id); free(c->pi); free(c->pos); free(c->df); free(c->db); free(c->mem); free(c->param);
     free(c);
 }
 
@@ -207,11 +207,13 @@ int or_prepare(const or_input *in, or_ctx **out, char *err, int errlen) {
     c->pos = malloc(sizeof(int) * (size_t)K);
     for (int p = 0; p < K; p++) c->pos[pi[p]] = p;
     c->df = malloc(8 * (size_t)K); c->db = malloc(8 * (size_t)K); c->mem = malloc(8 * (size_t)K);
+    c->param = malloc(8 * (size_t)K);
     for (int p = 0; p < K; p++) {
         int k = pi[p];
         c->df[p] = in->fwd_ps[k];
         c->db[p] = in->bwd_ps[k];
         c->mem[p] = in->mem_bytes ? in->mem_bytes[k] : 0;
+        c->param[p] = in->param_bytes ? in->param_bytes[k] : 0;
     }
     c->cap = in->dev_mem_cap_bytes;
     c->in_cnt = calloc((size_t)K, sizeof(int)); c->out_cnt = calloc((size_t)K, sizeof(int));
@@ -603,6 +605,19 @@ int or_eft_orig(const or_ctx *c, int M, uint8_t *d_orig) {
     return rc;
 }
 
+/* NEXT f4 (reading R24): gradient shard of each device under a placement,
+ * S_d = Σ param_bytes of the ops on device d (descriptor order placement).   */
+int or_shard_bytes(const or_ctx *c, int M, const uint8_t *d_orig, uint64_t *out8) {
+    if (M < 1 || M > 8) return OR_E_INVALID;
+    for (int m = 0; m < 8; m++) out8[m] = 0;
+    for (int p = 0; p < c->K; p++) {
+        int k = c->pi[p];
+        if (d_orig[k] >= M) return OR_E_INVALID;
+        out8[d_orig[k]] += c->param[p];
+    }
+    return OR_OK;
+}
+
 /* ------------------------------------------------------- O5 / O6 generators */
 #define OR_GEN_GRAY 0
 #define OR_GEN_RANDOM 1
@@ -777,9 +792,13 @@ typedef struct {
     uint32_t node_size;                /* 0 => 8 */
     uint32_t ar_mode;                  /* 0 = EQ5 (paper Eq. 5), 1 = TIME */
     uint64_t t1_ps;                    /* T_1 */
+    /* NEXT f4 */
+    uint32_t n_accum, _pad;            /* accumulation factors a per cell; 0 => {1} */
+    const uint32_t *accum;             /* PAPER.md:251 delayed gradient update      */
+    const uint64_t *shard_bytes;       /* [nM][8] per-device gradient shards, or NULL */
 } or_scenario;
 
-typedef struct { uint64_t C_lo, C_hi, step_ps, steps, uepochs; uint32_t feasible, _pad; } or_cell;
+typedef struct { uint64_t C_lo, C_hi, step_ps, steps, uepochs; uint32_t feasible, accum; } or_cell;
 
 static int bitlen128(u128 x) { int n = 0; while (x) { n++; x >>= 1; } return n; }
 
@@ -788,7 +807,7 @@ static int bitlen128(u128 x) { int n = 0; while (x) { n++; x >>= 1; } return n; 
  *   AR(n,S) = 0 if n = 1, else ⌈2(n−1)·S·10^12 / (n·BW)⌉ + 2(n−1)·α,
  *   tier = intra if the cell's device count ≤ node_size else inter;
  *   a tier with BW = 0 is "AR off" (SE ≡ 1).                    */
-int or_ar(const or_scenario *s, uint64_t n, uint64_t n_devices, u128 *out) {
+static int or_ar_S(const or_scenario *s, uint64_t n, uint64_t n_devices, uint64_t S, u128 *out) {
     *out = 0;
     if (n <= 1) return OR_OK;
     uint64_t node = s->node_size ? s->node_size : 8;
@@ -796,12 +815,16 @@ int or_ar(const or_scenario *s, uint64_t n, uint64_t n_devices, u128 *out) {
     uint64_t al = (n_devices <= node) ? s->lat_intra_ps : s->lat_inter_ps;
     if (bw == 0) return OR_OK;
     u128 num = (u128)2 * (n - 1);
-    if (bitlen128(num) + bitlen128(s->grad_bytes) + 40 > 127) return OR_E_RANGE;
-    num = num * s->grad_bytes * (u128)1000000000000ULL;
+    if (bitlen128(num) + bitlen128(S) + 40 > 127) return OR_E_RANGE;
+    num = num * S * (u128)1000000000000ULL;
     u128 den = (u128)n * bw;
     u128 q = num / den + (num % den ? 1 : 0);
     *out = q + (u128)2 * (n - 1) * al;
     return OR_OK;
+}
+
+int or_ar(const or_scenario *s, uint64_t n, uint64_t n_devices, u128 *out) {
+    return or_ar_S(s, n, n_devices, s->grad_bytes, out);
 }
 
 uint64_t or_ar64(const or_scenario *s, uint64_t n, uint64_t n_devices, int *rc) {
@@ -829,6 +852,8 @@ int or_epochs(const or_scenario *s, uint64_t G, uint64_t *E) {
 
 static int validate_scenario(const or_scenario *s) {
     if (s->mini_batch == 0 || s->dataset_items == 0 || s->t1_ps == 0 || s->ar_mode > 1) return OR_E_INVALID;
+    if (s->n_accum > 32 || (s->n_accum && !s->accum)) return OR_E_INVALID;
+    for (uint32_t j = 0; j < s->n_accum; j++) if (s->accum[j] == 0) return OR_E_INVALID;
     if (s->n_knots == 0 || !s->knot_G || !s->knot_uepochs) return OR_E_INVALID;
     for (uint32_t i = 0; i < s->n_knots; i++) {
         if (s->knot_uepochs[i] == 0) return OR_E_INVALID;
@@ -842,36 +867,62 @@ static int validate_scenario(const or_scenario *s) {
 }
 
 /* O10: one cell (M, N).  Eq. 1 C = T×S×E; S = ⌈D/G⌉
- * (reading R14); G = W·B with W = N/M workers;
- * EQ5 (Eq. 5, reading R11): T = ⌊(T_1 + AR(W))·T_M / T_1⌋;
- * TIME: T = T_M + AR(W).  M ∤ N => infeasible (R15).                          */
-int or_cell_compute(const or_scenario *s, uint32_t M, uint64_t T_M, uint32_t N, or_cell *cell) {
+ * (reading R14); G = W·B·a with W = N/M workers
+ * and a mini-batches accumulated per step (NEXT f4, PAPER.md:251 delayed
+ * gradient update; a = 1 unless the scenario offers more);
+ * EQ5 (Eq. 5, reading R11): T = ⌊(a·T_1 + AR(W))·T_M / T_1⌋;
+ * TIME: T = a·T_M + AR(W).  AR(W) all-reduces grad_bytes, or with per-device
+ * shards (NEXT f4, reading R24) the slowest shard: max_d AR(W, S_d).
+ * The cell keeps the a with the smallest C (ties → the earlier a in the list).
+ * M ∤ N => infeasible (R15).                                                  */
+int or_cell_compute_ex(const or_scenario *s, uint32_t M, uint64_t T_M, uint32_t N, const uint64_t *shard,
+                       or_cell *cell) {
     memset(cell, 0, sizeof *cell);
     if (M == 0 || N == 0) return OR_E_INVALID;
     if (N % M != 0) return OR_OK;
     uint64_t W = N / M;
-    u128 G = (u128)W * s->mini_batch;
-    uint64_t E;
-    if (G >> 64) return OR_OK;
-    if (!or_epochs(s, (uint64_t)G, &E)) return OR_OK;
-    u128 A;
-    int rc = or_ar(s, W, N, &A);
-    if (rc) return rc;
-    u128 T;
-    if (s->ar_mode == 0) {
-        u128 a = (u128)s->t1_ps + A;
-        if (bitlen128(a) + bitlen128(T_M) > 127) return OR_E_RANGE;
-        T = a * T_M / s->t1_ps;
+    u128 A = 0;
+    if (shard) {
+        for (uint32_t d = 0; d < M && d < 8; d++) {
+            u128 Ad;
+            int rc = or_ar_S(s, W, N, shard[d], &Ad);
+            if (rc) return rc;
+            if (Ad > A) A = Ad;
+        }
     } else {
-        T = (u128)T_M + A;
+        int rc = or_ar(s, W, N, &A);
+        if (rc) return rc;
     }
-    if (T >> 64) return OR_E_RANGE;
-    uint64_t steps = (uint64_t)((s->dataset_items + (uint64_t)G - 1) / (uint64_t)G);
-    if (bitlen128(T) + bitlen128(steps) + bitlen128(E) > 127) return OR_E_RANGE;
-    u128 C = T * steps * E;
-    cell->C_lo = (uint64_t)C; cell->C_hi = (uint64_t)(C >> 64);
-    cell->step_ps = (uint64_t)T; cell->steps = steps; cell->uepochs = E; cell->feasible = 1;
+    uint32_t na = s->n_accum ? s->n_accum : 1;
+    for (uint32_t j = 0; j < na; j++) {
+        uint64_t a = s->n_accum ? s->accum[j] : 1;
+        u128 G = (u128)W * s->mini_batch * a;
+        uint64_t E;
+        if (G >> 64) continue;
+        if (!or_epochs(s, (uint64_t)G, &E)) continue;
+        u128 T;
+        if (s->ar_mode == 0) {
+            u128 x = (u128)a * s->t1_ps + A;
+            if (bitlen128(x) + bitlen128(T_M) > 127) return OR_E_RANGE;
+            T = x * T_M / s->t1_ps;
+        } else {
+            T = (u128)a * T_M + A;
+        }
+        if (T >> 64) return OR_E_RANGE;
+        uint64_t steps = (uint64_t)((s->dataset_items + (uint64_t)G - 1) / (uint64_t)G);
+        if (bitlen128(T) + bitlen128(steps) + bitlen128(E) > 127) return OR_E_RANGE;
+        u128 C = T * steps * E;
+        if (!cell->feasible || C < (((u128)cell->C_hi << 64) | cell->C_lo)) {
+            cell->C_lo = (uint64_t)C; cell->C_hi = (uint64_t)(C >> 64);
+            cell->step_ps = (uint64_t)T; cell->steps = steps; cell->uepochs = E; cell->feasible = 1;
+            cell->accum = (uint32_t)a;
+        }
+    }
     return OR_OK;
+}
+
+int or_cell_compute(const or_scenario *s, uint32_t M, uint64_t T_M, uint32_t N, or_cell *cell) {
+    return or_cell_compute_ex(s, M, T_M, N, NULL, cell);
 }
 
 /* cells[m*N_max + (N-1)] */
@@ -883,7 +934,8 @@ int or_project(const or_scenario *s, int nM, const uint32_t *Ms, const uint64_t 
     for (int m = 0; m < nM; m++) if (Ms[m] == 0 || T_M[m] == 0) return OR_E_INVALID;
     for (int m = 0; m < nM; m++)
         for (uint32_t N = 1; N <= N_max; N++) {
-            rc = or_cell_compute(s, Ms[m], T_M[m], N, &cells[(size_t)m * N_max + (N - 1)]);
+            rc = or_cell_compute_ex(s, Ms[m], T_M[m], N, s->shard_bytes ? s->shard_bytes + 8 * (size_t)m : NULL,
+                                    &cells[(size_t)m * N_max + (N - 1)]);
             if (rc) return rc;
         }
     return OR_OK;

@@ -476,6 +476,20 @@ int pp_search_exact(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
                      stream);
 }
 
+// ------------------------------------- placement-aware AR shards (NEXT f4)
+int pp_shard_bytes(const pp_dfg *g, int M, const uint8_t *placement, uint64_t *out) {
+    if (!g || M < 1 || M > 8 || !placement || !out) {
+        set_error("invalid arguments");
+        return PP_E_INVALID;
+    }
+    for (int d = 0; d < 8; d++) out[d] = 0;
+    for (int k = 0; k < g->K; k++) {
+        if (placement[k] >= M) { set_error("placement value >= M"); return PP_E_INVALID; }
+        out[placement[k]] += g->param[k];
+    }
+    return PP_OK;
+}
+
 // ------------------------------------------------- EFT base seed (NEXT f4)
 int pp_eft_place(const pp_dfg *g, int M, uint8_t *placement, void *stream) {
     if (!g || M < 1 || M > 8 || (g->hw && M > g->nd) || !placement) {

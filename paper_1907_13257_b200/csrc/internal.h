@@ -235,6 +235,7 @@ struct pp_dfg {
     uint64_t t1 = 0, grad_bytes = 0, cap = 0;
     std::vector<int32_t> pi;     // π position → descriptor index
     std::vector<int32_t> pos;    // descriptor index → π position
+    std::vector<uint64_t> param; // param_bytes by descriptor index
     std::vector<uint8_t> image;  // host copy of the image
     uint32_t off_extra = 0, off_mem = 0, off_orig = 0, image_bytes = 0;
     uint32_t base_bytes = 0;     // K rounded up to 16

@@ -378,6 +378,9 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     g->nd = nd;
     g->off_cls = (uint32_t)off_cls;
     g->grad_bytes = 0;
+    g->param.assign(K, 0);
+    if (d->param_bytes)
+        for (int k = 0; k < K; k++) g->param[k] = d->param_bytes[k];
     if (d->param_bytes)
         for (int k = 0; k < K; k++) g->grad_bytes += d->param_bytes[k];
     g->pi = pi;

@@ -8,6 +8,8 @@
 //           tier = intra iff N ≤ node_size
 //   T = ⌊(T_1 + AR)·T_M / T_1⌋ (EQ5 = SU^M·SE_W, Eq. 5)
 //       or T_M + AR (TIME)
+//   NEXT f4: accumulation factors a (G = W·B·a, T = ⌊(a·T_1 + AR)·T_M/T_1⌋ or
+//   a·T_M + AR, the least-C a kept) and per-device shards (AR = max_d AR(S_d))
 //   steps = ⌈D/G⌉, C = T·steps·E (Eq. 1)
 // Crossover (Eq. 6, strict; R16).
 #include <cuda_runtime.h>
@@ -23,14 +25,17 @@ namespace pp {
 typedef unsigned __int128 u128;
 
 constexpr int kMaxKnots = 64;
+constexpr int kMaxAccum = 32;
 
 struct ProjParams {
     uint64_t D, grad, bw_in, lat_in, bw_out, lat_out, t1;
     uint32_t B, n_knots, node, mode;
-    uint32_t nM, N_max;
+    uint32_t nM, N_max, nA, sharded;
     uint32_t Ms[8];
     uint64_t TM[8];
     uint64_t kG[kMaxKnots], kE[kMaxKnots];
+    uint32_t A[kMaxAccum];           // accumulation factors (NEXT f4)
+    uint64_t shard[8][8];            // per-M per-device gradient shards
 };
 
 __device__ __forceinline__ int bitlen(u128 x) {
@@ -38,59 +43,84 @@ __device__ __forceinline__ int bitlen(u128 x) {
     return hi ? 128 - __clzll((long long)hi) : (lo ? 64 - __clzll((long long)lo) : 0);
 }
 
-// returns 0 = ok, 1 = infeasible handled via *feasible, -3 = range
-__device__ int cell_value(const ProjParams &P, uint32_t M, uint64_t TM, uint32_t N, pp_cell &c) {
+// ring all-reduce of S bytes over W workers in the tier of N devices
+__device__ int ring_ar(const ProjParams &P, uint64_t W, uint32_t N, uint64_t S, u128 &A) {
+    A = 0;
+    if (W <= 1) return 0;
+    const bool intra = N <= P.node;
+    const uint64_t bw = intra ? P.bw_in : P.bw_out;
+    const uint64_t al = intra ? P.lat_in : P.lat_out;
+    if (!bw) return 0;
+    const u128 steps2 = (u128)2 * (W - 1);
+    if (bitlen(steps2) + bitlen(S) + 40 > 127) return -3;
+    const u128 num = steps2 * S * (u128)1000000000000ull;
+    const u128 den = (u128)W * bw;
+    A = num / den + ((num % den) ? 1 : 0) + steps2 * al;
+    return 0;
+}
+
+// E(G) from the knots; false outside them
+__device__ bool epochs_of(const ProjParams &P, uint64_t g, uint64_t &E) {
+    if (g < P.kG[0] || g > P.kG[P.n_knots - 1]) return false;
+    for (uint32_t i = 0; i < P.n_knots; i++) {
+        if (P.kG[i] == g) { E = P.kE[i]; return true; }
+        if (i + 1 < P.n_knots && P.kG[i] < g && g < P.kG[i + 1]) {
+            u128 num = (u128)P.kE[i] * (P.kG[i + 1] - g) + (u128)P.kE[i + 1] * (g - P.kG[i]);
+            E = (uint64_t)(num / (P.kG[i + 1] - P.kG[i]));
+            return true;
+        }
+    }
+    return false;
+}
+
+// returns 0 = ok (infeasible cells have feasible = 0), -3 = range
+__device__ int cell_value(const ProjParams &P, uint32_t m, uint32_t N, pp_cell &c) {
+    const uint32_t M = P.Ms[m];
+    const uint64_t TM = P.TM[m];
     c = pp_cell{0, 0, 0, 0, 0, 0, 0};
     if (N % M) return 0;
     const uint64_t W = N / M;
-    const u128 G = (u128)W * P.B;
-    if (G >> 64) return 0;
-    const uint64_t g = (uint64_t)G;
-    // E(G)
-    if (g < P.kG[0] || g > P.kG[P.n_knots - 1]) return 0;
-    uint64_t E = 0;
-    bool found = false;
-    for (uint32_t i = 0; i < P.n_knots && !found; i++) {
-        if (P.kG[i] == g) { E = P.kE[i]; found = true; }
-        else if (i + 1 < P.n_knots && P.kG[i] < g && g < P.kG[i + 1]) {
-            u128 num = (u128)P.kE[i] * (P.kG[i + 1] - g) + (u128)P.kE[i + 1] * (g - P.kG[i]);
-            E = (uint64_t)(num / (P.kG[i + 1] - P.kG[i]));
-            found = true;
-        }
-    }
-    if (!found) return 0;
-    // ring all-reduce
     u128 A = 0;
-    if (W > 1) {
-        const bool intra = N <= P.node;
-        const uint64_t bw = intra ? P.bw_in : P.bw_out;
-        const uint64_t al = intra ? P.lat_in : P.lat_out;
-        if (bw) {
-            const u128 steps2 = (u128)2 * (W - 1);
-            if (bitlen(steps2) + bitlen(P.grad) + 40 > 127) return -3;
-            const u128 num = steps2 * P.grad * (u128)1000000000000ull;
-            const u128 den = (u128)W * bw;
-            A = num / den + ((num % den) ? 1 : 0) + steps2 * al;
+    if (P.sharded) {   // placement-aware: the slowest device's shard (R24)
+        for (uint32_t d = 0; d < M && d < 8; d++) {
+            u128 Ad;
+            if (ring_ar(P, W, N, P.shard[m][d], Ad)) return -3;
+            A = Ad > A ? Ad : A;
+        }
+    } else if (ring_ar(P, W, N, P.grad, A)) {
+        return -3;
+    }
+    u128 best = 0;
+    for (uint32_t j = 0; j < P.nA; j++) {
+        const uint64_t a = P.A[j];
+        const u128 G = (u128)W * P.B * a;
+        if (G >> 64) continue;
+        const uint64_t g = (uint64_t)G;
+        uint64_t E;
+        if (!epochs_of(P, g, E)) continue;
+        u128 T;
+        if (P.mode == 0) {
+            const u128 x = (u128)a * P.t1 + A;
+            if (bitlen(x) + bitlen(TM) > 127) return -3;
+            T = x * TM / P.t1;
+        } else {
+            T = (u128)a * TM + A;
+        }
+        if (T >> 64) return -3;
+        const uint64_t steps = (P.D + g - 1) / g;
+        if (bitlen(T) + bitlen(steps) + bitlen(E) > 127) return -3;
+        const u128 C = T * steps * E;
+        if (!c.feasible || C < best) {
+            best = C;
+            c.C_lo = (uint64_t)C;
+            c.C_hi = (uint64_t)(C >> 64);
+            c.step_ps = (uint64_t)T;
+            c.steps = steps;
+            c.uepochs = E;
+            c.feasible = 1;
+            c.accum = (uint32_t)a;
         }
     }
-    u128 T;
-    if (P.mode == 0) {
-        const u128 a = (u128)P.t1 + A;
-        if (bitlen(a) + bitlen(TM) > 127) return -3;
-        T = a * TM / P.t1;
-    } else {
-        T = (u128)TM + A;
-    }
-    if (T >> 64) return -3;
-    const uint64_t steps = (P.D + g - 1) / g;
-    if (bitlen(T) + bitlen(steps) + bitlen(E) > 127) return -3;
-    const u128 C = T * steps * E;
-    c.C_lo = (uint64_t)C;
-    c.C_hi = (uint64_t)(C >> 64);
-    c.step_ps = (uint64_t)T;
-    c.steps = steps;
-    c.uepochs = E;
-    c.feasible = 1;
     return 0;
 }
 
@@ -99,7 +129,7 @@ __global__ void project_kernel(const ProjParams P, pp_cell *cells, int *err) {
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
         const uint32_t m = t / P.N_max, N = t % P.N_max + 1;
         pp_cell c;
-        int rc = cell_value(P, P.Ms[m], P.TM[m], N, c);
+        int rc = cell_value(P, m, N, c);
         if (rc) atomicMin(err, rc);
         cells[t] = c;
     }
@@ -342,6 +372,18 @@ extern "C" int pp_project_e2e(const pp_scenario *sc, int nM, const uint32_t *Ms,
     P.mode = sc->ar_mode;
     P.nM = (uint32_t)nM;
     P.N_max = N_max;
+    if (sc->n_accum > kMaxAccum || (sc->n_accum && !sc->accum))
+        return proj_fail(PP_E_INVALID, "n_accum in [0,32] with a host array");
+    P.nA = sc->n_accum ? sc->n_accum : 1;
+    P.A[0] = 1;
+    for (uint32_t j = 0; j < sc->n_accum; j++) {
+        if (sc->accum[j] == 0) return proj_fail(PP_E_INVALID, "accumulation factors must be >= 1");
+        P.A[j] = sc->accum[j];
+    }
+    P.sharded = sc->shard_bytes != nullptr;
+    if (P.sharded)
+        for (int m = 0; m < nM; m++)
+            for (int d = 0; d < 8; d++) P.shard[m][d] = sc->shard_bytes[8 * m + d];
     Scratch *s = nullptr;
     int rc = scratch(&s);
     if (rc) return rc;

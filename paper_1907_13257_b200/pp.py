@@ -70,12 +70,13 @@ class Scenario(C.Structure):
                 ("knot_G", P(C.c_uint64)), ("knot_uepochs", P(C.c_uint64)), ("grad_bytes", C.c_uint64),
                 ("bw_intra_Bps", C.c_uint64), ("lat_intra_ps", C.c_uint64), ("bw_inter_Bps", C.c_uint64),
                 ("lat_inter_ps", C.c_uint64), ("node_size", C.c_uint32), ("ar_mode", C.c_uint32),
-                ("t1_ps", C.c_uint64)]
+                ("t1_ps", C.c_uint64), ("n_accum", C.c_uint32), ("_pad", C.c_uint32),
+                ("accum", P(C.c_uint32)), ("shard_bytes", P(C.c_uint64))]
 
 
 class Cell(C.Structure):
     _fields_ = [("C_lo", C.c_uint64), ("C_hi", C.c_uint64), ("step_ps", C.c_uint64), ("steps", C.c_uint64),
-                ("uepochs", C.c_uint64), ("feasible", C.c_uint32), ("_pad", C.c_uint32)]
+                ("uepochs", C.c_uint64), ("feasible", C.c_uint32), ("accum", C.c_uint32)]
 
 
 CELL_BYTES = C.sizeof(Cell)   # 48
@@ -105,6 +106,7 @@ SIGNATURES = {
                                  C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "pp_search_exact": ([C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint64,
                          C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
+    "pp_shard_bytes": ([C.c_void_p, C.c_int, P(C.c_uint8), P(C.c_uint64)], C.c_int),
     "pp_eft_place": ([C.c_void_p, C.c_int, P(C.c_uint8), C.c_void_p], C.c_int),
     "pp_search_best": ([C.c_void_p, C.c_int, P(SearchDesc), C.c_void_p, C.c_void_p, P(SearchResultC)], C.c_int),
     "pp_comm_get_unique_id": ([P(C.c_uint8)], C.c_int),
@@ -287,6 +289,13 @@ class Dfg:
                                      _stream(stream)))
         return out
 
+    def shard_bytes(self, M, placement) -> list:
+        """Per-device gradient shard S_d of a placement (descriptor order)."""
+        pl = np.ascontiguousarray(np.asarray(placement, dtype=np.uint8))
+        out = np.zeros(8, dtype=np.uint64)
+        _check(lib().pp_shard_bytes(self._h, M, _ptr(pl, C.c_uint8), _ptr(out, C.c_uint64)))
+        return [int(x) for x in out]
+
     def eft_place(self, M, stream=None) -> np.ndarray:
         """EFT-greedy placement (descriptor order), computed on the GPU."""
         pl = np.zeros(self.K, dtype=np.uint8)
@@ -415,12 +424,17 @@ def get_kernel_timing():
 # ------------------------------------------------------------ projection
 def _scenario(spec):
     kG, kE = _u64(spec["knot_G"]), _u64(spec["knot_uepochs"])
+    acc = spec.get("accum")
+    acc = np.ascontiguousarray(np.asarray(acc, dtype=np.uint32)) if acc is not None else None
+    sh = spec.get("shard_bytes")
+    sh = _u64(np.asarray(sh, dtype=np.uint64).reshape(-1)) if sh is not None else None
     s = Scenario(int(spec["dataset_items"]), int(spec["mini_batch"]), len(kG), _ptr(kG, C.c_uint64),
                  _ptr(kE, C.c_uint64), int(spec.get("grad_bytes", 0)), int(spec.get("bw_intra_Bps", 0)),
                  int(spec.get("lat_intra_ps", 0)), int(spec.get("bw_inter_Bps", 0)),
                  int(spec.get("lat_inter_ps", 0)), int(spec.get("node_size", 8)), int(spec.get("ar_mode", 0)),
-                 int(spec["t1_ps"]))
-    return s, (kG, kE)
+                 int(spec["t1_ps"]), len(acc) if acc is not None else 0, 0, _ptr(acc, C.c_uint32),
+                 _ptr(sh, C.c_uint64))
+    return s, (kG, kE, acc, sh)
 
 
 def project_e2e(spec, Ms, T_M, N_max, cells=None, device=0, stream=None):
@@ -462,7 +476,7 @@ def crossover(cells, Ms, N_max, best_m=True, stream=None):
 def cells_to_numpy(cells) -> np.ndarray:
     """pp_cell records → structured numpy array (host copy)."""
     dt = np.dtype([("C_lo", "<u8"), ("C_hi", "<u8"), ("step_ps", "<u8"), ("steps", "<u8"),
-                   ("uepochs", "<u8"), ("feasible", "<u4"), ("_pad", "<u4")])
+                   ("uepochs", "<u8"), ("feasible", "<u4"), ("accum", "<u4")])
     raw = cells.cpu().numpy().reshape(-1, CELL_BYTES)
     return raw.view(dt).reshape(cells.shape[0], cells.shape[1])
 

@@ -25,7 +25,8 @@ def _compare(sc, Ms, TM, Nmax):
         for N in range(1, Nmax + 1):
             c, o = got[m, N - 1], oc[m * Nmax + N - 1]
             assert (int(c["C_lo"]), int(c["C_hi"]), int(c["step_ps"]), int(c["steps"]), int(c["uepochs"]),
-                    int(c["feasible"])) == (o.C_lo, o.C_hi, o.step_ps, o.steps, o.uepochs, o.feasible), (m, N)
+                    int(c["feasible"]), int(c["accum"])) == \
+                   (o.C_lo, o.C_hi, o.step_ps, o.steps, o.uepochs, o.feasible, o.accum), (m, N)
     if 1 in Ms:
         x = pp.crossover(cells, Ms, Nmax)
         ox = O.crossover(oc, Ms, Nmax)
@@ -79,3 +80,20 @@ def test_projection_errors_match():
     with pytest.raises(O.OracleError) as e2:
         O.Scenario.from_spec(big).project([1], [2**63], 4)
     assert e2.value.code == -3
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("model", ["inception_v3", "gnmt", "biglstm"])
+def test_accumulation_axis_and_shards(model, mode):
+    # a ∈ {1, 2, 4, 8, 16} per cell and placement-aware
+    # all-reduce shards from the EFT placements of the paper-shaped DFG
+    spec = getattr(synth, model)()
+    g = pp.Dfg(spec)
+    Ms = [1, 2, 4, 8]
+    shards = [[g.grad_bytes] + [0] * 7] + [g.shard_bytes(M, g.eft_place(M)) for M in Ms[1:]]
+    assert all(sum(r) == g.grad_bytes for r in shards)
+    t1 = g.t1
+    sc = synth.sweep_scenario(model, t1, g.grad_bytes, ar_mode=mode)
+    sc = dict(sc, accum=[1, 2, 4, 8, 16], shard_bytes=shards)
+    x = _compare(sc, Ms, [t1, t1 * 3 // 4, t1 * 2 // 3, t1 * 3 // 5], 1024)
+    assert x is not None
