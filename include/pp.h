@@ -213,6 +213,37 @@ int pp_search_exact(const pp_dfg *dfg, int M, int gen, uint64_t seed_r, uint32_t
                     const uint8_t *d_base_pi, uint64_t begin, uint64_t end, uint64_t node_limit,
                     uint64_t *d_best, void *cuda_stream);
 
+/* ----------------------------------- pipeline-parallel MP (§8(f) f3) --
+ * GPipe-style pipelining (§2; §4.4: how GNMT and
+ * BigLSTM were split).  Reading R26: M stages are contiguous
+ * π ranges [cut_s, cut_{s+1}) on devices 0..M−1; a mini-batch is split into m
+ * micro-batches, stage times ⌈ΣΔ/m⌉; the activations of a micro-batch from
+ * stage a to b travel as one transfer ⌈D_ab·10^12/(m·BW)⌉ + L (uniform link);
+ * forward micro-batches in order, then the backward in reverse order; the
+ * makespan is the last stage's finish.  Candidates: index = rank·nm + j, rank
+ * = lexicographic rank of the cut vector (C(K−1, M−1) of them), j indexes
+ * micro[] (nm ≤ 16).  Needs K ≤ 1024 and a uniform-link pp_dfg.            */
+typedef struct {
+    uint64_t makespan_ps;        /* T_M of the best pipeline (SU = T_1 / T_M)   */
+    uint64_t index;              /* its candidate index                         */
+    uint64_t candidates;         /* C(K−1, M−1)·nm                              */
+    uint32_t micro_batches, n_stages;
+    int32_t  cuts[8];            /* first π position of stages 1..M−1          */
+} pp_pipeline_result;
+
+/* *count = C(K−1, M−1)·nm (PP_E_TOO_LARGE if ≥ 2^63). */
+int pp_pipeline_space(const pp_dfg *dfg, int M, int nm, uint64_t *count);
+/* Candidates [begin, end): d_best (device ptr uint64[2] = {makespan, index},
+ * lexicographic argmin) and/or d_makespan (device ptr uint64 [end−begin]).
+ * micro: host ptr uint32 [nm].  Asynchronous.                               */
+int pp_pipeline_range(const pp_dfg *dfg, int M, const uint32_t *micro, int nm, uint64_t begin, uint64_t end,
+                      uint64_t *d_best, uint64_t *d_makespan, void *cuda_stream);
+/* The whole space; fills *out (host ptr) with the winner's cuts.
+ * Synchronises cuda_stream.  PP_E_INFEASIBLE if every stage split violates
+ * the memory cap.                                                           */
+int pp_pipeline_search(const pp_dfg *dfg, int M, const uint32_t *micro, int nm, void *cuda_stream,
+                       pp_pipeline_result *out);
+
 /* ----------------------------------------- EFT base seed (§8(f) f4) --
  * The earliest-finish-time greedy placement (SPEC.md:245–253
  * heuristic_place; reading R23): forward ops in π order, each

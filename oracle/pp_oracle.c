@@ -32,6 +32,8 @@
  *   or_eft                     pinned (SPEC heuristic_place examples, closed
  *                              forms: round-robin of equal independent ops,
  *                              chain kept whole, diamond → (0,0,1,1))
+ *   or_pipeline(_search)       pinned (GPipe bubble closed form, M = 1,
+ *                              discrete-event simulation, exhaustive brute)
  *   or_exact / or_round_exact  pinned (SPEC exact_schedule examples, a hand
  *                              case where in-order issue loses, brute force
  *                              over per-device orders, exact ≤ in-order)
@@ -86,6 +88,10 @@ typedef struct {
     /* general hardware graph (NEXT f2): per-edge cost for every ordered
      * device pair, cfm[(eid·nd + a)·nd + b]; adjacency lists carry edge ids */
     int nd;                 /* 0 = one uniform hop (R4) */
+    /* pipeline MP (NEXT f3): edges by π position, bytes, the uniform link */
+    int *e_src, *e_dst;
+    uint64_t *e_bf, *e_bb;
+    uint64_t link_bw, link_lat;
     int **in_eid, **out_eid;
     uint64_t *cfm, *cbm;
 } or_ctx;
@@ -98,6 +104,8 @@ typedef struct {
     const uint64_t *link_bw_Bps, *link_lat_ps;
     uint64_t dev_mem_cap_bytes;
 } or_hw;
+
+typedef struct { uint64_t makespan, index; } or_best;   /* an argmin (O7) */
 
 static void set_err(char *err, int errlen, const char *msg) {
     if (err && errlen > 0) { strncpy(err, msg, (size_t)errlen - 1); err[errlen - 1] = 0; }
@@ -125,6 +133,7 @@ void or_free(or_ctx *c) {
     if (c->in_eid) for (int p = 0; p < c->K; p++) { free(c->in_eid[p]); free(c->out_eid[p]); }
     free(c->in_eid); free(c->out_eid); free(c->cfm); free(c->cbm);
     free(c->in_src); free(c->in_cf); free(c->out_dst); free(c->out_cb);
+    free(c->e_src); free(c->e_dst); free(c->e_bf); free(c->e_bb);
     free(c->in_cnt); free(c->out_cnt);
     free(c->id); free(c->pi); free(c->pos); free(c->df); free(c->db); free(c->mem); free(c->param);
     free(c);
@@ -230,10 +239,14 @@ int or_prepare(const or_input *in, or_ctx **out, char *err, int errlen) {
     /* O3 edge costs, and the R3/range bound: Σ(Δf+Δb) + Σ(c_f+c_b) < 2^61 */
     u128 bound = 0;
     int ovf = 0;
+    c->e_src = malloc(sizeof(int) * (size_t)(E + 1)); c->e_dst = malloc(sizeof(int) * (size_t)(E + 1));
+    c->e_bf = malloc(8 * (size_t)(E + 1)); c->e_bb = malloc(8 * (size_t)(E + 1));
+    c->link_bw = in->link_bw_Bps; c->link_lat = in->link_lat_ps;
     for (int e = 0; e < E; e++) {
         int u = c->pos[in->edge_src[e]], v = c->pos[in->edge_dst[e]];
         uint64_t bf = in->edge_fwd_bytes[e];
         uint64_t bb = in->edge_bwd_bytes ? in->edge_bwd_bytes[e] : bf;
+        c->e_src[e] = u; c->e_dst[e] = v; c->e_bf[e] = bf; c->e_bb[e] = bb;
         uint64_t cf = or_edge_cost(bf, in->link_bw_Bps, in->link_lat_ps, &ovf);
         uint64_t cb = or_edge_cost(bb, in->link_bw_Bps, in->link_lat_ps, &ovf);
         c->in_src[v][c->in_cnt[v]] = u; c->in_cf[v][c->in_cnt[v]] = cf; c->in_cnt[v]++;
@@ -618,6 +631,138 @@ int or_shard_bytes(const or_ctx *c, int M, const uint8_t *d_orig, uint64_t *out8
     return OR_OK;
 }
 
+/* ------------------------------------------ NEXT f3: pipeline-parallel MP */
+/* GPipe-style pipelining (§2: "Networks are partitioned into
+ * groups containing one or a few layers of the network, where each group is
+ * placed on a different device ... a mini-batch is split into yet smaller
+ * micro-batches and each device processes a different micro-batch
+ * sequentially but concurrently"; §4.4: GNMT and BigLSTM are
+ * split by pipelining).  Reading R26:
+ *   stage s = π positions [cut_s, cut_{s+1}), cut_0 = 0 < cut_1 < … < cut_M = K,
+ *     on device s (π is topological, so every edge goes to the same or a
+ *     later stage);
+ *   per micro-batch: tf_s = ⌈Σ_{p∈s} Δf(p) / m⌉, tb_s = ⌈Σ Δb / m⌉;
+ *   a → b (a < b) carries the micro-batch's activations of every edge from a
+ *     to b as one transfer of ⌈D_ab·10^12 / (m·BW)⌉ + L ps (D_ab = Σ D_f), the
+ *     gradients back from b to a likewise with Σ D_b; no edge, no transfer;
+ *   forward, micro-batches j = 0..m−1 in order:
+ *     F[s][j] = max(F[s][j−1], max_{a<s} F[a][j] + cf(a,s)) + tf_s
+ *   backward after the forward flush, micro-batches in reverse order:
+ *     B[s][j] = max(B[s][j+1], max_{b>s} B[b][j] + cb(b,s)) + tb_s,
+ *     B[s][m] := F[s][m−1]   (each device runs its ops one at a time)
+ *   makespan = max_s B[s][0]; a stage whose Σ M(k) exceeds the cap makes the
+ *   pipeline infeasible.                                 */
+uint64_t or_pipeline(const or_ctx *c, int M, const int32_t *cuts, uint32_t m) {
+    int K = c->K;
+    if (M < 1 || M > 8 || M > K || m < 1 || m > 65536 || c->nd) return OR_INFEASIBLE_MAKESPAN;  /* invalid */
+    for (int s = 0; s < M - 1; s++)
+        if (cuts[s] < 1 || cuts[s] > K - 1 || (s > 0 && cuts[s] <= cuts[s - 1])) return OR_INFEASIBLE_MAKESPAN;
+    int st[9];
+    st[0] = 0; st[M] = K;
+    for (int s = 1; s < M; s++) st[s] = cuts[s - 1];
+    int *stage_of = malloc(sizeof(int) * (size_t)K);
+    for (int s = 0; s < M; s++) for (int p = st[s]; p < st[s + 1]; p++) stage_of[p] = s;
+    uint64_t tf[8], tb[8];
+    for (int s = 0; s < M; s++) {
+        u128 sf = 0, sb = 0, mem = 0;
+        for (int p = st[s]; p < st[s + 1]; p++) { sf += c->df[p]; sb += c->db[p]; mem += c->mem[p]; }
+        if (c->cap > 0 && mem > c->cap) { free(stage_of); return OR_INFEASIBLE_MAKESPAN; }
+        tf[s] = (uint64_t)((sf + m - 1) / m);
+        tb[s] = (uint64_t)((sb + m - 1) / m);
+    }
+    u128 Df[8][8], Db[8][8];
+    int has[8][8];
+    memset(Df, 0, sizeof Df); memset(Db, 0, sizeof Db); memset(has, 0, sizeof has);
+    for (int e = 0; e < c->E; e++) {
+        int a = stage_of[c->e_src[e]], b = stage_of[c->e_dst[e]];
+        if (a == b) continue;
+        Df[a][b] += c->e_bf[e]; Db[a][b] += c->e_bb[e]; has[a][b] = 1;
+    }
+    free(stage_of);
+    uint64_t cf[8][8], cb[8][8];
+    for (int a = 0; a < M; a++)
+        for (int b = 0; b < M; b++) {
+            u128 den = (u128)m * c->link_bw;
+            cf[a][b] = has[a][b] ? (uint64_t)((Df[a][b] * 1000000000000ULL + den - 1) / den) + c->link_lat : 0;
+            cb[a][b] = has[a][b] ? (uint64_t)((Db[a][b] * 1000000000000ULL + den - 1) / den) + c->link_lat : 0;
+        }
+    uint64_t *F = calloc((size_t)M * m, 8), *B = calloc((size_t)M * m, 8);
+#define FF(s, j) F[(size_t)(s) * m + (j)]
+#define BB(s, j) B[(size_t)(s) * m + (j)]
+    for (uint32_t j = 0; j < m; j++)
+        for (int s = 0; s < M; s++) {
+            uint64_t r = j > 0 ? FF(s, j - 1) : 0;
+            for (int a = 0; a < s; a++)
+                if (has[a][s] && FF(a, j) + cf[a][s] > r) r = FF(a, j) + cf[a][s];
+            FF(s, j) = r + tf[s];
+        }
+    for (int64_t j = (int64_t)m - 1; j >= 0; j--)
+        for (int s = M - 1; s >= 0; s--) {
+            uint64_t r = (j == (int64_t)m - 1) ? FF(s, m - 1) : BB(s, j + 1);
+            for (int b = s + 1; b < M; b++)
+                if (has[s][b] && BB(b, j) + cb[s][b] > r) r = BB(b, j) + cb[s][b];
+            BB(s, j) = r + tb[s];
+        }
+    uint64_t mk = 0;
+    for (int s = 0; s < M; s++) if (BB(s, 0) > mk) mk = BB(s, 0);
+#undef FF
+#undef BB
+    free(F); free(B);
+    return mk;
+}
+
+/* Exhaustive pipeline search: cut vectors in lexicographic order (rank r),
+ * micro-batch counts micro[0..nm−1]; candidate index = r·nm + j.  Returns the
+ * lexicographically smallest (makespan, index) over [begin, end).            */
+or_best or_pipeline_search(const or_ctx *c, int M, const uint32_t *micro, int nm,
+                           uint64_t begin, uint64_t end) {
+    or_best best = { UINT64_MAX, UINT64_MAX };
+    if (M < 1 || M > 8 || M > c->K || nm < 1) return best;
+    /* start at the first rank touching [begin, end): unrank it (combinatorial
+     * number system, lexicographic order of cut vectors from {1..K−1})      */
+    uint64_t r = begin / (uint64_t)nm;
+    int cuts[8];
+    {
+        u128 rank = r;
+        int x = 1;
+        for (int i = 0; i < M - 1; i++) {
+            for (;;) {
+                /* combinations with cuts[i] = x: choose the remaining M−2−i cuts
+                 * from {x+1..K−1} */
+                u128 cnt = 1;
+                int n = c->K - 1 - x, k = M - 2 - i;
+                if (k > n) cnt = 0;
+                else for (int t = 1; t <= k; t++) cnt = cnt * (u128)(n - k + t) / (u128)t;
+                if (rank < cnt) break;
+                rank -= cnt;
+                x++;
+                if (x > c->K - 1) return best;       /* beyond the last combination */
+            }
+            cuts[i] = x++;
+        }
+    }
+    for (;;) {
+        for (int j = 0; j < nm; j++) {
+            uint64_t idx = r * (uint64_t)nm + (uint64_t)j;
+            if (idx >= begin && idx < end) {
+                uint64_t mk = or_pipeline(c, M, cuts, micro[j]);
+                if (mk < best.makespan || (mk == best.makespan && idx < best.index)) {
+                    best.makespan = mk; best.index = idx;
+                }
+            }
+        }
+        /* next combination of M−1 cuts from {1..K−1} */
+        int i = M - 2;
+        while (i >= 0 && cuts[i] == c->K - 1 - (M - 2 - i)) i--;
+        if (i < 0) break;
+        cuts[i]++;
+        for (int t = i + 1; t < M - 1; t++) cuts[t] = cuts[t - 1] + 1;
+        r++;
+        if (r * (uint64_t)nm >= end) break;
+    }
+    return best;
+}
+
 /* ------------------------------------------------------- O5 / O6 generators */
 #define OR_GEN_GRAY 0
 #define OR_GEN_RANDOM 1
@@ -694,7 +839,6 @@ void or_gen(int K, int M, int gen, uint64_t seed_r, uint32_t tau,
 
 /* O7 (one round): lexicographic min of (makespan, i) over candidates
  * i ∈ [begin, end) with seed_r and base (π order).                         */
-typedef struct { uint64_t makespan, index; } or_best;
 
 or_best or_round(const or_ctx *c, int M, int gen, uint64_t seed_r, uint32_t tau,
                  const uint8_t *base, uint64_t begin, uint64_t end) {

@@ -41,6 +41,7 @@ def _sources():
         jobs.append(("search_inst.cu", f"search_m{m}.o", [f"-DPP_M={m}"]))
     jobs.append(("projection.cu", "projection.o", []))
     jobs.append(("eft.cu", "eft.o", []))
+    jobs.append(("pipeline.cu", "pipeline.o", []))
     jobs.append(("loader.cpp", "loader.o", []))
     jobs.append(("capi.cpp", "capi.o", ["-I", _nccl_include()]))
     return jobs

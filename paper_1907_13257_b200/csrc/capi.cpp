@@ -476,6 +476,166 @@ int pp_search_exact(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
                      stream);
 }
 
+// ------------------------------------------- pipeline-parallel MP (NEXT f3)
+static uint64_t binom_sat(uint64_t n, uint64_t k) {   // C(n, k) saturating at 2^63
+    if (k > n) return 0;
+    unsigned __int128 c = 1;
+    for (uint64_t i = 1; i <= k; i++) {
+        c = c * (n - k + i) / i;
+        if (c >= ((unsigned __int128)1 << 63)) return 1ull << 63;
+    }
+    return (uint64_t)c;
+}
+
+static int pipe_check(const pp_dfg *g, int M, const uint32_t *micro, int nm) {
+    if (!g || M < 1 || M > 8 || !micro || nm < 1 || nm > 16) {
+        set_error("M in [1,8], 1..16 micro-batch counts");
+        return PP_E_INVALID;
+    }
+    if (g->hw) { set_error("pipeline evaluation uses the uniform link (not a hardware graph)"); return PP_E_INVALID; }
+    if (M > g->K) { set_error("more stages than ops"); return PP_E_INVALID; }
+    if (g->K > kMaxPipelineK) { set_error("pipeline evaluation supports K <= 1024"); return PP_E_TOO_LARGE; }
+    for (int j = 0; j < nm; j++)
+        if (micro[j] < 1 || micro[j] > 65536) { set_error("micro-batch counts in [1,65536]"); return PP_E_INVALID; }
+    return PP_OK;
+}
+
+static int pipe_tables(pp_dfg *g) {
+    if (g->d_pipe) return PP_OK;
+    const uint64_t K1 = (uint64_t)g->K + 1;
+    std::vector<uint64_t> h(3 * K1 + 3 * K1 * K1 + K1 * 8, 0);
+    uint64_t *pf = h.data(), *pb = pf + K1, *pm = pb + K1, *qf = pm + K1, *qb = qf + K1 * K1, *qc = qb + K1 * K1,
+             *bn = qc + K1 * K1;
+    for (int p = 0; p < g->K; p++) {
+        pf[p + 1] = pf[p] + g->fwd[p];
+        pb[p + 1] = pb[p] + g->bwd[p];
+        pm[p + 1] = pm[p] + g->mem[p];
+    }
+    for (size_t e = 0; e < g->e_src.size(); e++) {
+        const uint64_t at = (uint64_t)(g->e_src[e] + 1) * K1 + (uint64_t)(g->e_dst[e] + 1);
+        qf[at] += g->e_bf[e];
+        qb[at] += g->e_bb[e];
+        qc[at] += 1;
+    }
+    for (uint64_t i = 1; i < K1; i++)
+        for (uint64_t j = 1; j < K1; j++) {
+            const uint64_t a = i * K1 + j, l = i * K1 + j - 1, u = (i - 1) * K1 + j, ul = (i - 1) * K1 + j - 1;
+            qf[a] += qf[l] + qf[u] - qf[ul];
+            qb[a] += qb[l] + qb[u] - qb[ul];
+            qc[a] += qc[l] + qc[u] - qc[ul];
+        }
+    for (uint64_t n = 0; n < K1; n++)
+        for (uint64_t k = 0; k < 8; k++) bn[n * 8 + k] = binom_sat(n, k);
+    cudaError_t ce;
+    if ((ce = cudaMalloc(&g->d_pipe, h.size() * 8)) != cudaSuccess) return cuda_err(ce, "pipeline tables");
+    if ((ce = cudaMemcpy(g->d_pipe, h.data(), h.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cuda_err(ce, "pipeline tables");
+    return PP_OK;
+}
+
+int pp_pipeline_space(const pp_dfg *g, int M, int nm, uint64_t *count) {
+    if (!g || M < 1 || M > 8 || M > g->K || nm < 1 || nm > 16 || !count) {
+        set_error("invalid arguments");
+        return PP_E_INVALID;
+    }
+    const unsigned __int128 c = (unsigned __int128)binom_sat((uint64_t)g->K - 1, (uint64_t)M - 1) * (unsigned)nm;
+    if (c >= ((unsigned __int128)1 << 63)) { set_error("pipeline space exceeds 2^63"); return PP_E_TOO_LARGE; }
+    *count = (uint64_t)c;
+    return PP_OK;
+}
+
+int pp_pipeline_range(const pp_dfg *gc, int M, const uint32_t *micro, int nm, uint64_t begin, uint64_t end,
+                      uint64_t *d_best, uint64_t *d_makespan, void *stream) {
+    int rc = pipe_check(gc, M, micro, nm);
+    if (rc) return rc;
+    uint64_t space = 0;
+    if ((rc = pp_pipeline_space(gc, M, nm, &space))) return rc;
+    if (end <= begin || end > space || (!d_best && !d_makespan)) {
+        set_error("invalid range or no output");
+        return PP_E_INVALID;
+    }
+    pp_dfg *g = const_cast<pp_dfg *>(gc);   // the tables are a cache
+    DeviceGuard dg(g->device);
+    if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
+    if ((rc = pipe_tables(g))) return rc;
+    const uint64_t K1 = (uint64_t)g->K + 1;
+    PipeParams p{};
+    p.g_pf = g->d_pipe;
+    p.g_pb = p.g_pf + K1;
+    p.g_pm = p.g_pb + K1;
+    p.g_qf = p.g_pm + K1;
+    p.g_qb = p.g_qf + K1 * K1;
+    p.g_qc = p.g_qb + K1 * K1;
+    p.g_binom = p.g_qc + K1 * K1;
+    p.g_makespan = d_makespan;
+    p.g_partials = g->d_partials;
+    p.g_ticket = g->d_ticket;
+    p.g_out = d_best;
+    p.bw = g->link_bw;
+    p.lat = g->link_lat;
+    p.cap = g->cap;
+    p.begin = begin;
+    p.end = end;
+    p.K = (uint32_t)g->K;
+    p.nm = (uint32_t)nm;
+    for (int j = 0; j < nm; j++) p.micro[j] = micro[j];
+    const int threads = 256;
+    const uint64_t ranks = (end + nm - 1) / nm - begin / nm;
+    uint64_t grid = (uint64_t)g->sm_count * 8;
+    const uint64_t want = (ranks + threads - 1) / threads;
+    if (want < grid) grid = want;
+    if (grid < 1) grid = 1;
+    if (grid > (uint64_t)kMaxGrid) grid = kMaxGrid;
+    p.block = (ranks + grid * threads - 1) / (grid * threads);
+    if (p.block < 1) p.block = 1;
+    rc = launch_pipeline(M, p, (int)grid, threads, stream);
+    g_launches++;
+    if (rc) return cuda_err((cudaError_t)rc, "pipeline kernel launch");
+    return PP_OK;
+}
+
+int pp_pipeline_search(const pp_dfg *g, int M, const uint32_t *micro, int nm, void *stream,
+                       pp_pipeline_result *out) {
+    if (!out) { set_error("out is NULL"); return PP_E_INVALID; }
+    int rc = pipe_check(g, M, micro, nm);
+    if (rc) return rc;
+    uint64_t space = 0;
+    if ((rc = pp_pipeline_space(g, M, nm, &space))) return rc;
+    DeviceGuard dg(g->device);
+    if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
+    uint64_t *d_best = g->d_scalars + 32;    // scratch slots 32, 33
+    if ((rc = pp_pipeline_range(g, M, micro, nm, 0, space, d_best, nullptr, stream))) return rc;
+    uint64_t best[2];
+    cudaError_t ce;
+    if ((ce = cudaMemcpyAsync(best, d_best, sizeof best, cudaMemcpyDeviceToHost, (cudaStream_t)stream)) !=
+            cudaSuccess ||
+        (ce = cudaStreamSynchronize((cudaStream_t)stream)) != cudaSuccess)
+        return cuda_err(ce, "pipeline result");
+    memset(out, 0, sizeof *out);
+    out->makespan_ps = best[0];
+    out->index = best[1];
+    out->candidates = space;
+    out->n_stages = (uint32_t)M;
+    out->micro_batches = micro[best[1] % (uint64_t)nm];
+    uint64_t rank = best[1] / (uint64_t)nm;       // unrank the cut vector
+    uint64_t x = 1;
+    for (int i = 0; i < M - 1; i++) {
+        for (;;) {
+            const uint64_t c = binom_sat((uint64_t)g->K - 1 - x, (uint64_t)(M - 2 - i));
+            if (rank < c) break;
+            rank -= c;
+            x++;
+        }
+        out->cuts[i] = (int32_t)x;
+        x++;
+    }
+    if (best[0] == PP_INFEASIBLE_MAKESPAN) {
+        set_error("every pipeline violates the device memory capacity");
+        return PP_E_INFEASIBLE;
+    }
+    return PP_OK;
+}
+
 // ------------------------------------- placement-aware AR shards (NEXT f4)
 int pp_shard_bytes(const pp_dfg *g, int M, const uint8_t *placement, uint64_t *out) {
     if (!g || M < 1 || M > 8 || !placement || !out) {

@@ -149,6 +149,23 @@ struct GArc {
     uint32_t row;         // cost row
 };
 
+// ---- pipeline-parallel MP, built on first use:
+// π-prefix sums of Δf, Δb, M(k) ([K+1] each), 2-D prefix sums over
+// (producer π position, consumer π position) of the edges' forward bytes,
+// backward bytes and count ([(K+1)²] each), binomials C(n, k) for k < 8.
+struct PipeParams {
+    const uint64_t *g_pf, *g_pb, *g_pm, *g_qf, *g_qb, *g_qc, *g_binom;
+    uint64_t *g_makespan;        // optional per-candidate output [end − begin]
+    uint64_t *g_partials;        // [grid][2]
+    unsigned *g_ticket;
+    uint64_t *g_out;             // {makespan, index} or null
+    uint64_t bw, lat, cap, begin, end, block;
+    uint32_t K, nm;
+    uint32_t micro[16];
+};
+constexpr int kMaxPipelineK = 1024;
+int launch_pipeline(int M, const PipeParams &p, int grid, int threads, void *stream);
+
 // per-warp branch-and-bound state of the exact kernel (shared memory)
 struct XWarp {
     uint64_t fin[kMaxExactNodes];
@@ -236,6 +253,10 @@ struct pp_dfg {
     std::vector<int32_t> pi;     // π position → descriptor index
     std::vector<int32_t> pos;    // descriptor index → π position
     std::vector<uint64_t> param; // param_bytes by descriptor index
+    uint64_t link_bw = 0, link_lat = 0;            // uniform link (0 in hw mode)
+    std::vector<int32_t> e_src, e_dst;             // edges by π position
+    std::vector<uint64_t> e_bf, e_bb, fwd, bwd, mem;   // bytes; Δf, Δb, M(k) by π position
+    uint64_t *d_pipe = nullptr;                    // pipeline tables (lazily built)
     std::vector<uint8_t> image;  // host copy of the image
     uint32_t off_extra = 0, off_mem = 0, off_orig = 0, image_bytes = 0;
     uint32_t base_bytes = 0;     // K rounded up to 16

@@ -377,6 +377,23 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     g->hw = hw != nullptr;
     g->nd = nd;
     g->off_cls = (uint32_t)off_cls;
+    if (link) {
+        g->link_bw = link->link_bw_Bps;
+        g->link_lat = link->link_lat_ps;
+    }
+    g->e_src.resize(E); g->e_dst.resize(E); g->e_bf.resize(E); g->e_bb.resize(E);
+    for (int e = 0; e < E; e++) {
+        g->e_src[e] = pos[src[e]];
+        g->e_dst[e] = pos[dst[e]];
+        g->e_bf[e] = d->edge_fwd_bytes[e];
+        g->e_bb[e] = d->edge_bwd_bytes ? d->edge_bwd_bytes[e] : d->edge_fwd_bytes[e];
+    }
+    g->fwd.resize(K); g->bwd.resize(K); g->mem.resize(K);
+    for (int p = 0; p < K; p++) {
+        g->fwd[p] = d->fwd_ps[pi[p]];
+        g->bwd[p] = d->bwd_ps[pi[p]];
+        g->mem[p] = d->mem_bytes ? d->mem_bytes[pi[p]] : 0;
+    }
     g->grad_bytes = 0;
     g->param.assign(K, 0);
     if (d->param_bytes)
@@ -595,6 +612,7 @@ extern "C" void pp_free_dfg(pp_dfg *g) {
     if (g->d_ximage) cudaFree(g->d_ximage);
     if (g->d_xwork) cudaFree(g->d_xwork);
     if (g->d_gimage) cudaFree(g->d_gimage);
+    if (g->d_pipe) cudaFree(g->d_pipe);
     cudaSetDevice(prev);
     delete g;
 }

@@ -87,6 +87,11 @@ class CrossoverC(C.Structure):
                 ("persistent_M", C.c_uint32 * 8), ("n_star_vs_best_dp", C.c_uint32)]
 
 
+class PipelineResultC(C.Structure):
+    _fields_ = [("makespan_ps", C.c_uint64), ("index", C.c_uint64), ("candidates", C.c_uint64),
+                ("micro_batches", C.c_uint32), ("n_stages", C.c_uint32), ("cuts", C.c_int32 * 8)]
+
+
 # exported symbol → (argtypes, restype); the C-ABI load test checks this list
 # against include/pp.h
 SIGNATURES = {
@@ -106,6 +111,11 @@ SIGNATURES = {
                                  C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "pp_search_exact": ([C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint64,
                          C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
+    "pp_pipeline_space": ([C.c_void_p, C.c_int, C.c_int, P(C.c_uint64)], C.c_int),
+    "pp_pipeline_range": ([C.c_void_p, C.c_int, P(C.c_uint32), C.c_int, C.c_uint64, C.c_uint64, C.c_void_p,
+                           C.c_void_p, C.c_void_p], C.c_int),
+    "pp_pipeline_search": ([C.c_void_p, C.c_int, P(C.c_uint32), C.c_int, C.c_void_p, P(PipelineResultC)],
+                           C.c_int),
     "pp_shard_bytes": ([C.c_void_p, C.c_int, P(C.c_uint8), P(C.c_uint64)], C.c_int),
     "pp_eft_place": ([C.c_void_p, C.c_int, P(C.c_uint8), C.c_void_p], C.c_int),
     "pp_search_best": ([C.c_void_p, C.c_int, P(SearchDesc), C.c_void_p, C.c_void_p, P(SearchResultC)], C.c_int),
@@ -288,6 +298,32 @@ class Dfg:
         _check(lib().pp_search_range(self._h, M, gen, seed_r, tau, _dptr(b), begin, end, _dptr(out),
                                      _stream(stream)))
         return out
+
+    # ------------------------------------------ pipeline MP (§8(f) f3)
+    def pipeline_space(self, M, nm) -> int:
+        c = C.c_uint64()
+        _check(lib().pp_pipeline_space(self._h, M, nm, C.byref(c)))
+        return int(c.value)
+
+    def pipeline_search(self, M, micro, stream=None) -> dict:
+        mi = np.ascontiguousarray(np.asarray(micro, dtype=np.uint32))
+        r = PipelineResultC()
+        _check(lib().pp_pipeline_search(self._h, M, _ptr(mi, C.c_uint32), len(mi), _stream(stream), C.byref(r)))
+        return {"makespan_ps": int(r.makespan_ps), "index": int(r.index), "candidates": int(r.candidates),
+                "micro_batches": int(r.micro_batches), "cuts": [int(x) for x in r.cuts[:M - 1]]}
+
+    def pipeline_range(self, M, micro, begin, end, all_values=False, stream=None):
+        """(makespan, index) argmin over [begin, end) — and the per-candidate
+        makespans (int64 CUDA tensor) when all_values."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        mi = np.ascontiguousarray(np.asarray(micro, dtype=np.uint32))
+        best = torch.empty(2, dtype=torch.int64, device=dev)
+        vals = torch.empty(end - begin, dtype=torch.int64, device=dev) if all_values else None
+        _check(lib().pp_pipeline_range(self._h, M, _ptr(mi, C.c_uint32), len(mi), begin, end, _dptr(best),
+                                       _dptr(vals), _stream(stream)))
+        b = u64(best)
+        return (int(b[0]), int(b[1])), vals
 
     def shard_bytes(self, M, placement) -> list:
         """Per-device gradient shard S_d of a placement (descriptor order)."""

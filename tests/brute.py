@@ -233,3 +233,56 @@ def gray_first_index(spec, M, best):
         if longest_path_makespan(spec, M, pl) == best:
             return i, pl
     return None, None
+
+
+def pipeline_makespan(spec, M, cuts, m):
+    """GPipe makespan (NEXT f3, reading R26) as the longest path of an explicit
+    task graph: tasks F(s,j) and B(s,j) with their micro-batch times; arcs for
+    each device's task order F(s,0..m−1), B(s,m−1..0) and for the stage-to-
+    stage transfers of every micro-batch.  A different formulation from the
+    oracle's row recurrences."""
+    K = len(spec["fwd_ps"])
+    ids = spec.get("op_id") or list(range(K))
+    order = kahn_by_id(K, ids, spec["edge_src"], spec["edge_dst"])
+    bounds = [0] + list(cuts) + [K]
+    stage = {}
+    for s in range(M):
+        for p in range(bounds[s], bounds[s + 1]):
+            stage[order[p]] = s
+    cap = spec.get("dev_mem_cap_bytes") or 0
+    if cap:
+        mem = spec.get("mem_bytes") or [0] * K
+        for s in range(M):
+            if sum(mem[k] for k in range(K) if stage[k] == s) > cap:
+                return (1 << 64) - 1
+    tf = [-(-sum(spec["fwd_ps"][k] for k in range(K) if stage[k] == s) // m) for s in range(M)]
+    tb = [-(-sum(spec["bwd_ps"][k] for k in range(K) if stage[k] == s) // m) for s in range(M)]
+    bf = spec["edge_fwd_bytes"]
+    bb = spec.get("edge_bwd_bytes") or bf
+    bw, lat = spec["link_bw_Bps"], spec["link_lat_ps"]
+    link = {}
+    for e, (u, v) in enumerate(zip(spec["edge_src"], spec["edge_dst"])):
+        a, b = stage[u], stage[v]
+        if a != b:
+            x = link.setdefault((a, b), [0, 0])
+            x[0] += bf[e]
+            x[1] += bb[e]
+    preds = {}
+    for s in range(M):
+        seq = [("F", s, j) for j in range(m)] + [("B", s, j) for j in reversed(range(m))]
+        for i, t in enumerate(seq):
+            preds[t] = [(seq[i - 1], 0)] if i else []
+    for (a, b), (df, db) in link.items():
+        for j in range(m):
+            preds[("F", b, j)].append((("F", a, j), -(-df * 10**12 // (m * bw)) + lat))
+            preds[("B", a, j)].append((("B", b, j), -(-db * 10**12 // (m * bw)) + lat))
+    dur = {("F", s, j): tf[s] for s in range(M) for j in range(m)}
+    dur.update({("B", s, j): tb[s] for s in range(M) for j in range(m)})
+    memo = {}
+
+    def fin(t):
+        if t not in memo:
+            memo[t] = max([fin(p) + c for p, c in preds[t]] or [0]) + dur[t]
+        return memo[t]
+
+    return max(fin(("B", s, 0)) for s in range(M))
