@@ -7,10 +7,12 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "internal.h"
 
@@ -130,44 +132,34 @@ static int choose(const pp_dfg *g, int M, int gen, bool write_all, int np, Choic
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device);
     const size_t max_dyn = (size_t)std::min<int>(optin, kMaxSmemBytes) - fa.sharedSizeBytes - 1024;
+    // CTA size: the most resident warps per SM (each CTA holds its own copy
+    // of the image), ties to the larger CTA; up to the kernel's launch bound
     c.threads = 0;
-    for (int threads = 256; threads >= 32; threads >>= 1) {
-        size_t smem = c.slots_off + (size_t)(threads / 32) * c.region;
-        if (smem <= max_dyn) { c.threads = threads; c.smem = (int)smem; break; }
+    int best_warps = 0;
+    const int max_threads = std::min(fa.maxThreadsPerBlock, 1024) / 32 * 32;
+    for (int threads = max_threads; threads >= 32; threads -= 32) {
+        const size_t smem = c.slots_off + (size_t)(threads / 32) * c.region;
+        if (smem > max_dyn) continue;
+        e = cudaFuncSetAttribute(c.k.func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
+        int ctas = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, c.k.func, threads, (int)smem);
+        if (e != cudaSuccess) return cuda_err(e, "occupancy");
+        const int warps = ctas * threads / 32;
+        if (ctas >= 1 && warps > best_warps) {
+            best_warps = warps;
+            c.threads = threads;
+            c.smem = (int)smem;
+            c.ctas = ctas;
+        }
     }
     if (!c.threads) return PP_E_TOO_LARGE;
     e = cudaFuncSetAttribute(c.k.func, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem);
     if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.ctas, c.k.func, c.threads, c.smem);
-    if (e != cudaSuccess) return cuda_err(e, "occupancy");
-    if (c.ctas < 1) c.ctas = 1;
     return PP_OK;
 }
 
-static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin, uint64_t end, Launch &L) {
-    Choice best;
-    int best_warps = -1;
-    int forced = 0;   // PP_NP=1|2|4 pins NP (tests cover every variant)
-    if (const char *v = getenv("PP_NP")) forced = atoi(v);
-    for (int np : {4, 2, 1}) {
-        if (forced && np != forced) continue;
-        Choice c;
-        int rc = choose(g, M, gen, write_all, np, c);
-        if (rc == PP_E_TOO_LARGE) continue;
-        if (rc) return rc;
-        const int warps = c.ctas * c.threads / 32;
-        if (warps >= 12 || write_all || forced) { best = c; best_warps = warps; break; }
-        // otherwise keep the most placements in flight, ties to more warps
-        if (best_warps < 0 || warps * c.np > best_warps * best.np ||
-            (warps * c.np == best_warps * best.np && warps > best_warps)) {
-            best = c;
-            best_warps = warps;
-        }
-    }
-    if (best_warps < 0) {
-        set_error("per-lane schedule state does not fit in shared memory");
-        return PP_E_TOO_LARGE;
-    }
+static void fill(const pp_dfg *g, const Choice &best, uint64_t begin, uint64_t end, Launch &L) {
     L.k = best.k;
     const uint64_t n = end - begin;
     const uint64_t per_warp = 32ull * best.np;
@@ -200,6 +192,80 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
     p.g_partials = g->d_partials;
     p.g_ticket = g->d_ticket;
     p.g_out = g->d_scalars + SC_LOCAL_MK;
+}
+
+// Placements per lane (NP) for the argmin kernels is chosen by MEASUREMENT:
+// the first search call for a (DFG, M, generator) times each NP variant (its
+// best CTA shape) on the same probe range and keeps the fastest.  The result
+// does not depend on the choice (every variant is bit-exact), only the speed.
+// The per-candidate (write-all) kernels are built for NP = 2 only.
+static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin, uint64_t end, Launch &L,
+                 void *stream = nullptr) {
+    int forced = 0;   // PP_NP=1|2|4 pins NP (tests cover every variant)
+    if (const char *v = getenv("PP_NP")) forced = atoi(v);
+    std::vector<Choice> cands;
+    for (int np : {4, 2, 1}) {
+        if (write_all && np != 2) continue;
+        if (forced && np != forced) continue;
+        Choice c;
+        int rc = choose(g, M, gen, write_all, np, c);
+        if (rc == PP_E_TOO_LARGE) continue;
+        if (rc) return rc;
+        cands.push_back(c);
+    }
+    if (cands.empty()) {
+        set_error("per-lane schedule state does not fit in shared memory");
+        return PP_E_TOO_LARGE;
+    }
+    size_t pick = 0;
+    const int key = (M << 8) | (gen << 4) | (write_all ? 1 : 0);
+    auto it = g->tuned.find(key);
+    if (cands.size() > 1 && it != g->tuned.end()) {
+        for (size_t i = 0; i < cands.size(); i++)
+            if (cands[i].np == it->second) pick = i;
+    } else if (cands.size() > 1) {
+        // probe: the same candidate range for every variant, long enough to
+        // fill the GPU a few times; each variant runs twice (the first run
+        // absorbs module loading), the second is timed
+        uint64_t probe = 0;
+        for (auto &c : cands)
+            probe = std::max<uint64_t>(probe, 4ull * c.ctas * g->sm_count * c.threads * c.np);
+        probe = std::min<uint64_t>(probe, end - begin);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        float best_ms = 0;
+        for (size_t i = 0; i < cands.size(); i++) {
+            Launch T;
+            fill(g, cands[i], begin, begin + probe, T);
+            T.p.g_out = g->d_scalars + 40;          // scratch slots: no result is touched
+            float ms = 0;
+            for (int rep = 0; rep < 2; rep++) {
+                cudaEventRecord(e0, (cudaStream_t)stream);
+                int e = T.k.launch(T.p, T.grid, T.threads, T.smem, stream);
+                g_launches++;
+                cudaEventRecord(e1, (cudaStream_t)stream);
+                if (e) { cudaEventDestroy(e0); cudaEventDestroy(e1); return cuda_err((cudaError_t)e, "probe"); }
+                cudaEventSynchronize(e1);
+                cudaEventElapsedTime(&ms, e0, e1);
+            }
+            if (i == 0 || ms < best_ms) { best_ms = ms; pick = i; }
+            if (getenv("PP_VERBOSE"))
+                fprintf(stderr, "pp: probe M=%d gen=%d np=%d threads=%d warps/SM=%d: %.3f ms\n", M, gen,
+                        cands[i].np, cands[i].threads, cands[i].ctas * cands[i].threads / 32, ms);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        g->tuned[key] = cands[pick].np;
+    }
+    const Choice &best = cands[pick];
+    if (getenv("PP_VERBOSE")) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, best.k.func);
+        fprintf(stderr, "pp: M=%d gen=%d np=%d threads=%d ctas/SM=%d warps/SM=%d smem=%d regs=%d W=%d\n", M, gen,
+                best.np, best.threads, best.ctas, best.ctas * best.threads / 32, best.smem, fa.numRegs, g->W);
+    }
+    fill(g, best, begin, end, L);
     return PP_OK;
 }
 
@@ -368,7 +434,7 @@ int pp_search_range(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
         g_launches++;
     }
     Launch L;
-    rc = setup(g, M, gen, false, begin, end, L);
+    rc = setup(g, M, gen, false, begin, end, L, stream);
     if (rc) return rc;
     L.p.seed = seed_r;
     L.p.tau = tau;
@@ -731,7 +797,7 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
     Launch L;
     const bool empty = end <= begin;
     if (!empty) {
-        rc = setup(g, M, desc->gen, false, begin, end, L);
+        rc = setup(g, M, desc->gen, false, begin, end, L, stream);
         if (rc) return rc;
         L.p.tau = desc->flip_thresh;
     }

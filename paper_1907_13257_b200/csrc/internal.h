@@ -40,6 +40,7 @@
 // only in the tag, which is cleared before use).
 #pragma once
 #include <cstdint>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -257,6 +258,7 @@ struct pp_dfg {
     std::vector<int32_t> e_src, e_dst;             // edges by π position
     std::vector<uint64_t> e_bf, e_bb, fwd, bwd, mem;   // bytes; Δf, Δb, M(k) by π position
     uint64_t *d_pipe = nullptr;                    // pipeline tables (lazily built)
+    mutable std::map<int, int> tuned;              // (M, gen) -> measured best NP
     std::vector<uint8_t> image;  // host copy of the image
     uint32_t off_extra = 0, off_mem = 0, off_orig = 0, image_bytes = 0;
     uint32_t base_bytes = 0;     // K rounded up to 16

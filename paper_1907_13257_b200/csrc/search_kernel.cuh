@@ -34,8 +34,11 @@
 
 #include "internal.h"
 
+#ifndef PP_CTA_THREADS
+#define PP_CTA_THREADS 640   // largest CTA the register allocation targets (A/B: profiles/r01_ab_matrix.txt)
+#endif
 #ifndef PP_MIN_CTAS
-#define PP_MIN_CTAS 2   // resident CTAs per SM the register allocation targets (measured best)
+#define PP_MIN_CTAS 1   // resident CTAs per SM the register allocation targets (measured best)
 #endif
 
 namespace pp {
@@ -654,10 +657,10 @@ __device__ __forceinline__ bool lex_less(uint64_t m1, uint64_t i1, uint64_t m2, 
 
 // ------------------------------------------------------------------ kernel
 template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64, int NP, bool HW>
-__global__ void __launch_bounds__(256, PP_MIN_CTAS) search_kernel(const KParams P) {
+__global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(const KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t mbar;
-    __shared__ uint64_t red_mk[8], red_i[8];
+    __shared__ uint64_t red_mk[32], red_i[32];
     __shared__ bool is_last;
 
     const uint32_t tid = threadIdx.x;
