@@ -459,10 +459,11 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], uint3
 // region, where free[pdev] may be stale (≤ prev) because the live value is
 // prev.  Slot values stay tagged (t + d·ulp(t)) for the non-chain reads; the
 // tag is set only when a value is stored.  With cut = [dev ≠ pdev] ∈ {0.0,
-// 1.0} and same = 1 − cut, a chain step is
-//   s = max(prev + cut·c0, free[dev] − same·2^50)   (free[dev] = prev if same)
+// 1.0}, a chain step is
+//   s = max(prev + cut·c0, cut·free[dev])   (no cut: free[dev] is prev, and
+//                                            cut·free = 0 ≤ prev drops out)
 //   prev' = s + cost, pdev' = dev, and the old prev becomes free[pdev]:
-//   M = 2: oth' = cut·prev + same·oth;  M ≥ 3: free[pdev] ← prev (always)
+//   M = 2: oth' = oth + cut·(prev − oth);  M ≥ 3: free[pdev] ← prev (always)
 // — every operation exact on integers < 2^49; only the max needs a select.
 // x ∈ {0,1} → 0.0 / 1.0 as one IMAD on the FMA pipe: khi = 0x3FF00000 (the
 // high word of 1.0) is a kernel parameter, so ptxas cannot turn the multiply
@@ -504,7 +505,6 @@ template <int M, int NP, bool MEM, bool HW, class Gen>
 __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint32_t ops, uint32_t xr,
                                              const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
                                              uint32_t K8, uint64_t cap, uint32_t khi, uint32_t cls) {
-    constexpr double kBig = 1125899906842624.0;   // 2^50
     constexpr bool SM = M > 2;                    // free[] in shared memory
     double prev[NP], oth[NP];
     uint32_t pdev[NP];
@@ -538,16 +538,17 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
             // chain step: the only input is the previous step's output
 #pragma unroll
             for (int k = 0; k < NP; k++) {
+                // free[dev] matters only across a cut (else it is prev, and
+                // cut·free = 0 ≤ prev): s = max(prev + cut·c0, cut·free[dev])
                 const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
-                const double same = __dadd_rn(1.0, -cut);
                 const double t = HW ? __dadd_rn(prev[k], hwc(a.z, pdev[k], dev[k])) : __fma_rn(c0, cut, prev[k]);
                 double s;
                 if (SM) {
-                    s = dmax(t, __fma_rn(same, -kBig, ldd(fslot(k, dev[k]))));
+                    s = dmax(t, __dmul_rn(cut, ldd(fslot(k, dev[k]))));
                     std_(fslot(k, pdev[k]), prev[k]);
                 } else {
-                    s = dmax(t, __fma_rn(same, -kBig, oth[k]));
-                    oth[k] = __fma_rn(cut, prev[k], __dmul_rn(same, oth[k]));
+                    s = dmax(t, __dmul_rn(cut, oth[k]));
+                    oth[k] = __fma_rn(cut, __dadd_rn(prev[k], -oth[k]), oth[k]);   // cut ? prev : oth
                 }
                 prev[k] = __dadd_rn(s, cost);
                 pdev[k] = dev[k];
@@ -582,16 +583,16 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
             }
 #pragma unroll
             for (int k = 0; k < NP; k++) {
-                // free[dev] = same ? prev : other, as exact products (FP64 pipe)
+                // free[dev] = cut ? other : prev, exact on the FP64 pipe
                 const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
-                const double same = __dadd_rn(1.0, -cut);
                 double f;
                 if (SM) {
-                    f = __fma_rn(same, prev[k], __dmul_rn(cut, ldd(fslot(k, dev[k]))));
+                    f = __fma_rn(cut, __dadd_rn(ldd(fslot(k, dev[k])), -prev[k]), prev[k]);
                     std_(fslot(k, pdev[k]), prev[k]);
                 } else {
-                    f = __fma_rn(same, prev[k], __dmul_rn(cut, oth[k]));
-                    oth[k] = __fma_rn(cut, prev[k], __dmul_rn(same, oth[k]));
+                    const double d = __dadd_rn(prev[k], -oth[k]);
+                    f = __fma_rn(-cut, d, prev[k]);
+                    oth[k] = __fma_rn(cut, d, oth[k]);
                 }
                 prev[k] = __dadd_rn(clear_tag(dmax(r[k], f)), cost);
                 pdev[k] = dev[k];
