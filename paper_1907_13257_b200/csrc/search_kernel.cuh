@@ -415,10 +415,13 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], uint3
             for (int k = 0; k < NP; k++) mu[k].add(Dev<M>::canon(dev[k]), m);
         }
     };
+    // the two half-groups of an 8-op group: looped at NP = 4 (the unrolled
+    // body overflows the instruction cache), unrolled below (A/B measured)
+    constexpr int kHalfUnroll = NP >= 4 ? 1 : 2;
     const uint32_t G = K8 / 8;
     for (uint32_t g = 0; g < G; g++) {           // forward, π order
         gen.refresh(g);
-#pragma unroll 1
+#pragma unroll (kHalfUnroll)
         for (uint32_t h = 0; h < 2; h++) {
             gen.sub(h);
             const uint32_t rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
@@ -428,7 +431,7 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], uint3
     }
     for (uint32_t g = G; g-- > 0;) {             // backward, reverse π order
         gen.refresh(g);
-#pragma unroll 1
+#pragma unroll (kHalfUnroll)
         for (uint32_t h = 2; h-- > 0;) {
             gen.sub(h);
             const uint32_t rec = ops + (2 * K8 - 1 - g * 8 - h * 4) * (uint32_t)sizeof(OpRec);
@@ -608,10 +611,13 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
             for (int k = 0; k < NP; k++) mu[k].add(Dev<M>::canon(dev[k]), m);
         }
     };
+    // the two half-groups of an 8-op group: looped at NP = 4 (the unrolled
+    // body overflows the instruction cache), unrolled below (A/B measured)
+    constexpr int kHalfUnroll = NP >= 4 ? 1 : 2;
     const uint32_t G = K8 / 8;
     for (uint32_t g = 0; g < G; g++) {           // forward, π order
         gen.refresh(g);
-#pragma unroll 1
+#pragma unroll (kHalfUnroll)
         for (uint32_t h = 0; h < 2; h++) {
             gen.sub(h);
             const uint32_t rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
@@ -621,7 +627,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
     }
     for (uint32_t g = G; g-- > 0;) {             // backward, reverse π order
         gen.refresh(g);
-#pragma unroll 1
+#pragma unroll (kHalfUnroll)
         for (uint32_t h = 2; h-- > 0;) {
             gen.sub(h);
             const uint32_t rec = ops + (2 * K8 - 1 - g * 8 - h * 4) * (uint32_t)sizeof(OpRec);
