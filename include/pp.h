@@ -275,6 +275,16 @@ int  pp_comm_get_unique_id(uint8_t out_id[128]);
 int  pp_comm_init(const uint8_t id[128], int rank, int world, int cuda_device, pp_comm **out);
 void pp_comm_destroy(pp_comm *comm);
 
+/* The (makespan, index) argmin across the ranks of comm:
+ * each rank's d_best (device ptr uint64[2] = {makespan, index} over its own
+ * candidate slice, e.g. from pp_search_range / pp_search_exact /
+ * pp_pipeline_range on its pp_rank_slice) is replaced in place by the global
+ * lexicographic argmin: one NCCL min all-reduce of the packed key
+ * (pp_pack_key: the smallest makespan, ties to the lowest rank, i.e. the
+ * lowest indices for contiguous slices), a second of the winner's index.
+ * Asynchronous on cuda_stream.  Errors: PP_E_INVALID, PP_E_NCCL, PP_E_CUDA. */
+int pp_argmin_allreduce(const pp_dfg *dfg, pp_comm *comm, uint64_t *d_best, void *cuda_stream);
+
 /* Sharding protocol (host only, no GPU needed; exported so multi-process CPU
  * tests exercise the exact same rules):
  *   rank r of R owns candidates [⌊r·n/R⌋, ⌊(r+1)·n/R⌋) of every round;

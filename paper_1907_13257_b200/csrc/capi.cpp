@@ -80,6 +80,7 @@ struct CrossParams;
 int launch_pack_key(uint64_t *s, int rank, void *stream);
 int launch_patch_base(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8, void *stream);
 int launch_contrib(uint64_t *s, int rank, void *stream);
+int launch_unpack_best(const uint64_t *s, uint64_t *out, void *stream);
 
 static int cuda_err(cudaError_t e, const char *what) {
     set_error(std::string("CUDA: ") + what + ": " + cudaGetErrorString(e));
@@ -871,6 +872,30 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
         set_error("every candidate violates the device memory capacity");
         return PP_E_INFEASIBLE;
     }
+    return PP_OK;
+}
+
+int pp_argmin_allreduce(const pp_dfg *g, pp_comm *comm, uint64_t *d_best, void *stream) {
+    if (!g || !comm || !d_best) { set_error("invalid arguments"); return PP_E_INVALID; }
+    Nccl *nc = nccl();
+    if (!nc) { set_error("NCCL not loadable"); return PP_E_NCCL; }
+    DeviceGuard dg(g->device);
+    if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(g->d_scalars + SC_LOCAL_MK, d_best, 2 * sizeof(uint64_t),
+                                    cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_err(e, "argmin copy");
+    int rc;
+    if ((rc = launch_pack_key(g->d_scalars, comm->rank, stream))) return cuda_err((cudaError_t)rc, "pack");
+    ncclResult_t nr = nc->AllReduce(g->d_scalars + SC_KEY_LOCAL, g->d_scalars + SC_KEY_GLOBAL, 1, ncclUint64,
+                                    ncclMin, comm->comm, st);
+    if (nr != ncclSuccess) return nccl_err(nr, "allreduce key");
+    if ((rc = launch_contrib(g->d_scalars, comm->rank, stream))) return cuda_err((cudaError_t)rc, "contrib");
+    nr = nc->AllReduce(g->d_scalars + SC_IDX_LOCAL, g->d_scalars + SC_IDX_GLOBAL, 1, ncclUint64, ncclMin,
+                       comm->comm, st);
+    if (nr != ncclSuccess) return nccl_err(nr, "allreduce index");
+    if ((rc = launch_unpack_best(g->d_scalars, d_best, stream))) return cuda_err((cudaError_t)rc, "unpack");
+    g_launches += 3;
     return PP_OK;
 }
 

@@ -284,6 +284,15 @@ int launch_pack_key(uint64_t *s, int rank, void *stream) {
     pack_key_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(s, rank);
     return (int)cudaGetLastError();
 }
+__global__ void unpack_best_kernel(const uint64_t *s, uint64_t *out) {
+    const uint64_t m = s[SC_KEY_GLOBAL] >> 3;
+    out[0] = (m == ((1ull << 61) - 1)) ? kInfeasible : m;
+    out[1] = s[SC_IDX_GLOBAL];
+}
+int launch_unpack_best(const uint64_t *s, uint64_t *out, void *stream) {
+    unpack_best_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(s, out);
+    return (int)cudaGetLastError();
+}
 int launch_contrib(uint64_t *s, int rank, void *stream) {
     contrib_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(s, rank);
     return (int)cudaGetLastError();

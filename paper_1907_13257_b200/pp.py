@@ -122,6 +122,7 @@ SIGNATURES = {
     "pp_comm_get_unique_id": ([P(C.c_uint8)], C.c_int),
     "pp_comm_init": ([P(C.c_uint8), C.c_int, C.c_int, C.c_int, P(C.c_void_p)], C.c_int),
     "pp_comm_destroy": ([C.c_void_p], None),
+    "pp_argmin_allreduce": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "pp_rank_slice": ([C.c_uint64, C.c_int, C.c_int, P(C.c_uint64), P(C.c_uint64)], None),
     "pp_pack_key": ([C.c_uint64, C.c_int], C.c_uint64),
     "pp_key_makespan": ([C.c_uint64], C.c_uint64),
@@ -405,6 +406,12 @@ class Comm:
         _check(lib().pp_comm_init(uid, rank, world, device, C.byref(h)))
         self._h = h
         self.rank, self.world = rank, world
+
+    def argmin_allreduce(self, dfg, best, stream=None):
+        """In place: best (int64[2] CUDA tensor {makespan, index} over this
+        rank's slice) becomes the global lexicographic argmin."""
+        _check(lib().pp_argmin_allreduce(dfg._h, self._h, _dptr(best), _stream(stream)))
+        return best
 
     def close(self):
         if getattr(self, "_h", None):

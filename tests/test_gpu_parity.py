@@ -287,3 +287,47 @@ def test_every_placements_per_lane_variant(dfgs, np_, monkeypatch):
         got = pp.u64(g.search_range(M, gen, 77, 24, base, 3, 3 + count))
         want = od.round(M, gen, 77, 24, base, 3, 3 + count)
         assert (int(got[0]), int(got[1])) == want, (name, np_)
+
+
+def test_sharded_exact_and_pipeline_searches():
+    """The exact-schedule (§8(f) f1) and pipeline (f3) searches shard like the
+    main search: per-rank slices + the packed-key argmin equal the full range
+    (3 emulated ranks on one GPU), and pp_argmin_allreduce at world size 1
+    leaves a rank's argmin unchanged."""
+    import os
+    import socket
+    import torch.distributed as dist
+    spec = synth.toy12()
+    g = pp.Dfg(spec)
+    full_x = g.search_exact(2, pp.GEN_GRAY, 0, 0, None, 0, 4096)
+    micro = [1, 2, 4, 8]
+    n_pipe = g.pipeline_space(3, len(micro))
+    (full_p, full_pi), _ = g.pipeline_range(3, micro, 0, n_pipe)
+    for world in (2, 3):
+        keys_x, idx_x, keys_p, idx_p = [], {}, [], {}
+        for r in range(world):
+            b, e = pp.rank_slice(4096, r, world)
+            mk, ix, _ = g.search_exact(2, pp.GEN_GRAY, 0, 0, None, b, e)
+            keys_x.append(pp.pack_key(mk, r))
+            idx_x[r] = ix
+            b, e = pp.rank_slice(n_pipe, r, world)
+            (mk, ix), _ = g.pipeline_range(3, micro, b, e)
+            keys_p.append(pp.pack_key(mk, r))
+            idx_p[r] = ix
+        kx, kp = min(keys_x), min(keys_p)
+        assert (pp.key_makespan(kx), idx_x[pp.key_rank(kx)]) == full_x[:2]
+        assert (pp.key_makespan(kp), idx_p[pp.key_rank(kp)]) == (full_p, full_pi)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = pp.Comm(0, 1, 0)
+        best = torch.tensor([full_x[0], full_x[1]], dtype=torch.int64, device="cuda")
+        comm.argmin_allreduce(g, best)
+        assert tuple(int(x) for x in pp.u64(best)) == full_x[:2]
+        comm.close()
+    finally:
+        dist.destroy_process_group()
