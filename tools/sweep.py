@@ -1,8 +1,11 @@
 """BASELINE config 5: the full end-to-end projection sweep on one GPU.
 
 For each paper-shaped DFG (Inception-V3, GNMT, BigLSTM): a PERTURB search for
-M ∈ {2, 4, 8} (rounds × count candidates each) gives T_M (T_1 = ΣΔ needs no
-search), then the projection over M ∈ {1, 2, 4, 8} × N = 1..N_max with the
+M ∈ {2, 4, 8} (rounds × count candidates each, seeded with the EFT placement)
+gives T_M (T_1 = ΣΔ needs no search); for GNMT and BigLSTM — which the paper
+split by pipelining — the GPipe search (§8(f) f3, stage cuts ×
+m ∈ {1..32}) gives a second T_M, and the projection takes the better of the
+two.  Then the projection over M ∈ {1, 2, 4, 8} × N = 1..N_max with the
 16-knot epochs curve (reading R13) in EQ5 and TIME modes, and the crossover.
 Prints one JSON line per model plus a summary line.
 
@@ -24,6 +27,8 @@ import synth  # noqa: E402
 
 MODELS = ["inception_v3", "gnmt", "biglstm"]
 MS = [1, 2, 4, 8]
+PIPELINED = ("gnmt", "biglstm")
+MICRO = [1, 2, 4, 8, 16, 32]
 
 
 def run(count, rounds, nmax, seed=13257, tau=8):
@@ -35,13 +40,20 @@ def run(count, rounds, nmax, seed=13257, tau=8):
     for model in MODELS:
         g = pp.Dfg(getattr(synth, model)())
         T = [g.t1]
-        su = {}
+        su, su_pipe = {}, {}
         for M in MS[1:]:
-            r = g.search_best(M, pp.GEN_PERTURB, seed, count, rounds=rounds, tau=tau)
-            T.append(r.best_makespan_ps)
-            su[M] = g.t1 / r.best_makespan_ps
+            r = g.search_best(M, pp.GEN_PERTURB, seed, count, rounds=rounds, tau=tau, base=g.eft_place(M))
+            t_m = r.best_makespan_ps
             total += r.evaluated
-        res = {"model": model, "K": g.K, "T_ps": dict(zip(MS, T)), "su_mp": su}
+            su[M] = g.t1 / t_m
+            if model in PIPELINED and M <= 4:          # M = 8 spans 10^13 stage splits
+                p = g.pipeline_search(M, MICRO)
+                total += p["candidates"]
+                su_pipe[M] = g.t1 / p["makespan_ps"]
+                t_m = min(t_m, p["makespan_ps"])
+            T.append(t_m)
+        res = {"model": model, "K": g.K, "T_ps": dict(zip(MS, T)), "su_mp_placement": su,
+               "su_mp_pipeline": su_pipe, "su_mp": {M: g.t1 / t for M, t in zip(MS[1:], T[1:])}}
         for mode, name in ((0, "EQ5"), (1, "TIME")):
             sc = synth.sweep_scenario(model, g.t1, g.grad_bytes, ar_mode=mode)
             cells = pp.project_e2e(sc, MS, T, nmax)
