@@ -217,7 +217,9 @@ int pp_search_exact(const pp_dfg *dfg, int M, int gen, uint64_t seed_r, uint32_t
  * GPipe-style pipelining (§2; §4.4: how GNMT and
  * BigLSTM were split).  Reading R26: M stages are contiguous
  * π ranges [cut_s, cut_{s+1}) on devices 0..M−1; a mini-batch is split into m
- * micro-batches, stage times ⌈ΣΔ/m⌉; the activations of a micro-batch from
+ * micro-batches, stage times ⌈ΣΔ/m⌉ + n_s·overhead_ps (n_s ops in the stage; a
+ * fixed per-op cost every micro-batch pays — the "kernel overheads" of
+ * PAPER.md:299, reading R27; 0 = none); the activations of a micro-batch from
  * stage a to b travel as one transfer ⌈D_ab·10^12/(m·BW)⌉ + L (uniform link);
  * forward micro-batches in order, then the backward in reverse order; the
  * makespan is the last stage's finish.  Candidates: index = rank·nm + j, rank
@@ -236,13 +238,13 @@ int pp_pipeline_space(const pp_dfg *dfg, int M, int nm, uint64_t *count);
 /* Candidates [begin, end): d_best (device ptr uint64[2] = {makespan, index},
  * lexicographic argmin) and/or d_makespan (device ptr uint64 [end−begin]).
  * micro: host ptr uint32 [nm].  Asynchronous.                               */
-int pp_pipeline_range(const pp_dfg *dfg, int M, const uint32_t *micro, int nm, uint64_t begin, uint64_t end,
-                      uint64_t *d_best, uint64_t *d_makespan, void *cuda_stream);
+int pp_pipeline_range(const pp_dfg *dfg, int M, const uint32_t *micro, int nm, uint64_t overhead_ps,
+                      uint64_t begin, uint64_t end, uint64_t *d_best, uint64_t *d_makespan, void *cuda_stream);
 /* The whole space; fills *out (host ptr) with the winner's cuts.
  * Synchronises cuda_stream.  PP_E_INFEASIBLE if every stage split violates
  * the memory cap.                                                           */
-int pp_pipeline_search(const pp_dfg *dfg, int M, const uint32_t *micro, int nm, void *cuda_stream,
-                       pp_pipeline_result *out);
+int pp_pipeline_search(const pp_dfg *dfg, int M, const uint32_t *micro, int nm, uint64_t overhead_ps,
+                       void *cuda_stream, pp_pipeline_result *out);
 
 /* ----------------------------------------- EFT base seed (§8(f) f4) --
  * The earliest-finish-time greedy placement (SPEC.md:245–253

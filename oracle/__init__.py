@@ -121,10 +121,11 @@ def lib():
                                      C.c_uint64, C.c_uint64]
         L.or_round_exact.restype = _Best
         L.or_eft_orig.argtypes = [C.c_void_p, C.c_int, P(C.c_uint8)]
-        L.or_pipeline.argtypes = [C.c_void_p, C.c_int, P(C.c_int32), C.c_uint32]
-        L.or_pipeline.restype = C.c_uint64
-        L.or_pipeline_search.argtypes = [C.c_void_p, C.c_int, P(C.c_uint32), C.c_int, C.c_uint64, C.c_uint64]
-        L.or_pipeline_search.restype = _Best
+        L.or_pipeline_ex.argtypes = [C.c_void_p, C.c_int, P(C.c_int32), C.c_uint32, C.c_uint64]
+        L.or_pipeline_ex.restype = C.c_uint64
+        L.or_pipeline_search_ex.argtypes = [C.c_void_p, C.c_int, P(C.c_uint32), C.c_int, C.c_uint64, C.c_uint64,
+                                            C.c_uint64]
+        L.or_pipeline_search_ex.restype = _Best
         L.or_shard_bytes.argtypes = [C.c_void_p, C.c_int, P(C.c_uint8), P(C.c_uint64)]
         L.or_mix.argtypes = [C.c_uint64]; L.or_mix.restype = C.c_uint64
         L.or_gen.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint32, P(C.c_uint8),
@@ -266,17 +267,19 @@ class Dfg:
             raise OracleError(rc)
         return [int(x) for x in out]
 
-    def pipeline(self, M: int, cuts, micro: int) -> int:
+    def pipeline(self, M: int, cuts, micro: int, overhead=0) -> int:
         """NEXT f3: GPipe makespan of stages cut at π positions `cuts` (M−1
-        increasing values in 1..K−1) with `micro` micro-batches."""
+        increasing values in 1..K−1) with `micro` micro-batches and a per-op
+        per-micro-batch overhead (ps)."""
         cu = np.ascontiguousarray(np.asarray(list(cuts) + [0], dtype=np.int32))
-        return int(lib().or_pipeline(self._h, M, cu.ctypes.data_as(C.POINTER(C.c_int32)), micro))
+        return int(lib().or_pipeline_ex(self._h, M, cu.ctypes.data_as(C.POINTER(C.c_int32)), micro, overhead))
 
-    def pipeline_search(self, M: int, micro, begin=0, end=None):
+    def pipeline_search(self, M: int, micro, begin=0, end=None, overhead=0):
         """(makespan, index) over candidates [begin, end), index = rank·len(micro) + j."""
         mi = np.ascontiguousarray(np.asarray(micro, dtype=np.uint32))
         end = (1 << 64) - 1 if end is None else end
-        r = lib().or_pipeline_search(self._h, M, mi.ctypes.data_as(C.POINTER(C.c_uint32)), len(mi), begin, end)
+        r = lib().or_pipeline_search_ex(self._h, M, mi.ctypes.data_as(C.POINTER(C.c_uint32)), len(mi), begin, end,
+                                        overhead)
         return int(r.makespan), int(r.index)
 
     def eft(self, M: int) -> np.ndarray:

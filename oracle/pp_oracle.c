@@ -641,7 +641,9 @@ int or_shard_bytes(const or_ctx *c, int M, const uint8_t *d_orig, uint64_t *out8
  *   stage s = π positions [cut_s, cut_{s+1}), cut_0 = 0 < cut_1 < … < cut_M = K,
  *     on device s (π is topological, so every edge goes to the same or a
  *     later stage);
- *   per micro-batch: tf_s = ⌈Σ_{p∈s} Δf(p) / m⌉, tb_s = ⌈Σ Δb / m⌉;
+ *   per micro-batch: tf_s = ⌈Σ_{p∈s} Δf(p) / m⌉ + n_s·o, tb_s = ⌈Σ Δb / m⌉ + n_s·o
+ *     (n_s ops in the stage; o = a fixed per-op cost each micro-batch pays,
+ *     the "kernel overheads" of PAPER.md:299, reading R27; o = 0 by default);
  *   a → b (a < b) carries the micro-batch's activations of every edge from a
  *     to b as one transfer of ⌈D_ab·10^12 / (m·BW)⌉ + L ps (D_ab = Σ D_f), the
  *     gradients back from b to a likewise with Σ D_b; no edge, no transfer;
@@ -652,7 +654,7 @@ int or_shard_bytes(const or_ctx *c, int M, const uint8_t *d_orig, uint64_t *out8
  *     B[s][m] := F[s][m−1]   (each device runs its ops one at a time)
  *   makespan = max_s B[s][0]; a stage whose Σ M(k) exceeds the cap makes the
  *   pipeline infeasible.                                 */
-uint64_t or_pipeline(const or_ctx *c, int M, const int32_t *cuts, uint32_t m) {
+uint64_t or_pipeline_ex(const or_ctx *c, int M, const int32_t *cuts, uint32_t m, uint64_t o) {
     int K = c->K;
     if (M < 1 || M > 8 || M > K || m < 1 || m > 65536 || c->nd) return OR_INFEASIBLE_MAKESPAN;  /* invalid */
     for (int s = 0; s < M - 1; s++)
@@ -667,8 +669,9 @@ uint64_t or_pipeline(const or_ctx *c, int M, const int32_t *cuts, uint32_t m) {
         u128 sf = 0, sb = 0, mem = 0;
         for (int p = st[s]; p < st[s + 1]; p++) { sf += c->df[p]; sb += c->db[p]; mem += c->mem[p]; }
         if (c->cap > 0 && mem > c->cap) { free(stage_of); return OR_INFEASIBLE_MAKESPAN; }
-        tf[s] = (uint64_t)((sf + m - 1) / m);
-        tb[s] = (uint64_t)((sb + m - 1) / m);
+        uint64_t n_s = (uint64_t)(st[s + 1] - st[s]);
+        tf[s] = (uint64_t)((sf + m - 1) / m) + n_s * o;
+        tb[s] = (uint64_t)((sb + m - 1) / m) + n_s * o;
     }
     u128 Df[8][8], Db[8][8];
     int has[8][8];
@@ -711,11 +714,15 @@ uint64_t or_pipeline(const or_ctx *c, int M, const int32_t *cuts, uint32_t m) {
     return mk;
 }
 
+uint64_t or_pipeline(const or_ctx *c, int M, const int32_t *cuts, uint32_t m) {
+    return or_pipeline_ex(c, M, cuts, m, 0);
+}
+
 /* Exhaustive pipeline search: cut vectors in lexicographic order (rank r),
  * micro-batch counts micro[0..nm−1]; candidate index = r·nm + j.  Returns the
  * lexicographically smallest (makespan, index) over [begin, end).            */
-or_best or_pipeline_search(const or_ctx *c, int M, const uint32_t *micro, int nm,
-                           uint64_t begin, uint64_t end) {
+or_best or_pipeline_search_ex(const or_ctx *c, int M, const uint32_t *micro, int nm,
+                              uint64_t begin, uint64_t end, uint64_t o) {
     or_best best = { UINT64_MAX, UINT64_MAX };
     if (M < 1 || M > 8 || M > c->K || nm < 1) return best;
     /* start at the first rank touching [begin, end): unrank it (combinatorial
@@ -745,7 +752,7 @@ or_best or_pipeline_search(const or_ctx *c, int M, const uint32_t *micro, int nm
         for (int j = 0; j < nm; j++) {
             uint64_t idx = r * (uint64_t)nm + (uint64_t)j;
             if (idx >= begin && idx < end) {
-                uint64_t mk = or_pipeline(c, M, cuts, micro[j]);
+                uint64_t mk = or_pipeline_ex(c, M, cuts, micro[j], o);
                 if (mk < best.makespan || (mk == best.makespan && idx < best.index)) {
                     best.makespan = mk; best.index = idx;
                 }
@@ -761,6 +768,10 @@ or_best or_pipeline_search(const or_ctx *c, int M, const uint32_t *micro, int nm
         if (r * (uint64_t)nm >= end) break;
     }
     return best;
+}
+
+or_best or_pipeline_search(const or_ctx *c, int M, const uint32_t *micro, int nm, uint64_t begin, uint64_t end) {
+    return or_pipeline_search_ex(c, M, micro, nm, begin, end, 0);
 }
 
 /* ------------------------------------------------------- O5 / O6 generators */

@@ -611,8 +611,8 @@ int pp_pipeline_space(const pp_dfg *g, int M, int nm, uint64_t *count) {
     return PP_OK;
 }
 
-int pp_pipeline_range(const pp_dfg *gc, int M, const uint32_t *micro, int nm, uint64_t begin, uint64_t end,
-                      uint64_t *d_best, uint64_t *d_makespan, void *stream) {
+int pp_pipeline_range(const pp_dfg *gc, int M, const uint32_t *micro, int nm, uint64_t overhead_ps, uint64_t begin,
+                      uint64_t end, uint64_t *d_best, uint64_t *d_makespan, void *stream) {
     int rc = pipe_check(gc, M, micro, nm);
     if (rc) return rc;
     uint64_t space = 0;
@@ -645,6 +645,7 @@ int pp_pipeline_range(const pp_dfg *gc, int M, const uint32_t *micro, int nm, ui
     p.end = end;
     p.K = (uint32_t)g->K;
     p.nm = (uint32_t)nm;
+    p.overhead = overhead_ps;
     for (int j = 0; j < nm; j++) p.micro[j] = micro[j];
     const int threads = 256;
     const uint64_t ranks = (end + nm - 1) / nm - begin / nm;
@@ -661,7 +662,7 @@ int pp_pipeline_range(const pp_dfg *gc, int M, const uint32_t *micro, int nm, ui
     return PP_OK;
 }
 
-int pp_pipeline_search(const pp_dfg *g, int M, const uint32_t *micro, int nm, void *stream,
+int pp_pipeline_search(const pp_dfg *g, int M, const uint32_t *micro, int nm, uint64_t overhead_ps, void *stream,
                        pp_pipeline_result *out) {
     if (!out) { set_error("out is NULL"); return PP_E_INVALID; }
     int rc = pipe_check(g, M, micro, nm);
@@ -671,7 +672,7 @@ int pp_pipeline_search(const pp_dfg *g, int M, const uint32_t *micro, int nm, vo
     DeviceGuard dg(g->device);
     if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
     uint64_t *d_best = g->d_scalars + 32;    // scratch slots 32, 33
-    if ((rc = pp_pipeline_range(g, M, micro, nm, 0, space, d_best, nullptr, stream))) return rc;
+    if ((rc = pp_pipeline_range(g, M, micro, nm, overhead_ps, 0, space, d_best, nullptr, stream))) return rc;
     uint64_t best[2];
     cudaError_t ce;
     if ((ce = cudaMemcpyAsync(best, d_best, sizeof best, cudaMemcpyDeviceToHost, (cudaStream_t)stream)) !=

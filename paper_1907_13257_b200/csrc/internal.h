@@ -161,6 +161,7 @@ struct PipeParams {
     unsigned *g_ticket;
     uint64_t *g_out;             // {makespan, index} or null
     uint64_t bw, lat, cap, begin, end, block;
+    uint64_t overhead;           // per op per micro-batch (ps)
     uint32_t K, nm;
     uint32_t micro[16];
 };

@@ -104,8 +104,9 @@ __global__ void __launch_bounds__(256) pipeline_kernel(const PipeParams P) {
                     uint64_t tf[M], tb[M], cf[M][M], cb[M][M];
 #pragma unroll
                     for (int s = 0; s < M; s++) {
-                        tf[s] = (sf[s] + m - 1) / m;
-                        tb[s] = (sb[s] + m - 1) / m;
+                        const uint64_t ov = (uint64_t)(st[s + 1] - st[s]) * P.overhead;
+                        tf[s] = (sf[s] + m - 1) / m + ov;
+                        tb[s] = (sb[s] + m - 1) / m + ov;
                     }
                     const u128 den = (u128)m * P.bw;
 #pragma unroll

@@ -112,10 +112,10 @@ SIGNATURES = {
     "pp_search_exact": ([C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint64,
                          C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
     "pp_pipeline_space": ([C.c_void_p, C.c_int, C.c_int, P(C.c_uint64)], C.c_int),
-    "pp_pipeline_range": ([C.c_void_p, C.c_int, P(C.c_uint32), C.c_int, C.c_uint64, C.c_uint64, C.c_void_p,
-                           C.c_void_p, C.c_void_p], C.c_int),
-    "pp_pipeline_search": ([C.c_void_p, C.c_int, P(C.c_uint32), C.c_int, C.c_void_p, P(PipelineResultC)],
-                           C.c_int),
+    "pp_pipeline_range": ([C.c_void_p, C.c_int, P(C.c_uint32), C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                           C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "pp_pipeline_search": ([C.c_void_p, C.c_int, P(C.c_uint32), C.c_int, C.c_uint64, C.c_void_p,
+                            P(PipelineResultC)], C.c_int),
     "pp_shard_bytes": ([C.c_void_p, C.c_int, P(C.c_uint8), P(C.c_uint64)], C.c_int),
     "pp_eft_place": ([C.c_void_p, C.c_int, P(C.c_uint8), C.c_void_p], C.c_int),
     "pp_search_best": ([C.c_void_p, C.c_int, P(SearchDesc), C.c_void_p, C.c_void_p, P(SearchResultC)], C.c_int),
@@ -306,14 +306,15 @@ class Dfg:
         _check(lib().pp_pipeline_space(self._h, M, nm, C.byref(c)))
         return int(c.value)
 
-    def pipeline_search(self, M, micro, stream=None) -> dict:
+    def pipeline_search(self, M, micro, overhead=0, stream=None) -> dict:
         mi = np.ascontiguousarray(np.asarray(micro, dtype=np.uint32))
         r = PipelineResultC()
-        _check(lib().pp_pipeline_search(self._h, M, _ptr(mi, C.c_uint32), len(mi), _stream(stream), C.byref(r)))
+        _check(lib().pp_pipeline_search(self._h, M, _ptr(mi, C.c_uint32), len(mi), overhead, _stream(stream),
+                                        C.byref(r)))
         return {"makespan_ps": int(r.makespan_ps), "index": int(r.index), "candidates": int(r.candidates),
                 "micro_batches": int(r.micro_batches), "cuts": [int(x) for x in r.cuts[:M - 1]]}
 
-    def pipeline_range(self, M, micro, begin, end, all_values=False, stream=None):
+    def pipeline_range(self, M, micro, begin, end, all_values=False, overhead=0, stream=None):
         """(makespan, index) argmin over [begin, end) — and the per-candidate
         makespans (int64 CUDA tensor) when all_values."""
         import torch
@@ -321,8 +322,8 @@ class Dfg:
         mi = np.ascontiguousarray(np.asarray(micro, dtype=np.uint32))
         best = torch.empty(2, dtype=torch.int64, device=dev)
         vals = torch.empty(end - begin, dtype=torch.int64, device=dev) if all_values else None
-        _check(lib().pp_pipeline_range(self._h, M, _ptr(mi, C.c_uint32), len(mi), begin, end, _dptr(best),
-                                       _dptr(vals), _stream(stream)))
+        _check(lib().pp_pipeline_range(self._h, M, _ptr(mi, C.c_uint32), len(mi), overhead, begin, end,
+                                       _dptr(best), _dptr(vals), _stream(stream)))
         b = u64(best)
         return (int(b[0]), int(b[1])), vals
 

@@ -76,3 +76,20 @@ def test_errors():
         g.pipeline_search(13, MICRO)            # more stages than ops
     with pytest.raises(pp.PPError):
         g.pipeline_search(2, [0])
+
+
+@pytest.mark.parametrize("overhead", [1, 5_000_000])
+def test_op_overhead(overhead):
+    spec = synth.gnmt()
+    g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
+    for M in (2, 3):
+        r = g.pipeline_search(M, MICRO, overhead=overhead)
+        assert (r["makespan_ps"], r["index"]) == od.pipeline_search(M, MICRO, overhead=overhead)
+    small = synth.random_dag(1900, 9, max_cost=10**4, max_bytes=10**5, bw=10**11, lat_max=100, window=4)
+    g, od = pp.Dfg(small), O.Dfg.from_spec(small)
+    n = g.pipeline_space(3, 4)
+    _, vals = g.pipeline_range(3, [1, 2, 3, 5], 0, n, all_values=True, overhead=overhead)
+    combos = list(itertools.combinations(range(1, 9), 2))
+    want = np.array([od.pipeline(3, list(combos[i // 4]), [1, 2, 3, 5][i % 4], overhead=overhead) for i in range(n)],
+                    dtype=np.uint64)
+    assert np.array_equal(pp.u64(vals), want)

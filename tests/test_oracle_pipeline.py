@@ -93,3 +93,25 @@ def test_range_start_unranking(K, M):
         for j, m in enumerate(micro):
             idx = 2 * i + j
             assert od.pipeline_search(M, micro, idx, idx + 1) == (od.pipeline(M, list(cuts), m), idx)
+
+
+@pytest.mark.parametrize("M,m,o", [(2, 4, 5), (4, 8, 1), (3, 6, 100)])
+def test_bubble_closed_form_with_op_overhead(M, m, o):
+    # reading R27: every op pays o per micro-batch; on the uniform chain the
+    # stage times grow by q·o and the bubble formula still holds
+    q, d = 3, 48
+    spec = synth.chain(M * q, d, 2 * d, 0, lat=0)
+    od = O.Dfg.from_spec(spec)
+    cuts = [q * s for s in range(1, M)]
+    tf, tb = q * d // m + q * o, q * 2 * d // m + q * o
+    assert od.pipeline(M, cuts, m, overhead=o) == (m + M - 1) * (tf + tb)
+    assert od.pipeline(M, cuts, m, overhead=0) == od.pipeline(M, cuts, m)
+
+
+def test_overhead_makes_many_micro_batches_lose():
+    # with a per-op overhead the best micro-batch count is finite
+    od = O.Dfg.from_spec(synth.gnmt())
+    micro = [1, 2, 4, 8, 16, 32]
+    _, idx0 = od.pipeline_search(2, micro)
+    _, idx1 = od.pipeline_search(2, micro, overhead=20_000_000)     # 20 µs per op per micro-batch
+    assert micro[idx0 % 6] == 32 and micro[idx1 % 6] < 32
