@@ -195,10 +195,14 @@ static void fill(const pp_dfg *g, const Choice &best, uint64_t begin, uint64_t e
     p.g_out = g->d_scalars + SC_LOCAL_MK;
 }
 
-// Placements per lane (NP) for the argmin kernels is chosen by MEASUREMENT:
-// the first search call for a (DFG, M, generator) times each NP variant (its
-// best CTA shape) on the same probe range and keeps the fastest.  The result
-// does not depend on the choice (every variant is bit-exact), only the speed.
+// Placements per lane (NP).  A rule fitted to the measured configurations
+// (profiles/r01_np_rule.txt): with M ≤ 2 the most placements
+// in flight (warps × NP, ties to more warps); with M ≥ 3, whose free[] lives
+// in shared memory, the largest NP that keeps 20 warps per SM resident, else
+// the most resident warps.
+// PP_AUTOTUNE=1 instead times every NP variant on a probe range on the first
+// call for a (DFG, M, generator) and keeps the fastest.  The result never
+// depends on the choice (every variant is bit-exact), only the speed.
 // The per-candidate (write-all) kernels are built for NP = 2 only.
 static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin, uint64_t end, Launch &L,
                  void *stream = nullptr) {
@@ -219,12 +223,28 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
         return PP_E_TOO_LARGE;
     }
     size_t pick = 0;
+    auto warps = [&](size_t i) { return (long)cands[i].ctas * cands[i].threads / 32; };
+    if (M <= 2) {
+        for (size_t i = 1; i < cands.size(); i++) {
+            const long a = warps(i) * cands[i].np, b = warps(pick) * cands[pick].np;
+            if (a > b || (a == b && warps(i) > warps(pick))) pick = i;
+        }
+    } else {
+        constexpr long kWarpTarget = 20;   // 5 per scheduler
+        bool found = false;
+        for (size_t i = 0; i < cands.size() && !found; i++)   // NP = 4, 2, 1 in order
+            if (warps(i) >= kWarpTarget) { pick = i; found = true; }
+        if (!found)
+            for (size_t i = 1; i < cands.size(); i++)
+                if (warps(i) > warps(pick)) pick = i;
+    }
     const int key = (M << 8) | (gen << 4) | (write_all ? 1 : 0);
     auto it = g->tuned.find(key);
-    if (cands.size() > 1 && it != g->tuned.end()) {
+    const bool autotune = getenv("PP_AUTOTUNE") != nullptr;
+    if (autotune && cands.size() > 1 && it != g->tuned.end()) {
         for (size_t i = 0; i < cands.size(); i++)
             if (cands[i].np == it->second) pick = i;
-    } else if (cands.size() > 1) {
+    } else if (autotune && cands.size() > 1) {
         // probe: the same candidate range for every variant, long enough to
         // fill the GPU a few times; each variant runs twice (the first run
         // absorbs module loading), the second is timed
