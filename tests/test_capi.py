@@ -43,6 +43,42 @@ def test_struct_sizes(pp):
     assert C.sizeof(pp.pp.CrossoverC) == 76
 
 
+# every C-ABI struct the binding mirrors: (C typedef, ctypes class name)
+STRUCTS = [("pp_dfg_desc", "DfgDesc"), ("pp_link_desc", "LinkDesc"), ("pp_hw_desc", "HwDesc"),
+           ("pp_dfg_info", "DfgInfo"), ("pp_search_desc", "SearchDesc"), ("pp_search_result", "SearchResultC"),
+           ("pp_pipeline_result", "PipelineResultC"), ("pp_scenario", "Scenario"), ("pp_cell", "Cell"),
+           ("pp_crossover_result", "CrossoverC")]
+
+
+def test_struct_layout_matches_header(pp, tmp_path):
+    """gcc compiles include/pp.h and prints sizeof / offsetof of every field of
+    every struct; the ctypes mirrors in pp.py must agree byte for byte."""
+    import ctypes as C
+    import subprocess
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "pp.h"', "int main(void) {"]
+    for cname, pyname in STRUCTS:
+        cls = getattr(pp.pp, pyname)
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f in cls._fields_:
+            lines.append(f'  printf("{cname} {f[0]} %zu\\n", offsetof({cname}, {f[0]}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = subprocess.check_output([str(exe)], text=True).split("\n")
+    got = {}
+    for line in out:
+        if line:
+            a, b, v = line.split()
+            got[(a, b)] = int(v)
+    for cname, pyname in STRUCTS:
+        cls = getattr(pp.pp, pyname)
+        assert got[(cname, "size")] == C.sizeof(cls), cname
+        for f in cls._fields_:
+            assert got[(cname, f[0])] == getattr(cls, f[0]).offset, (cname, f[0])
+
+
 def test_rank_slices_partition(pp):
     for count in (1, 7, 8, 1000, 10**8, 2**63 + 5):
         for world in range(1, 9):
