@@ -65,7 +65,10 @@ struct OpRec {
     uint32_t out_off;     // region byte offset of the output slot, or kNoStore
     uint32_t ctrl;        // 0: fast chain step (first input = previous step, no extras);
                           // else 0x10000 | n_extra (further inputs, ExtraRec in order)
-    uint32_t base;        // PERTURB base device of this op (patched every round)
+    uint32_t base;        // PERTURB base (patched every round): bits 0..2 the base device
+                          // of this op; bits 7, 15, 23, 31 bit 0 of the base devices of
+                          // the 4 ops of its half-group (π positions 4h..4h+3), read by
+                          // the M = 2 cut-word schedule (search_kernel.cuh)
 };
 static_assert(sizeof(OpRec) == 32, "OpRec is 32 B");
 
@@ -75,6 +78,22 @@ struct ExtraRec {
     uint32_t pad;
 };
 static_assert(sizeof(ExtraRec) == 16, "ExtraRec is 16 B");
+
+// The packed half-group word of π position p: bit 8c+7 = bit 0 of the base
+// device of position 4⌊p/4⌋ + c (positions ≥ K, the no-op pads, count as 0).
+#ifdef __CUDACC__
+__host__ __device__ __forceinline__
+#else
+inline
+#endif
+uint32_t half_group_word(const uint8_t *base, uint32_t p, uint32_t K) {
+    uint32_t w = 0;
+    for (uint32_t c = 0; c < 4; c++) {
+        const uint32_t q = (p & ~3u) + c;
+        if (q < K) w |= (uint32_t)(base[q] & 1u) << (8 * c + 7);
+    }
+    return w;
+}
 
 enum GenKind : int { GEN_GRAY = 0, GEN_RANDOM = 1, GEN_PERTURB = 2, GEN_EXPLICIT = 3 };
 

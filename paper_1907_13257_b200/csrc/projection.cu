@@ -266,18 +266,20 @@ __global__ void contrib_kernel(uint64_t *s, int rank) {
     s[SC_IDX_LOCAL] = ((int)(s[SC_KEY_GLOBAL] & 7) == rank) ? s[SC_LOCAL_IDX] : ~0ull;
 }
 // Copies a π-order base into the canonical buffer and into OpRec.base of the
-// forward and backward records of every op (PERTURB).
+// forward and backward records of every position p < K8 (PERTURB): the op's
+// device plus the packed half-group word (internal.h, OpRec.base).
 __global__ void patch_base_kernel(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8) {
     OpRec *ops = reinterpret_cast<OpRec *>(image);
-    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < K; p += gridDim.x * blockDim.x) {
-        uint8_t d = src[p];
-        base[p] = d;
-        ops[p].base = d;
-        ops[2 * K8 - 1 - p].base = d;
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < K8; p += gridDim.x * blockDim.x) {
+        const uint8_t d = p < K ? src[p] : 0;
+        if (p < K) base[p] = d;
+        const uint32_t w = half_group_word(src, p, K);
+        ops[p].base = d | w;
+        ops[2 * K8 - 1 - p].base = d | w;
     }
 }
 int launch_patch_base(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8, void *stream) {
-    patch_base_kernel<<<(K + 255) / 256, 256, 0, (cudaStream_t)stream>>>(image, base, src, K, K8);
+    patch_base_kernel<<<(K8 + 255) / 256, 256, 0, (cudaStream_t)stream>>>(image, base, src, K, K8);
     return (int)cudaGetLastError();
 }
 int launch_pack_key(uint64_t *s, int rank, void *stream) {

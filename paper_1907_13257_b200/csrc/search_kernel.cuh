@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstddef>
 #include <type_traits>
 
 #include "internal.h"
@@ -197,6 +198,7 @@ struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops
     // cc = position within the half-group (compile-time in the schedule loop)
     __device__ __forceinline__ uint32_t dev(int k, uint32_t, uint32_t cc, uint32_t bs) const {
         if (M == 1) return 0;
+        bs &= 7u;   // bits 7..31 of OpRec.base hold the M = 2 half-group word
         const uint32_t u = __byte_perm(uh[k], 0, 0x4440u | (cc & 3u));
         if (M == 2) {
             // device = base + [u < τ], read modulo 2 (see Dev<M>): one PRMT and a sign bit
@@ -650,10 +652,193 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
     }
 }
 
+// ------------------------------- M = 2 PERTURB: cut words (tagged f64)
+// The same schedule as schedule_f64<2> for the PERTURB generator, with the
+// devices of a half-group (4 ops) decided at once.  Per placement and
+// half-group, with the 4 PERTURB bytes u_c of the half-group in one word:
+//   flip_c = [u_c < τ]                  — 4 byte compares in 4 SIMD-within-a-
+//                                          register ops (bit 7 of byte c)
+//   dev_c  = flip_c ⊕ base_c            — the packed base word of the image
+//   cut_c  = dev_c ⊕ dev of the previous scheduled step   (one PRMT, one XOR)
+// and per step the cut flag is widened to a full-word mask by one PRMT
+// (sign replication of byte c).  The byte compare, with τ' = τ (τ ≤ 128) or
+// τ − 128 (τ > 128) in every byte and x = (u | 0x80…) − τ' (no borrow crosses
+// a byte; bit 7 of byte c of x is [u_c mod 128 ≥ τ']):
+//   τ ≤ 128:  u_c < τ  ⟺  ¬(u_c,7 ∨ x_c,7)
+//   τ > 128:  u_c < τ  ⟺  ¬(u_c,7 ∧ x_c,7)
+// — both ¬MAJ(u, x, A) with A = all ones (τ ≤ 128) or zero (τ > 128).
+// Candidate 0 (the base) masks its flips to zero.  The arithmetic is
+// schedule_f64's, operation for operation; only the cut flags are derived
+// differently, so the results are identical (the parity suite checks both).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return d;
+}
+
+// The PERTURB words of this lane's placements i_k =
+// i_0 + 32k: word g of placement i is mix64(key(i) + γ·g) with key(i) =
+// (seed ⊕ C1) + γ·(i·Wd + 1), i.e. mix64(A_g + k·Δ) with A_g = key(i_0) + γ·g
+// (one running 64-bit value per lane) and Δ = γ·32·Wd (uniform).
+template <int NP, bool MEM>
+__device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t hk0, uint64_t (&mk)[NP], uint32_t ops,
+                                             uint32_t xr, const uint64_t *__restrict__ mem, uint32_t lane, uint32_t K8,
+                                             uint64_t cap, uint32_t khi, uint32_t tau) {
+    constexpr uint32_t H = 0x80808080u;
+    const uint32_t tq = (tau <= 128 ? tau : tau - 128) * 0x01010101u;
+    const uint32_t amaj = tau <= 128 ? ~0u : 0u;
+    double prev[NP], oth[NP];
+    uint32_t dw[NP], cw[NP], dprev[NP];
+    uint64_t w[NP];
+    MemUse<2> mu[NP];
+#pragma unroll
+    for (int k = 0; k < NP; k++) {
+        prev[k] = 0.0;
+        oth[k] = 0.0;
+        dprev[k] = 0;                  // device 0 before the first step (schedule_f64's pdev = 0)
+        dw[k] = cw[k] = 0;
+        w[k] = 0;
+        if (MEM) mu[k].init();
+    }
+    uint32_t x = xr;
+    auto refresh = [&]() {
+#pragma unroll
+        for (int k = 0; k < NP; k++) w[k] = mix64(A + (uint64_t)k * dA);
+    };
+
+    // the device and cut words of half-group h of the current group, whose
+    // records carry the packed base word `bw`
+    auto half = [&](uint32_t h, uint32_t bw, bool fwd) {
+        const uint32_t bsw = bw & H;
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            const uint32_t u = h ? (uint32_t)(w[k] >> 32) : (uint32_t)w[k];
+            const uint32_t y = (u | H) - tq;
+            const uint32_t mj = lop3<0xE8>(u, y, amaj);                 // MAJ(u, y, A)
+            dw[k] = lop3<0x9A>(k == 0 ? hk0 : H, mj, bsw);            // (hk ∧ ¬mj) ⊕ bsw
+            // the previous scheduled step's device, byte-aligned with dev_c:
+            // forward (c − 1; c = 0 takes byte 3 of the previous half-group),
+            // backward (c + 1; c = 3 takes byte 0 of the previous half-group)
+            const uint32_t sh = fwd ? prmt(dw[k], dprev[k], 0x2107u) : prmt(dw[k], dprev[k], 0x4321u);
+            cw[k] = dw[k] ^ sh;
+            dprev[k] = dw[k];
+        }
+    };
+
+    auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
+        const uint4 a = lds128(rec);
+        const uint4 b = lds128(rec + 16);
+        const double cost = __hiloint2double((int)a.y, (int)a.x);
+        const double c0 = __hiloint2double((int)a.w, (int)a.z);
+        uint32_t m[NP];
+        double cut[NP];
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            m[k] = prmt(cw[k], 0u, 0x8888u | (c * 0x1111u));    // all ones iff cut_c
+            cut[k] = __hiloint2double((int)(m[k] & khi), 0);   // 1.0 or 0.0
+        }
+        if (b.z == 0) {
+            // chain step: s = max(prev + cut·c0, cut·oth), oth' = cut ? prev : oth
+#pragma unroll
+            for (int k = 0; k < NP; k++) {
+                const double t = __fma_rn(c0, cut[k], prev[k]);
+                const double s = dmax(t, __dmul_rn(cut[k], oth[k]));
+                oth[k] = __fma_rn(cut[k], __dadd_rn(prev[k], -oth[k]), oth[k]);
+                prev[k] = __dadd_rn(s, cost);
+            }
+        } else {
+            double r[NP];
+            if (b.x == kFromPrev) {
+#pragma unroll
+                for (int k = 0; k < NP; k++) r[k] = __fma_rn(c0, cut[k], prev[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NP; k++)
+                    r[k] = cut_add_f64<2>(ldd(lane + b.x * NP + k * 256), dw[k] >> (8 * c + 7), c0, khi);
+            }
+            const uint32_t nx = b.z & 0xFFFFu;
+#pragma unroll 1
+            for (uint32_t q = 0; q < nx; q++) {   // further inputs (uniform trip count)
+                const uint4 e = lds128(x);
+                x += sizeof(ExtraRec);
+                const double ce = __hiloint2double((int)e.y, (int)e.x);
+#pragma unroll
+                for (int k = 0; k < NP; k++)
+                    r[k] = dmax(r[k], cut_add_f64<2>(ldd(lane + e.z * NP + k * 256), dw[k] >> (8 * c + 7), ce, khi));
+            }
+#pragma unroll
+            for (int k = 0; k < NP; k++) {
+                // free[dev] = cut ? oth : prev
+                const double d = __dadd_rn(prev[k], -oth[k]);
+                const double f = __fma_rn(-cut[k], d, prev[k]);
+                oth[k] = __fma_rn(cut[k], d, oth[k]);
+                prev[k] = __dadd_rn(clear_tag(dmax(r[k], f)), cost);
+            }
+        }
+        if (b.y != kNoStore) {
+#pragma unroll
+            for (int k = 0; k < NP; k++) std_(lane + b.y * NP + k * 256, with_tag(prev[k], (dw[k] >> (8 * c + 7)) & 1u));
+        }
+        if (MEM && fwd) {
+            const uint64_t mm = mem[p];
+#pragma unroll
+            for (int k = 0; k < NP; k++) mu[k].add((dw[k] >> (8 * c + 7)) & 1u, mm);
+        }
+    };
+    constexpr int kHalfUnroll = NP >= 4 ? 1 : 2;
+    const uint32_t G = K8 / 8;
+    for (uint32_t g = 0; g < G; g++) {           // forward, π order
+        refresh();
+        A += kGamma;
+#pragma unroll (kHalfUnroll)
+        for (uint32_t h = 0; h < 2; h++) {
+            const uint32_t rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
+            half(h, lds32(rec + offsetof(OpRec, base)), true);
+#pragma unroll
+            for (uint32_t cc = 0; cc < 4; cc++) step(rec + cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, true);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NP; k++) dprev[k] >>= 24;   // byte 0 := the device of the last forward step
+    for (uint32_t g = G; g-- > 0;) {             // backward, reverse π order
+        A -= kGamma;
+        refresh();
+#pragma unroll (kHalfUnroll)
+        for (uint32_t h = 2; h-- > 0;) {
+            const uint32_t rec = ops + (2 * K8 - 1 - g * 8 - h * 4) * (uint32_t)sizeof(OpRec);
+            half(h, lds32(rec + offsetof(OpRec, base)), false);
+#pragma unroll
+            for (int cc = 3; cc >= 0; cc--)
+                step(rec - (uint32_t)cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, false);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NP; k++) {
+        mk[k] = (uint64_t)__double2ull_rz(dmax(prev[k], oth[k]));
+        if (MEM && mu[k].over(cap)) mk[k] = kInfeasible;
+    }
+}
+
+#ifndef PP_M2P
+#define PP_M2P 1   // the cut-word schedule for M = 2 PERTURB (0: schedule_f64, for A/B)
+#endif
+
 template <int M, int NP, bool MEM, bool F64, bool HW, class Gen>
 __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[NP], uint32_t ops, uint32_t xr,
                                             const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
-                                            uint32_t K8, uint64_t cap, uint32_t khi, uint32_t cls) {
+                                            uint32_t K8, uint64_t cap, uint32_t khi, uint32_t cls, uint32_t tau) {
     if constexpr (F64 && M >= 2) schedule_f64<M, NP, MEM, HW>(gen, mk, ops, xr, mem, lane, free_off, K8, cap, khi, cls);
     else schedule_gen<M, NP, MEM, F64>(gen, mk, ops, xr, mem, lane, free_off, K8, cap);
 }
@@ -719,6 +904,7 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
     bool have = false;
     const uint64_t n = P.end - P.begin;
     constexpr uint32_t TILE = 32 * NP;
+    constexpr bool kM2P = PP_M2P && F64 && M == 2 && !HW;   // schedule_m2p
     const uint64_t ntiles = (n + TILE - 1) / TILE;
     const uint64_t wpb = nthreads >> 5;
     for (uint64_t tile = blockIdx.x * wpb + warp; tile < ntiles; tile += (uint64_t)gridDim.x * wpb) {
@@ -735,24 +921,32 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
             GrayGen<M, NP> g;
             g.init(idx, P.K);
             schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
-                                              smem_base + P.off_cls);
+                                              smem_base + P.off_cls, P.tau);
         } else if (GEN == GEN_RANDOM) {
             RandomGen<M, NP> g;
             g.init(idx, P.seed, P.K);
             schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
-                                              smem_base + P.off_cls);
+                                              smem_base + P.off_cls, P.tau);
+        } else if constexpr (GEN == GEN_PERTURB && kM2P) {
+            // lane placements i_0 + 32k (unclamped: results of lanes past the
+            // end are discarded); only i = 0 can be candidate 0, the base
+            const uint64_t i0 = P.begin + tile * TILE + lane;
+            const uint64_t Wd = (P.K + 7) / 8;
+            const uint64_t A = (P.seed ^ 0xD1B54A32D192ED03ull) + kGamma * (i0 * Wd + 1);
+            schedule_m2p<NP, MEM>(A, kGamma * 32ull * Wd, i0 == 0 ? 0u : 0x80808080u, mk, ops, xr, mem, lane_region,
+                                  P.K8, P.cap, P.one_hi, P.tau);
         } else if (GEN == GEN_PERTURB) {
             PerturbGen<M, NP> g;
             g.init(idx, P.seed, P.K, P.tau);
             schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
-                                              smem_base + P.off_cls);
+                                              smem_base + P.off_cls, P.tau);
         } else {
             ExplicitGen<NP> g;
 #pragma unroll
             for (int k = 0; k < NP; k++) g.row[k] = P.g_place + (idx[k] - P.begin) * (uint64_t)P.K;
             g.orig = orig;
             schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
-                                              smem_base + P.off_cls);
+                                              smem_base + P.off_cls, P.tau);
         }
 #pragma unroll
         for (int k = 0; k < NP; k++) {
@@ -863,14 +1057,15 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
     }
     __syncthreads();
     OpRec *ops = reinterpret_cast<OpRec *>(U.image);
-    for (uint32_t p = threadIdx.x; p < U.K; p += blockDim.x) {
-        uint8_t d = U.winner[p];
+    for (uint32_t p = threadIdx.x; p < U.K8; p += blockDim.x) {
+        const uint8_t d = p < U.K ? U.winner[p] : 0;
         if (GEN == GEN_PERTURB) {
-            U.base[p] = d;
-            ops[p].base = d;
-            ops[2 * U.K8 - 1 - p].base = d;
+            const uint32_t w = half_group_word(U.winner, p, U.K);
+            if (p < U.K) U.base[p] = d;
+            ops[p].base = d | w;
+            ops[2 * U.K8 - 1 - p].base = d | w;
         }
-        if (improve) U.best_place[p] = d;
+        if (improve && p < U.K) U.best_place[p] = d;
     }
     if (threadIdx.x == 0 && improve) {
         s[SC_BEST_MK] = mk_s;

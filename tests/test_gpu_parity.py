@@ -331,3 +331,29 @@ def test_sharded_exact_and_pipeline_searches():
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("np_", ["1", "2", "4"])
+def test_perturb_m2_cut_words(dfgs, np_, monkeypatch):
+    """M = 2 PERTURB runs the cut-word schedule (search_kernel.cuh
+    schedule_m2p): 4 byte compares u < τ per SIMD word, whose two formulas
+    meet at τ = 128, a packed base word per half-group, and pads in the last
+    half-groups when K mod 8 ≠ 0.  Every τ boundary, a random base, begin = 0
+    (candidate 0 = the base itself) and both the per-candidate (write-all) and
+    the argmin kernels, against the oracle."""
+    monkeypatch.setenv("PP_NP", np_)
+    rng = np.random.default_rng(128)
+    cases = [dfgs["toy12"][1:], dfgs["inception_v3"][1:]]
+    for K in (13, 30):   # K mod 8 = 5 and 6: pad positions in the last half-groups
+        spec = synth.random_dag(4000 + K, K, avg_deg=1.6, max_cost=10**6, max_bytes=10**6)
+        cases.append((pp.Dfg(spec), O.Dfg.from_spec(spec)))
+    for g, od in cases:
+        base = rng.integers(0, 2, size=g.K, dtype=np.uint8)
+        for tau in (0, 1, 7, 8, 127, 128, 129, 200, 255, 256):
+            seed = int(rng.integers(0, 2**63))
+            got = pp.u64(g.eval_generated(2, pp.GEN_PERTURB, seed, tau, base, 0, 300))
+            want = _oracle_candidates(od, 2, O.GEN_PERTURB, seed, tau, base, range(300))
+            assert np.array_equal(got, want), (g.K, tau)
+            assert got[0] == od.makespan_pi(2, base)   # candidate 0 is the base
+            r = pp.u64(g.search_range(2, pp.GEN_PERTURB, seed, tau, base, 0, 1_000))
+            assert (int(r[0]), int(r[1])) == od.round(2, O.GEN_PERTURB, seed, tau, base, 0, 1_000), (g.K, tau)
