@@ -688,6 +688,18 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
     return d;
 }
 
+// m = all ones ? a : b, word by word (LOP3 on the ALU pipe)
+__device__ __forceinline__ double dsel(uint32_t m, double a, double b) {
+    return __hiloint2double((int)lop3<0xCA>(m, (uint32_t)__double2hiint(a), (uint32_t)__double2hiint(b)),
+                            (int)lop3<0xCA>(m, (uint32_t)__double2loint(a), (uint32_t)__double2loint(b)));
+}
+#ifndef PP_M2P_SEL
+#define PP_M2P_SEL 1   // oth / free[dev] by mask selects (ALU; A/B: -1.4% time) instead of DADD + DFMA (FP64)
+#endif
+#ifndef PP_M2P_STEPLOOP
+#define PP_M2P_STEPLOOP 0   // 1: the 4 steps of a half-group as a loop (smaller code) instead of unrolled
+#endif
+
 // The PERTURB words of this lane's placements i_k =
 // i_0 + 32k: word g of placement i is mix64(key(i) + γ·g) with key(i) =
 // (seed ⊕ C1) + γ·(i·Wd + 1), i.e. mix64(A_g + k·Δ) with A_g = key(i_0) + γ·g
@@ -755,7 +767,8 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
             for (int k = 0; k < NP; k++) {
                 const double t = __fma_rn(c0, cut[k], prev[k]);
                 const double s = dmax(t, __dmul_rn(cut[k], oth[k]));
-                oth[k] = __fma_rn(cut[k], __dadd_rn(prev[k], -oth[k]), oth[k]);
+                if (PP_M2P_SEL) oth[k] = dsel(m[k], prev[k], oth[k]);
+                else oth[k] = __fma_rn(cut[k], __dadd_rn(prev[k], -oth[k]), oth[k]);
                 prev[k] = __dadd_rn(s, cost);
             }
         } else {
@@ -781,9 +794,15 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
 #pragma unroll
             for (int k = 0; k < NP; k++) {
                 // free[dev] = cut ? oth : prev
-                const double d = __dadd_rn(prev[k], -oth[k]);
-                const double f = __fma_rn(-cut[k], d, prev[k]);
-                oth[k] = __fma_rn(cut[k], d, oth[k]);
+                double f;
+                if (PP_M2P_SEL) {
+                    f = dsel(m[k], oth[k], prev[k]);
+                    oth[k] = dsel(m[k], prev[k], oth[k]);
+                } else {
+                    const double d = __dadd_rn(prev[k], -oth[k]);
+                    f = __fma_rn(-cut[k], d, prev[k]);
+                    oth[k] = __fma_rn(cut[k], d, oth[k]);
+                }
                 prev[k] = __dadd_rn(clear_tag(dmax(r[k], f)), cost);
             }
         }
@@ -798,6 +817,7 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
         }
     };
     constexpr int kHalfUnroll = NP >= 4 ? 1 : 2;
+    constexpr int kStepUnroll = PP_M2P_STEPLOOP ? 1 : 4;
     const uint32_t G = K8 / 8;
     for (uint32_t g = 0; g < G; g++) {           // forward, π order
         refresh();
@@ -806,7 +826,7 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
         for (uint32_t h = 0; h < 2; h++) {
             const uint32_t rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
             half(h, lds32(rec + offsetof(OpRec, base)), true);
-#pragma unroll
+#pragma unroll (kStepUnroll)
             for (uint32_t cc = 0; cc < 4; cc++) step(rec + cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, true);
         }
     }
@@ -819,7 +839,7 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
         for (uint32_t h = 2; h-- > 0;) {
             const uint32_t rec = ops + (2 * K8 - 1 - g * 8 - h * 4) * (uint32_t)sizeof(OpRec);
             half(h, lds32(rec + offsetof(OpRec, base)), false);
-#pragma unroll
+#pragma unroll (kStepUnroll)
             for (int cc = 3; cc >= 0; cc--)
                 step(rec - (uint32_t)cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, false);
         }

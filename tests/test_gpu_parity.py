@@ -339,9 +339,8 @@ def test_perturb_m2_cut_words(dfgs, np_, monkeypatch):
     schedule_m2p): 4 byte compares u < τ per SIMD word, whose two formulas
     meet at τ = 128, a packed base word per half-group, and pads in the last
     half-groups when K mod 8 ≠ 0.  Every τ boundary, a random base, begin = 0
-    (candidate 0 = the base itself) and both the per-candidate (write-all) and
-    the argmin kernels, against the oracle."""
-    monkeypatch.setenv("PP_NP", np_)
+    (candidate 0 = the base itself) and both the per-candidate (write-all,
+    NP = 2 only) and the argmin kernels (NP pinned), against the oracle."""
     rng = np.random.default_rng(128)
     cases = [dfgs["toy12"][1:], dfgs["inception_v3"][1:]]
     for K in (13, 30):   # K mod 8 = 5 and 6: pad positions in the last half-groups
@@ -351,9 +350,11 @@ def test_perturb_m2_cut_words(dfgs, np_, monkeypatch):
         base = rng.integers(0, 2, size=g.K, dtype=np.uint8)
         for tau in (0, 1, 7, 8, 127, 128, 129, 200, 255, 256):
             seed = int(rng.integers(0, 2**63))
+            monkeypatch.delenv("PP_NP", raising=False)
             got = pp.u64(g.eval_generated(2, pp.GEN_PERTURB, seed, tau, base, 0, 300))
             want = _oracle_candidates(od, 2, O.GEN_PERTURB, seed, tau, base, range(300))
             assert np.array_equal(got, want), (g.K, tau)
             assert got[0] == od.makespan_pi(2, base)   # candidate 0 is the base
+            monkeypatch.setenv("PP_NP", np_)
             r = pp.u64(g.search_range(2, pp.GEN_PERTURB, seed, tau, base, 0, 1_000))
             assert (int(r[0]), int(r[1])) == od.round(2, O.GEN_PERTURB, seed, tau, base, 0, 1_000), (g.K, tau)
