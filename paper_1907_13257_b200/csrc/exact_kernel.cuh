@@ -44,13 +44,13 @@ __device__ __forceinline__ uint32_t x_gen_dev(const XParams &P, const uint8_t *o
         return Dev<M>::canon(g.dev(0, p, p % 8, 0));
     } else if (GEN == GEN_RANDOM) {
         RandomGen<M, 1> g;
-        g.init(ii, P.seed, P.K);
+        g.init(i, P.seed, P.K);
         g.refresh(p / 8);
         g.sub((p / 4) & 1);
         return Dev<M>::canon(g.dev(0, p, p % 4, 0));
     } else {
         PerturbGen<M, 1> g;
-        g.init(ii, P.seed, P.K, P.tau);
+        g.init(i, P.seed, P.K, P.tau);
         g.refresh(p / 8);
         g.sub((p / 4) & 1);
         return Dev<M>::canon(g.dev(0, p, p % 4, P.g_base[p]));

@@ -113,24 +113,29 @@ struct GrayGen {                           // O5: reflected M-ary Gray code
     }
 };
 
+// RANDOM and PERTURB keep one key per lane: the lane's placements are
+// i_k = i_0 + 32k (search_kernel), so key(i_k) = key(i_0) + kÂ·Î” with the
+// uniform Î” = Î³Â·32Â·Wd, and only i_0 can be candidate 0.  (Per-placement keys
+// cost registers that ptxas would rematerialise every group.)
 template <int M, int NP>
 struct RandomGen {                         // O6 RANDOM: b bits per op, P = 8Â·âŒŠ8/bâŒ‹ ops per word
     static constexpr int b = Bits<M>::b;
     static constexpr int GPW = b ? 8 / b : 8;      // 8-op groups per word
-    uint64_t key[NP];   // seed + Î³Â·(iÂ·Wd + 1)
-    uint64_t keep[NP];  // 0 for candidate 0 (all zeros), else ~0
+    uint64_t key0;      // seed + Î³Â·(i_0Â·Wd + 1)
+    uint64_t dk;        // Î³Â·32Â·Wd
+    uint64_t keep0;     // 0 if i_0 is candidate 0 (all zeros), else ~0
     uint64_t w[NP];     // current word
     uint32_t wg[NP];    // the current group's 8Â·b bits
     uint32_t wh[NP];    // the current half-group's 4Â·b bits
     uint32_t cur;        // word index held in w (shared by the lane's placements)
-    template <int N>
-    __device__ __forceinline__ void init(const uint64_t (&i)[N], uint64_t seed, uint32_t K) {
+    __device__ __forceinline__ void init(uint64_t i0, uint64_t seed, uint32_t K) {
         const uint64_t P = 8ull * GPW;
         const uint64_t Wd = (K + P - 1) / P;
+        key0 = seed + kGamma * (i0 * Wd + 1);
+        dk = kGamma * 32ull * Wd;
+        keep0 = (i0 == 0) ? 0ull : ~0ull;
 #pragma unroll
-        for (int k = 0; k < N; k++) {
-            key[k] = seed + kGamma * (i[k] * Wd + 1);
-            keep[k] = (i[k] == 0) ? 0ull : ~0ull;
+        for (int k = 0; k < NP; k++) {
             w[k] = 0;
             wg[k] = 0;
             wh[k] = 0;
@@ -143,7 +148,10 @@ struct RandomGen {                         // O6 RANDOM: b bits per op, P = 8Â·â
         if (t != cur) {   // warp-uniform
             cur = t;
 #pragma unroll
-            for (int k = 0; k < NP; k++) w[k] = mix64(key[k] + kGamma * t) & keep[k];
+            for (int k = 0; k < NP; k++) {
+                const uint64_t wk = mix64(key0 + ((uint64_t)k * dk + kGamma * t));
+                w[k] = k == 0 ? wk & keep0 : wk;
+            }
         }
         const uint32_t sh = 8 * b * (g - t * GPW);
 #pragma unroll
@@ -164,18 +172,20 @@ struct RandomGen {                         // O6 RANDOM: b bits per op, P = 8Â·â
 
 template <int M, int NP>
 struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops per word
-    uint64_t key1[NP], key2[NP];
+    uint64_t key1, key2;   // the two streams' keys of i_0
+    uint64_t dk;           // Î³Â·32Â·Wd
     uint64_t w[NP], y[NP];
     uint32_t uh[NP], yh[NP];   // the current half-group's u / y bytes
-    uint32_t tau[NP];   // 0 for candidate 0 (the base itself)
-    template <int N>
-    __device__ __forceinline__ void init(const uint64_t (&i)[N], uint64_t seed, uint32_t K, uint32_t tau_) {
+    uint32_t tau0, tau;        // Ï„ of placement 0 (0 if i_0 is candidate 0, the base) and of the others
+    __device__ __forceinline__ void init(uint64_t i0, uint64_t seed, uint32_t K, uint32_t tau_) {
         const uint64_t Wd = (K + 7) / 8;
+        key1 = (seed ^ 0xD1B54A32D192ED03ull) + kGamma * (i0 * Wd + 1);
+        key2 = (seed ^ 0x8CB92BA72F3D8DD7ull) + kGamma * (i0 * Wd + 1);
+        dk = kGamma * 32ull * Wd;
+        tau = tau_;
+        tau0 = (i0 == 0) ? 0u : tau_;
 #pragma unroll
-        for (int k = 0; k < N; k++) {
-            key1[k] = (seed ^ 0xD1B54A32D192ED03ull) + kGamma * (i[k] * Wd + 1);
-            key2[k] = (seed ^ 0x8CB92BA72F3D8DD7ull) + kGamma * (i[k] * Wd + 1);
-            tau[k] = (i[k] == 0) ? 0u : tau_;
+        for (int k = 0; k < NP; k++) {
             w[k] = y[k] = 0;
             uh[k] = yh[k] = 0;
         }
@@ -184,8 +194,9 @@ struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops
         if (M == 1) return;
 #pragma unroll
         for (int k = 0; k < NP; k++) {
-            w[k] = mix64(key1[k] + kGamma * g);
-            if (M > 2) y[k] = mix64(key2[k] + kGamma * g);
+            const uint64_t off = (uint64_t)k * dk + kGamma * g;   // uniform
+            w[k] = mix64(key1 + off);
+            if (M > 2) y[k] = mix64(key2 + off);
         }
     }
     __device__ __forceinline__ void sub(uint32_t h) {
@@ -200,13 +211,14 @@ struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops
         if (M == 1) return 0;
         bs &= 7u;   // bits 7..31 of OpRec.base hold the M = 2 half-group word
         const uint32_t u = __byte_perm(uh[k], 0, 0x4440u | (cc & 3u));
+        const uint32_t tk = k == 0 ? tau0 : tau;
         if (M == 2) {
             // device = base + [u < Ï„], read modulo 2 (see Dev<M>): one PRMT and a sign bit
-            return bs + ((uint32_t)((int)u - (int)tau[k]) >> 31);
+            return bs + ((uint32_t)((int)u - (int)tk) >> 31);
         }
         const uint32_t yv = __byte_perm(yh[k], 0, 0x4440u | (cc & 3u));
         const uint32_t flip = (bs + 1 + yv % (uint32_t)(M > 1 ? M - 1 : 1)) % (uint32_t)M;
-        return (u < tau[k]) ? flip : bs;
+        return (u < tk) ? flip : bs;
     }
 };
 
@@ -696,6 +708,9 @@ __device__ __forceinline__ double dsel(uint32_t m, double a, double b) {
 #ifndef PP_M2P_SEL
 #define PP_M2P_SEL 1   // oth / free[dev] by mask selects (ALU; A/B: -1.4% time) instead of DADD + DFMA (FP64)
 #endif
+#ifndef PP_M2P_LDS64
+#define PP_M2P_LDS64 1   // cost and c0 by two LDS.64 into their own pairs (A/B: -1.1%)
+#endif
 #ifndef PP_M2P_STEPLOOP
 #define PP_M2P_STEPLOOP 0   // 1: the 4 steps of a half-group as a loop (smaller code) instead of unrolled
 #endif
@@ -750,10 +765,18 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
     };
 
     auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
-        const uint4 a = lds128(rec);
-        const uint4 b = lds128(rec + 16);
-        const double cost = __hiloint2double((int)a.y, (int)a.x);
-        const double c0 = __hiloint2double((int)a.w, (int)a.z);
+        uint4 a, b;
+        double cost, c0;
+        if (PP_M2P_LDS64) {
+            cost = ldd(rec);
+            c0 = ldd(rec + 8);
+            b = lds128(rec + 16);
+        } else {
+            a = lds128(rec);
+            b = lds128(rec + 16);
+            cost = __hiloint2double((int)a.y, (int)a.x);
+            c0 = __hiloint2double((int)a.w, (int)a.z);
+        }
         uint32_t m[NP];
         double cut[NP];
 #pragma unroll
@@ -936,6 +959,9 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
             valid[k] = off[k] < n;
             idx[k] = P.begin + (valid[k] ? off[k] : n - 1);
         }
+        // the generators' lane placements i_0 + 32k (unclamped: results of
+        // lanes past the end are discarded); only i_0 can be candidate 0
+        const uint64_t i0 = P.begin + tile * TILE + lane;
         uint64_t mk[NP];
         if (GEN == GEN_GRAY) {
             GrayGen<M, NP> g;
@@ -944,20 +970,17 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
                                               smem_base + P.off_cls, P.tau);
         } else if (GEN == GEN_RANDOM) {
             RandomGen<M, NP> g;
-            g.init(idx, P.seed, P.K);
+            g.init(i0, P.seed, P.K);
             schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
                                               smem_base + P.off_cls, P.tau);
         } else if constexpr (GEN == GEN_PERTURB && kM2P) {
-            // lane placements i_0 + 32k (unclamped: results of lanes past the
-            // end are discarded); only i = 0 can be candidate 0, the base
-            const uint64_t i0 = P.begin + tile * TILE + lane;
             const uint64_t Wd = (P.K + 7) / 8;
             const uint64_t A = (P.seed ^ 0xD1B54A32D192ED03ull) + kGamma * (i0 * Wd + 1);
             schedule_m2p<NP, MEM>(A, kGamma * 32ull * Wd, i0 == 0 ? 0u : 0x80808080u, mk, ops, xr, mem, lane_region,
                                   P.K8, P.cap, P.one_hi, P.tau);
         } else if (GEN == GEN_PERTURB) {
             PerturbGen<M, NP> g;
-            g.init(idx, P.seed, P.K, P.tau);
+            g.init(i0, P.seed, P.K, P.tau);
             schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
                                               smem_base + P.off_cls, P.tau);
         } else {
@@ -1062,13 +1085,13 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
             d = g.dev(0, p, p % 8, 0);
         } else if (GEN == GEN_RANDOM) {
             RandomGen<M, 1> g;
-            g.init(ii, U.seed, U.K);
+            g.init(idx_s, U.seed, U.K);
             g.refresh(p / 8);
             g.sub((p / 4) & 1);
             d = g.dev(0, p, p % 4, 0);
         } else {
             PerturbGen<M, 1> g;
-            g.init(ii, U.seed, U.K, U.tau);
+            g.init(idx_s, U.seed, U.K, U.tau);
             g.refresh(p / 8);
             g.sub((p / 4) & 1);
             d = g.dev(0, p, p % 4, U.base[p]);
