@@ -22,3 +22,29 @@ if __name__ == "__main__":
     for k in KEYS:
         if k in d:
             print(f"{k:80s} {d[k][0]} {d[k][1]}")
+    # stall reasons per issued instruction, then the executed-opcode mix (SASS page)
+    print("\nstall reasons per issued instruction (smsp__average_warps_issue_stalled_*_per_issue_active):")
+    for k, (v, u) in sorted(d.items()):
+        if "issue_stalled" in k and k.endswith("per_issue_active.ratio"):
+            try:
+                if float(v) >= 0.05:
+                    print(f"  {k.split('stalled_')[1].replace('_per_issue_active.ratio', ''):28s} {float(v):.3f}")
+            except ValueError:
+                pass
+    out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))[2:]
+    import collections
+    ops, tot = collections.Counter(), 0
+    for r in rows:
+        try:
+            n = int(r[5])
+        except (ValueError, IndexError):
+            continue
+        t = r[1].split()
+        op = (t[1] if t[0].startswith("@") else t[0]).split(".")[0]
+        ops[op] += n
+        tot += n
+    if tot:
+        print("\nexecuted warp-instructions by opcode:")
+        print("  " + ", ".join(f"{o} {100 * n / tot:.1f}%" for o, n in ops.most_common(16)))
