@@ -22,7 +22,11 @@
 // are read from `prev`; other inputs from liveness-allocated shared slots.
 // The schedule loop runs over 8-op groups (one generator word per group),
 // each as two half-groups of 4 unrolled steps; K is padded to a multiple of 8
-// with state-preserving no-op records.
+// with state-preserving no-op records.  Three schedule bodies: schedule_gen
+// (tagged u64, any M), schedule_f64 (tagged f64, M ≥ 2) and schedule_m2p
+// (tagged f64, M = 2 PERTURB — the bench path), which decides the devices and
+// cut flags of a half-group at once with SIMD-within-a-register byte compares
+// (DESIGN.md §6).
 //
 // The DFG image is staged global → shared once per CTA with bulk TMA copies
 // (cp.async.bulk + mbarrier).  No tensor cores: integer max-plus work.
