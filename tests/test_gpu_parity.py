@@ -358,3 +358,28 @@ def test_perturb_m2_cut_words(dfgs, np_, monkeypatch):
             monkeypatch.setenv("PP_NP", np_)
             r = pp.u64(g.search_range(2, pp.GEN_PERTURB, seed, tau, base, 0, 1_000))
             assert (int(r[0]), int(r[1])) == od.round(2, O.GEN_PERTURB, seed, tau, base, 0, 1_000), (g.K, tau)
+
+
+@pytest.mark.parametrize("np_", ["1", "2", "4"])
+def test_perturb_m2_cut_words_memory_cap(np_, monkeypatch):
+    """The cut-word schedule with a per-device memory cap:
+    the memory use per device is summed from the same device words, and an
+    over-cap candidate is infeasible.  Caps chosen so that some candidates
+    fit and some do not."""
+    rng = np.random.default_rng(487)
+    for K in (29, 64, 131):
+        spec = synth.random_dag(9000 + K, K, avg_deg=1.5, max_cost=10**6, max_bytes=10**6)
+        spec["mem_bytes"] = [int(x) for x in rng.integers(0, 100, size=K)]
+        spec["dev_mem_cap_bytes"] = int(sum(spec["mem_bytes"]) * 0.55)
+        g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
+        base = (np.arange(K) % 2).astype(np.uint8)
+        seed = int(rng.integers(0, 2**63))
+        monkeypatch.delenv("PP_NP", raising=False)
+        got = pp.u64(g.eval_generated(2, pp.GEN_PERTURB, seed, 64, base, 0, 500))
+        want = _oracle_candidates(od, 2, O.GEN_PERTURB, seed, 64, base, range(500))
+        assert np.array_equal(got, want), K
+        inf = int(np.sum(got == np.uint64(2**64 - 1)))
+        assert 0 < inf < 500, (K, inf)   # both feasible and infeasible candidates occur
+        monkeypatch.setenv("PP_NP", np_)
+        r = pp.u64(g.search_range(2, pp.GEN_PERTURB, seed, 64, base, 0, 2_000))
+        assert (int(r[0]), int(r[1])) == od.round(2, O.GEN_PERTURB, seed, 64, base, 0, 2_000), K
