@@ -46,6 +46,18 @@
 #define PP_MIN_CTAS 1   // resident CTAs per SM the register allocation targets (measured best)
 #endif
 
+// max + cost of untagged times on the FP64 pipe (dmax_add) instead of DSETP +
+// 2 FSEL + DADD, per code path (A/B: profiles/r01_ab_matrix.txt)
+#ifndef PP_FMAX_M2P_CHAIN
+#define PP_FMAX_M2P_CHAIN 1   // cut-word schedule, chain steps
+#endif
+#ifndef PP_FMAX_M2P_JOIN
+#define PP_FMAX_M2P_JOIN 0    // cut-word schedule, non-chain steps
+#endif
+#ifndef PP_FMAX_F64
+#define PP_FMAX_F64 2         // schedule_f64: 0 never, 1 always, 2 only PERTURB with M ≥ 3
+#endif
+
 namespace pp {
 
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
@@ -495,6 +507,14 @@ __device__ __forceinline__ double one_if(uint32_t x, uint32_t khi) {
     return __hiloint2double((int)hi, 0);
 }
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+// max(a, b) + c for UNTAGGED exact integers a, b, c < 2^49 on the FP64 pipe:
+// ½·(a + b + |a − b|) + c — a + b and |a − b| are exact (< 2^50), their sum
+// is 2·max(a, b) (< 2^51, even), and the fused ½·x + c is the exact integer
+// max + c < 2^50.  Four FP64 instructions instead of DSETP, 2 FSEL (ALU pipe)
+// and DADD (A/B: profiles/r01_ab_matrix.txt).
+__device__ __forceinline__ double dmax_add(double a, double b, double c) {
+    return __fma_rn(0.5, __dadd_rn(__dadd_rn(a, b), fabs(__dadd_rn(a, -b))), c);
+}
 __device__ __forceinline__ double with_tag(double v, uint32_t dev) {
     return __hiloint2double(__double2hiint(v), __double2loint(v) | (int)dev);
 }
@@ -527,6 +547,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
                                              const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
                                              uint32_t K8, uint64_t cap, uint32_t khi, uint32_t cls) {
     constexpr bool SM = M > 2;                    // free[] in shared memory
+    constexpr bool kFmax = PP_FMAX_F64 == 1 || (PP_FMAX_F64 == 2 && SM && std::is_same<Gen, PerturbGen<M, NP>>::value);
     double prev[NP], oth[NP];
     uint32_t pdev[NP];
     MemUse<M> mu[NP];
@@ -563,15 +584,15 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
                 // cut·free = 0 ≤ prev): s = max(prev + cut·c0, cut·free[dev])
                 const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
                 const double t = HW ? __dadd_rn(prev[k], hwc(a.z, pdev[k], dev[k])) : __fma_rn(c0, cut, prev[k]);
-                double s;
+                double f;
                 if (SM) {
-                    s = dmax(t, __dmul_rn(cut, ldd(fslot(k, dev[k]))));
+                    f = __dmul_rn(cut, ldd(fslot(k, dev[k])));
                     std_(fslot(k, pdev[k]), prev[k]);
                 } else {
-                    s = dmax(t, __dmul_rn(cut, oth[k]));
+                    f = __dmul_rn(cut, oth[k]);
                     oth[k] = __fma_rn(cut, __dadd_rn(prev[k], -oth[k]), oth[k]);   // cut ? prev : oth
                 }
-                prev[k] = __dadd_rn(s, cost);
+                prev[k] = kFmax ? dmax_add(t, f, cost) : __dadd_rn(dmax(t, f), cost);
                 pdev[k] = dev[k];
             }
         } else {
@@ -615,7 +636,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
                     f = __fma_rn(-cut, d, prev[k]);
                     oth[k] = __fma_rn(cut, d, oth[k]);
                 }
-                prev[k] = __dadd_rn(clear_tag(dmax(r[k], f)), cost);
+                prev[k] = kFmax ? dmax_add(clear_tag(r[k]), f, cost) : __dadd_rn(clear_tag(dmax(r[k], f)), cost);
                 pdev[k] = dev[k];
             }
         }
@@ -793,10 +814,10 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
 #pragma unroll
             for (int k = 0; k < NP; k++) {
                 const double t = __fma_rn(c0, cut[k], prev[k]);
-                const double s = dmax(t, __dmul_rn(cut[k], oth[k]));
+                const double f = __dmul_rn(cut[k], oth[k]);
                 if (PP_M2P_SEL) oth[k] = dsel(m[k], prev[k], oth[k]);
                 else oth[k] = __fma_rn(cut[k], __dadd_rn(prev[k], -oth[k]), oth[k]);
-                prev[k] = __dadd_rn(s, cost);
+                prev[k] = PP_FMAX_M2P_CHAIN ? dmax_add(t, f, cost) : __dadd_rn(dmax(t, f), cost);
             }
         } else {
             double r[NP];
@@ -830,7 +851,7 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
                     f = __fma_rn(-cut[k], d, prev[k]);
                     oth[k] = __fma_rn(cut[k], d, oth[k]);
                 }
-                prev[k] = __dadd_rn(clear_tag(dmax(r[k], f)), cost);
+                prev[k] = PP_FMAX_M2P_JOIN ? dmax_add(clear_tag(r[k]), f, cost) : __dadd_rn(clear_tag(dmax(r[k], f)), cost);
             }
         }
         if (b.y != kNoStore) {
