@@ -135,8 +135,9 @@ int  pp_dfg_get_pi(const pp_dfg *dfg, int32_t *pi_out);
  *                  device of descriptor op k, each < M
  *   d_makespan   : device ptr uint64 [count]; PP_INFEASIBLE_MAKESPAN when the
  *                  memory cap is violated
- * Asynchronous on cuda_stream (a value ≥ M in a placement is not checked on
- * the device; results for such rows are unspecified).                       */
+ * Asynchronous on cuda_stream.  A row holding a value ≥ M is not an error
+ * of the call: the device checks every value, evaluates nothing out of range,
+ * and writes PP_INFEASIBLE_MAKESPAN for that row; other rows are unaffected. */
 int pp_eval_placements(const pp_dfg *dfg, int M, const uint8_t *d_placements, uint64_t count,
                        uint64_t *d_makespan, void *cuda_stream);
 
@@ -198,7 +199,8 @@ int pp_search_range(const pp_dfg *dfg, int M, int gen, uint64_t seed_r, uint32_t
  *                makespan found so far (an upper bound) and d_exact[i] = 0.
  *   d_exact      device ptr uint8 [count], optional (NULL): 1 = optimal.
  * Placements and generators as in pp_eval_placements / pp_eval_generated;
- * memory-infeasible placements give PP_INFEASIBLE_MAKESPAN.  Asynchronous.  */
+ * memory-infeasible placements, and explicit rows holding a value ≥ M, give
+ * PP_INFEASIBLE_MAKESPAN.  Asynchronous.                                    */
 int pp_eval_exact(const pp_dfg *dfg, int M, const uint8_t *d_placements, uint64_t count,
                   uint64_t node_limit, uint64_t *d_makespan, uint8_t *d_exact, void *cuda_stream);
 int pp_eval_exact_generated(const pp_dfg *dfg, int M, int gen, uint64_t seed_r, uint32_t flip_thresh,
@@ -280,22 +282,49 @@ void pp_comm_destroy(pp_comm *comm);
 /* The (makespan, index) argmin across the ranks of comm:
  * each rank's d_best (device ptr uint64[2] = {makespan, index} over its own
  * candidate slice, e.g. from pp_search_range / pp_search_exact /
- * pp_pipeline_range on its pp_rank_slice) is replaced in place by the global
- * lexicographic argmin: one NCCL min all-reduce of the packed key
- * (pp_pack_key: the smallest makespan, ties to the lowest rank, i.e. the
- * lowest indices for contiguous slices), a second of the winner's index.
- * Asynchronous on cuda_stream.  Errors: PP_E_INVALID, PP_E_NCCL, PP_E_CUDA. */
+ * pp_pipeline_range on its pp_rank_slice; {PP_INFEASIBLE_MAKESPAN, UINT64_MAX}
+ * for an empty slice) is replaced in place by the global lexicographic
+ * argmin: one NCCL min all-reduce of the packed key (pp_round_key: the
+ * smallest makespan, ties to the lowest rank, i.e. the lowest indices for
+ * contiguous slices; an empty slice never wins), a second of the winner's
+ * index — the same exchange pp_search_best runs every round.
+ * Synchronises cuda_stream, polling the communicator for asynchronous NCCL
+ * errors and the comm's timeout (pp_comm_set_timeout) while it waits; on an
+ * error or a timeout the communicator is aborted and PP_E_NCCL returned (the
+ * comm is then unusable; destroy it).  Errors: PP_E_INVALID, PP_E_NCCL,
+ * PP_E_CUDA.                                                                 */
 int pp_argmin_allreduce(const pp_dfg *dfg, pp_comm *comm, uint64_t *d_best, void *cuda_stream);
 
-/* Sharding protocol (host only, no GPU needed; exported so multi-process CPU
- * tests exercise the exact same rules):
+/* Timeout for the waits of pp_search_best / pp_argmin_allreduce on this comm
+ * (a dead or stalled rank otherwise hangs the collective).  0 ⇒ the default,
+ * PP_NCCL_TIMEOUT_S from the environment or 600 s.                          */
+int pp_comm_set_timeout(pp_comm *comm, uint64_t timeout_ms);
+
+/* Sharding protocol (host only, no GPU needed).  These are the functions the
+ * device kernels and the NCCL driver run (csrc/protocol.h), exported so that
+ * multi-process CPU tests exercise the product's own rules and sequence:
  *   rank r of R owns candidates [⌊r·n/R⌋, ⌊(r+1)·n/R⌋) of every round;
- *   key = (min(makespan, 2^61−1) << 3) | r, R ≤ 8; the global winner is the
- *   minimum key (ties to the lower rank = the lower global index).         */
+ *   key = (min(makespan, 2^61−1) << 3) | r for a slice whose local argmin
+ *   index is not UINT64_MAX, else UINT64_MAX (an empty slice never wins), R ≤ 8;
+ *   the global winner is the minimum key (ties to the lower rank = the lower
+ *   global index); the winning rank contributes its index, every other rank
+ *   UINT64_MAX, to a second min all-reduce.                                 */
 void     pp_rank_slice(uint64_t count, int rank, int world, uint64_t *begin, uint64_t *end);
-uint64_t pp_pack_key(uint64_t makespan, int rank);
-uint64_t pp_key_makespan(uint64_t key);   /* 2^61−1 maps back to PP_INFEASIBLE_MAKESPAN */
+uint64_t pp_round_key(uint64_t makespan, uint64_t index, int rank);
+uint64_t pp_pack_key(uint64_t makespan, int rank);   /* = pp_round_key(makespan, 0, rank) */
+uint64_t pp_key_makespan(uint64_t key);   /* 2^61−1 (and UINT64_MAX) map back to PP_INFEASIBLE_MAKESPAN */
 int      pp_key_rank(uint64_t key);
+uint64_t pp_round_contrib(uint64_t key_global, uint64_t local_index, int rank);
+/* 1 iff a PERTURB base moves to the round winner with this global index (the
+ * winner is strictly better than the base exactly when it is not candidate 0) */
+int      pp_round_moves_base(uint64_t win_index);
+/* One round's exchange on the host with a caller-supplied collective:
+ * allreduce_min(ctx, in, out) must set *out to the minimum of `in` over all
+ * ranks (0 = success).  The sequence is the one the NCCL path runs.
+ * win[0] = winning makespan (PP_INFEASIBLE_MAKESPAN if none), win[1] = index. */
+typedef int (*pp_allreduce_min_u64)(void *ctx, uint64_t in, uint64_t *out);
+int pp_round_exchange_host(uint64_t local_makespan, uint64_t local_index, int rank,
+                           pp_allreduce_min_u64 allreduce_min, void *ctx, uint64_t win[2]);
 
 /* ------------------------------------------------------------ projection --
  * End-to-end training time C = T × S × E (Eq. 1) for DP-only

@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -15,6 +17,8 @@
 #include <vector>
 
 #include "internal.h"
+
+typedef unsigned __int128 u128;
 
 namespace pp {
 
@@ -321,6 +325,8 @@ struct Nccl {
                               cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 
 static Nccl *nccl() {
@@ -335,7 +341,11 @@ static Nccl *nccl() {
         n.AllReduce = (decltype(n.AllReduce))dlsym(h, "ncclAllReduce");
         n.CommDestroy = (decltype(n.CommDestroy))dlsym(h, "ncclCommDestroy");
         n.GetErrorString = (decltype(n.GetErrorString))dlsym(h, "ncclGetErrorString");
-        if (n.GetUniqueId && n.CommInitRank && n.AllReduce && n.CommDestroy && n.GetErrorString) n.h = h;
+        n.CommGetAsyncError = (decltype(n.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+        n.CommAbort = (decltype(n.CommAbort))dlsym(h, "ncclCommAbort");
+        if (n.GetUniqueId && n.CommInitRank && n.AllReduce && n.CommDestroy && n.GetErrorString &&
+            n.CommGetAsyncError && n.CommAbort)
+            n.h = h;
     });
     return n.h ? &n : nullptr;
 }
@@ -351,7 +361,95 @@ static int nccl_err(ncclResult_t r, const char *what) {
 struct pp_comm {
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1, device = 0;
+    uint64_t timeout_ms = 0;     // 0: PP_NCCL_TIMEOUT_S or 600 s
+    bool aborted = false;
 };
+
+namespace pp {
+
+// The round exchange (protocol.h) on device scalars: the pack / contrib
+// kernels and NCCL min all-reduces, all stream-ordered on st.
+struct NcclExec {
+    Nccl *nc;
+    pp_comm *comm;
+    uint64_t *s;
+    cudaStream_t st;
+    int pack() {
+        int rc = launch_pack_key(s, comm->rank, st);
+        g_launches++;
+        return rc ? cuda_err((cudaError_t)rc, "pack") : PP_OK;
+    }
+    int contrib() {
+        int rc = launch_contrib(s, comm->rank, st);
+        g_launches++;
+        return rc ? cuda_err((cudaError_t)rc, "contrib") : PP_OK;
+    }
+    int allreduce_min(int src, int dst) {
+        ncclResult_t nr = nc->AllReduce(s + src, s + dst, 1, ncclUint64, ncclMin, comm->comm, st);
+        return nr == ncclSuccess ? PP_OK : nccl_err(nr, "allreduce");
+    }
+};
+
+// The same exchange on host scalars with a caller-supplied collective.
+struct HostExec {
+    uint64_t s[SC_COUNT];
+    int rank;
+    pp_allreduce_min_u64 fn;
+    void *ctx;
+    int pack() {
+        s[SC_KEY_LOCAL] = proto::key(s[SC_LOCAL_MK], s[SC_LOCAL_IDX], rank);
+        return PP_OK;
+    }
+    int contrib() {
+        s[SC_IDX_LOCAL] = proto::contrib(s[SC_KEY_GLOBAL], s[SC_LOCAL_IDX], rank);
+        return PP_OK;
+    }
+    int allreduce_min(int src, int dst) {
+        if (fn(ctx, s[src], &s[dst]) != 0) { set_error("allreduce callback failed"); return PP_E_NCCL; }
+        return PP_OK;
+    }
+};
+
+static uint64_t comm_timeout_ms(const pp_comm *c) {
+    if (c && c->timeout_ms) return c->timeout_ms;
+    if (const char *v = getenv("PP_NCCL_TIMEOUT_S")) {
+        const long long t = atoll(v);
+        if (t > 0) return (uint64_t)t * 1000;
+    }
+    return 600ull * 1000;
+}
+
+// Waits for st.  With a communicator, polls ncclCommGetAsyncError and the
+// timeout while the stream is busy: a failed or dead peer aborts the comm
+// (which also unblocks the stream) instead of hanging the caller.
+static int wait_stream(cudaStream_t st, pp_comm *comm, Nccl *nc) {
+    if (!comm) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        return e == cudaSuccess ? PP_OK : cuda_err(e, "stream synchronize");
+    }
+    const uint64_t limit = comm_timeout_ms(comm);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint32_t spin = 0;; spin++) {
+        cudaError_t q = cudaStreamQuery(st);
+        if (q == cudaSuccess) return PP_OK;
+        if (q != cudaErrorNotReady) return cuda_err(q, "stream query");
+        ncclResult_t ae = ncclSuccess;
+        nc->CommGetAsyncError(comm->comm, &ae);
+        const uint64_t ms = (uint64_t)std::chrono::duration_cast<std::chrono::milliseconds>(
+                                std::chrono::steady_clock::now() - t0).count();
+        if ((ae != ncclSuccess && ae != ncclInProgress) || ms > limit) {
+            nc->CommAbort(comm->comm);
+            comm->comm = nullptr;
+            comm->aborted = true;
+            if (ae != ncclSuccess && ae != ncclInProgress) return nccl_err(ae, "asynchronous error (comm aborted)");
+            set_error("NCCL: timeout after " + std::to_string(limit) + " ms (comm aborted)");
+            return PP_E_NCCL;
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+}
+
+}  // namespace pp
 
 using namespace pp;
 
@@ -587,6 +685,38 @@ static int pipe_check(const pp_dfg *g, int M, const uint32_t *micro, int nm) {
     return PP_OK;
 }
 
+// Range of the pipeline arithmetic (u64 in the kernel): with m micro-batches
+// and a per-op overhead o, every stage time is ≤ ⌈ΣΔ/m⌉ + K·o and every
+// transfer ≤ ⌈D·10^12/(m·BW)⌉ + L, and the makespan is a longest path
+// through ≤ 2·m·M stage slots and ≤ 2·m·M transfers, so
+//   makespan ≤ T_1 + 2·m·M·(K·o + 1) + 2·M·(Σ_e c_e) + 2·m·M·(L + 1).
+// That bound, the π-prefix sums of M(k) and the 2-D byte prefix sums must
+// stay below 2^63, else PP_E_RANGE (the loader's 2^61 bound covers only the
+// placement schedule).
+static int pipe_range(const pp_dfg *g, int M, const uint32_t *micro, int nm, uint64_t overhead) {
+    uint64_t mx = 0;
+    for (int j = 0; j < nm; j++) mx = std::max<uint64_t>(mx, micro[j]);
+    u128 comm = 0, bytes = 0, mem = 0;
+    for (size_t e = 0; e < g->e_src.size(); e++) {
+        bytes += (u128)g->e_bf[e] + g->e_bb[e];
+        comm += ((u128)g->e_bf[e] * 1000000000000ull + g->link_bw - 1) / g->link_bw;
+        comm += ((u128)g->e_bb[e] * 1000000000000ull + g->link_bw - 1) / g->link_bw;
+    }
+    for (int p = 0; p < g->K; p++) mem += g->mem[p];
+    const u128 lim = (u128)1 << 63;
+    if (overhead >= lim / ((u128)g->K + 1) || comm >= lim || bytes >= lim || mem >= lim) {
+        set_error("pipeline arithmetic exceeds 2^63");
+        return PP_E_RANGE;
+    }
+    const u128 bound = (u128)g->t1 + 2 * (u128)mx * M * ((u128)g->K * overhead + 1) + 2 * (u128)M * comm +
+                       2 * (u128)mx * M * ((u128)g->link_lat + 1);
+    if (bound >= lim) {
+        set_error("pipeline makespan bound exceeds 2^63 ps");
+        return PP_E_RANGE;
+    }
+    return PP_OK;
+}
+
 static int pipe_tables(pp_dfg *g) {
     if (g->d_pipe) return PP_OK;
     const uint64_t K1 = (uint64_t)g->K + 1;
@@ -635,6 +765,7 @@ int pp_pipeline_range(const pp_dfg *gc, int M, const uint32_t *micro, int nm, ui
                       uint64_t end, uint64_t *d_best, uint64_t *d_makespan, void *stream) {
     int rc = pipe_check(gc, M, micro, nm);
     if (rc) return rc;
+    if ((rc = pipe_range(gc, M, micro, nm, overhead_ps))) return rc;
     uint64_t space = 0;
     if ((rc = pp_pipeline_space(gc, M, nm, &space))) return rc;
     if (end <= begin || end > space || (!d_best && !d_makespan)) {
@@ -773,15 +904,9 @@ void pp_rank_slice(uint64_t count, int rank, int world, uint64_t *begin, uint64_
     *end = (uint64_t)(c * (unsigned)(rank + 1) / (unsigned)world);
 }
 
-uint64_t pp_pack_key(uint64_t makespan, int rank) {
-    const uint64_t cap = (1ull << 61) - 1;
-    return ((makespan < cap ? makespan : cap) << 3) | (uint64_t)(rank & 7);
-}
-uint64_t pp_key_makespan(uint64_t key) {
-    uint64_t m = key >> 3;
-    return m == ((1ull << 61) - 1) ? PP_INFEASIBLE_MAKESPAN : m;
-}
-int pp_key_rank(uint64_t key) { return (int)(key & 7); }
+uint64_t pp_pack_key(uint64_t makespan, int rank) { return proto::key(makespan, 0, rank); }
+uint64_t pp_key_makespan(uint64_t key) { return proto::key_makespan(key); }
+int pp_key_rank(uint64_t key) { return proto::key_rank(key); }
 
 int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *comm, void *stream,
                    pp_search_result *out) {
@@ -795,6 +920,7 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
     }
     const int rank = comm ? comm->rank : 0, world = comm ? comm->world : 1;
     if (world < 1 || world > 8) { set_error("1 to 8 ranks"); return PP_E_INVALID; }
+    if (comm && comm->aborted) { set_error("communicator was aborted"); return PP_E_NCCL; }
     Nccl *nc = comm ? nccl() : nullptr;
     if (comm && !nc) { set_error("NCCL not loadable"); return PP_E_NCCL; }
     DeviceGuard dg(g->device);
@@ -851,17 +977,10 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
             cudaStreamSynchronize(st);
         }
         if (comm) {
-            // key = (makespan << 3) | rank ; min over ranks picks the winning rank,
-            // then the winner's index travels in a second min all-reduce
-            if ((rc = launch_pack_key(g->d_scalars, rank, stream))) return cuda_err((cudaError_t)rc, "pack");
-            ncclResult_t nr = nc->AllReduce(g->d_scalars + SC_KEY_LOCAL, g->d_scalars + SC_KEY_GLOBAL, 1,
-                                            ncclUint64, ncclMin, comm->comm, st);
-            if (nr != ncclSuccess) return nccl_err(nr, "allreduce key");
-            if ((rc = launch_contrib(g->d_scalars, rank, stream))) return cuda_err((cudaError_t)rc, "contrib");
-            nr = nc->AllReduce(g->d_scalars + SC_IDX_LOCAL, g->d_scalars + SC_IDX_GLOBAL, 1, ncclUint64, ncclMin,
-                               comm->comm, st);
-            if (nr != ncclSuccess) return nccl_err(nr, "allreduce index");
-            g_launches += 2;
+            // the round exchange (protocol.h): packed-key min all-reduce picks
+            // the winning rank, a second min all-reduce delivers its index
+            NcclExec ex{nc, comm, g->d_scalars, st};
+            if ((rc = proto::exchange(ex))) return rc;
         }
         UParams u{g->d_image, g->d_base, g->d_winner, g->d_best_place, g->d_scalars, seed_r, (uint32_t)K,
                   (uint32_t)g->K8, desc->flip_thresh,
@@ -873,8 +992,8 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
     std::vector<uint8_t> place(g->base_bytes);
     e = cudaMemcpyAsync(best, g->d_scalars + SC_BEST_MK, sizeof best, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(place.data(), g->d_best_place, g->base_bytes, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_err(e, "search result");
+    if ((rc = wait_stream(st, comm, nc))) return rc;
     for (size_t i = 0; i + 1 < evs.size(); i += 2) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, evs[i], evs[i + 1]) == cudaSuccess) {
@@ -898,6 +1017,7 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
 
 int pp_argmin_allreduce(const pp_dfg *g, pp_comm *comm, uint64_t *d_best, void *stream) {
     if (!g || !comm || !d_best) { set_error("invalid arguments"); return PP_E_INVALID; }
+    if (comm->aborted) { set_error("communicator was aborted"); return PP_E_NCCL; }
     Nccl *nc = nccl();
     if (!nc) { set_error("NCCL not loadable"); return PP_E_NCCL; }
     DeviceGuard dg(g->device);
@@ -906,17 +1026,39 @@ int pp_argmin_allreduce(const pp_dfg *g, pp_comm *comm, uint64_t *d_best, void *
     cudaError_t e = cudaMemcpyAsync(g->d_scalars + SC_LOCAL_MK, d_best, 2 * sizeof(uint64_t),
                                     cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_err(e, "argmin copy");
+    NcclExec ex{nc, comm, g->d_scalars, st};
     int rc;
-    if ((rc = launch_pack_key(g->d_scalars, comm->rank, stream))) return cuda_err((cudaError_t)rc, "pack");
-    ncclResult_t nr = nc->AllReduce(g->d_scalars + SC_KEY_LOCAL, g->d_scalars + SC_KEY_GLOBAL, 1, ncclUint64,
-                                    ncclMin, comm->comm, st);
-    if (nr != ncclSuccess) return nccl_err(nr, "allreduce key");
-    if ((rc = launch_contrib(g->d_scalars, comm->rank, stream))) return cuda_err((cudaError_t)rc, "contrib");
-    nr = nc->AllReduce(g->d_scalars + SC_IDX_LOCAL, g->d_scalars + SC_IDX_GLOBAL, 1, ncclUint64, ncclMin,
-                       comm->comm, st);
-    if (nr != ncclSuccess) return nccl_err(nr, "allreduce index");
+    if ((rc = proto::exchange(ex))) return rc;
     if ((rc = launch_unpack_best(g->d_scalars, d_best, stream))) return cuda_err((cudaError_t)rc, "unpack");
-    g_launches += 3;
+    g_launches++;
+    return wait_stream(st, comm, nc);
+}
+
+int pp_comm_set_timeout(pp_comm *comm, uint64_t timeout_ms) {
+    if (!comm) { set_error("NULL comm"); return PP_E_INVALID; }
+    comm->timeout_ms = timeout_ms;
+    return PP_OK;
+}
+
+uint64_t pp_round_key(uint64_t makespan, uint64_t index, int rank) { return proto::key(makespan, index, rank); }
+uint64_t pp_round_contrib(uint64_t key_global, uint64_t local_index, int rank) {
+    return proto::contrib(key_global, local_index, rank);
+}
+int pp_round_moves_base(uint64_t win_index) { return proto::moves_base(win_index) ? 1 : 0; }
+
+int pp_round_exchange_host(uint64_t local_makespan, uint64_t local_index, int rank, pp_allreduce_min_u64 fn,
+                           void *ctx, uint64_t win[2]) {
+    if (!fn || !win || rank < 0 || rank > 7) { set_error("invalid arguments"); return PP_E_INVALID; }
+    HostExec ex{};
+    ex.s[SC_LOCAL_MK] = local_makespan;
+    ex.s[SC_LOCAL_IDX] = local_index;
+    ex.rank = rank;
+    ex.fn = fn;
+    ex.ctx = ctx;
+    int rc = proto::exchange(ex);
+    if (rc) return rc;
+    win[0] = proto::key_makespan(ex.s[SC_KEY_GLOBAL]);
+    win[1] = ex.s[SC_IDX_GLOBAL];
     return PP_OK;
 }
 
@@ -955,7 +1097,7 @@ int pp_comm_init(const uint8_t id_bytes[128], int rank, int world, int cuda_devi
 void pp_comm_destroy(pp_comm *c) {
     if (!c) return;
     Nccl *n = nccl();
-    if (n && c->comm) n->CommDestroy(c->comm);
+    if (n && c->comm && !c->aborted) n->CommDestroy(c->comm);
     delete c;
 }
 

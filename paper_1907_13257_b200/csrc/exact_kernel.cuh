@@ -101,7 +101,15 @@ __global__ void __launch_bounds__(256) exact_kernel(const XParams P) {
         if (lane == 0) i = P.begin + atomicAdd(&P.g_work[0], 1ull);
         i = shfl64(i, 0);
         if (i >= P.end) break;
-        for (uint32_t p = lane; p < P.K; p += 32) W.dev[p] = (uint8_t)x_gen_dev<M, GEN>(P, orig, i, p);
+        // an explicit value ≥ M is replaced by device 0 and the row reported
+        // infeasible (pp.h, pp_eval_exact): no table is indexed out of range
+        bool bad = false;
+        for (uint32_t p = lane; p < P.K; p += 32) {
+            const uint32_t d = x_gen_dev<M, GEN>(P, orig, i, p);
+            bad |= d >= (uint32_t)M;
+            W.dev[p] = (uint8_t)(d < (uint32_t)M ? d : 0u);
+        }
+        bad = __any_sync(0xffffffffu, bad);
         if (lane < 8) {
             W.freeT[lane] = 0;
             W.rem[lane] = 0;
@@ -118,7 +126,7 @@ __global__ void __launch_bounds__(256) exact_kernel(const XParams P) {
             W.rem[lane] = r;
             infeasible = P.cap > 0 && m > P.cap;
         }
-        infeasible = __any_sync(0xffffffffu, infeasible);
+        infeasible = __any_sync(0xffffffffu, infeasible) || bad;
         uint32_t odev[2];
 #pragma unroll
         for (int j = 0; j < 2; j++) odev[j] = own[j] ? W.dev[opos[j]] : 0u;

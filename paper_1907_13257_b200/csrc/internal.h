@@ -45,6 +45,7 @@
 #include <vector>
 
 #include "../../include/pp.h"
+#include "protocol.h"
 
 namespace pp {
 
@@ -235,6 +236,10 @@ enum ScalarSlot : int {
     SC_BEST_MK = 6, SC_BEST_IDX = 7, SC_BEST_ROUND = 8,
     SC_COUNT = 16
 };
+static_assert(SC_LOCAL_MK == proto::LOCAL_MK && SC_LOCAL_IDX == proto::LOCAL_IDX && SC_KEY_LOCAL == proto::KEY_LOCAL &&
+                  SC_KEY_GLOBAL == proto::KEY_GLOBAL && SC_IDX_LOCAL == proto::IDX_LOCAL &&
+                  SC_IDX_GLOBAL == proto::IDX_GLOBAL,
+              "scalar slots follow protocol.h");
 
 struct UParams {
     uint8_t *image;       // device image: the PERTURB base is patched into OpRec.base

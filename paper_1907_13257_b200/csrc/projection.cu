@@ -257,13 +257,12 @@ int launch_crossover(const CrossParams &X, const pp_cell *cells, pp_crossover_re
 }
 
 // --- tiny helpers of the multi-GPU exchange (stream-ordered, no host sync)
+// the two device steps of the round exchange (protocol.h)
 __global__ void pack_key_kernel(uint64_t *s, int rank) {
-    uint64_t mk = s[SC_LOCAL_MK];
-    const uint64_t cap = (1ull << 61) - 1;
-    s[SC_KEY_LOCAL] = ((mk < cap ? mk : cap) << 3) | (uint64_t)rank;
+    s[SC_KEY_LOCAL] = proto::key(s[SC_LOCAL_MK], s[SC_LOCAL_IDX], rank);
 }
 __global__ void contrib_kernel(uint64_t *s, int rank) {
-    s[SC_IDX_LOCAL] = ((int)(s[SC_KEY_GLOBAL] & 7) == rank) ? s[SC_LOCAL_IDX] : ~0ull;
+    s[SC_IDX_LOCAL] = proto::contrib(s[SC_KEY_GLOBAL], s[SC_LOCAL_IDX], rank);
 }
 // Copies a π-order base into the canonical buffer and into OpRec.base of the
 // forward and backward records of every position p < K8 (PERTURB): the op's
@@ -287,8 +286,7 @@ int launch_pack_key(uint64_t *s, int rank, void *stream) {
     return (int)cudaGetLastError();
 }
 __global__ void unpack_best_kernel(const uint64_t *s, uint64_t *out) {
-    const uint64_t m = s[SC_KEY_GLOBAL] >> 3;
-    out[0] = (m == ((1ull << 61) - 1)) ? kInfeasible : m;
+    out[0] = proto::key_makespan(s[SC_KEY_GLOBAL]);
     out[1] = s[SC_IDX_GLOBAL];
 }
 int launch_unpack_best(const uint64_t *s, uint64_t *out, void *stream) {
@@ -316,30 +314,20 @@ static int bitlen_h(u128 x) {
     return n;
 }
 
-// A small per-device scratch for the error flag and the crossover result.
-struct Scratch {
-    int *err = nullptr;
-    pp_crossover_result *xr = nullptr;
-};
-static std::mutex g_scratch_mu;
-static Scratch g_scratch[64];
-
-static int scratch(Scratch **out) {
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess || dev < 0 || dev >= 64) { set_error("no CUDA device"); return PP_E_CUDA; }
-    std::lock_guard<std::mutex> lk(g_scratch_mu);
-    Scratch &s = g_scratch[dev];
-    if (!s.err) {
-        if ((e = cudaMalloc(&s.err, sizeof(int))) != cudaSuccess ||
-            (e = cudaMalloc(&s.xr, sizeof(pp_crossover_result))) != cudaSuccess) {
-            set_error(cudaGetErrorString(e));
-            return PP_E_CUDA;
-        }
+// Per-call, stream-ordered scratch (cudaMallocAsync / cudaFreeAsync on the
+// caller's stream) for the error flag and the crossover result, so concurrent
+// calls on different streams or threads never share a buffer (pp.h: distinct
+// calls are independent).
+template <class T>
+struct StreamScratch {
+    T *p = nullptr;
+    cudaStream_t st;
+    explicit StreamScratch(cudaStream_t s) : st(s) {}
+    cudaError_t alloc() { return cudaMallocAsync(reinterpret_cast<void **>(&p), sizeof(T), st); }
+    ~StreamScratch() {
+        if (p) cudaFreeAsync(p, st);
     }
-    *out = &s;
-    return PP_OK;
-}
+};
 
 }  // namespace pp
 
@@ -395,16 +383,16 @@ extern "C" int pp_project_e2e(const pp_scenario *sc, int nM, const uint32_t *Ms,
     if (P.sharded)
         for (int m = 0; m < nM; m++)
             for (int d = 0; d < 8; d++) P.shard[m][d] = sc->shard_bytes[8 * m + d];
-    Scratch *s = nullptr;
-    int rc = scratch(&s);
-    if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e = cudaMemsetAsync(s->err, 0, sizeof(int), st);
+    StreamScratch<int> s(st);
+    cudaError_t e = s.alloc();
+    if (e == cudaSuccess) e = cudaMemsetAsync(s.p, 0, sizeof(int), st);
     if (e != cudaSuccess) return proj_fail(PP_E_CUDA, cudaGetErrorString(e));
-    if ((rc = launch_project(P, d_cells, s->err, stream))) return proj_fail(PP_E_CUDA, cudaGetErrorString((cudaError_t)rc));
+    int rc;
+    if ((rc = launch_project(P, d_cells, s.p, stream))) return proj_fail(PP_E_CUDA, cudaGetErrorString((cudaError_t)rc));
     note_launch();
     int err = 0;
-    e = cudaMemcpyAsync(&err, s->err, sizeof(int), cudaMemcpyDeviceToHost, st);
+    e = cudaMemcpyAsync(&err, s.p, sizeof(int), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return proj_fail(PP_E_CUDA, cudaGetErrorString(e));
     if (err) return proj_fail(PP_E_RANGE, "projection value overflows 127 bits");
@@ -427,13 +415,14 @@ extern "C" int pp_crossover(const pp_cell *d_cells, int nM, const uint32_t *Ms, 
     X.nM = (uint32_t)nM;
     X.N_max = N_max;
     X.m1 = (uint32_t)m1;
-    Scratch *s = nullptr;
-    int rc = scratch(&s);
-    if (rc) return rc;
-    if ((rc = launch_crossover(X, d_cells, s->xr, d_best_m, stream))) return proj_fail(PP_E_CUDA, cudaGetErrorString((cudaError_t)rc));
-    note_launch();
     cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e = cudaMemcpyAsync(out, s->xr, sizeof *out, cudaMemcpyDeviceToHost, st);
+    StreamScratch<pp_crossover_result> s(st);
+    cudaError_t e = s.alloc();
+    if (e != cudaSuccess) return proj_fail(PP_E_CUDA, cudaGetErrorString(e));
+    int rc;
+    if ((rc = launch_crossover(X, d_cells, s.p, d_best_m, stream))) return proj_fail(PP_E_CUDA, cudaGetErrorString((cudaError_t)rc));
+    note_launch();
+    e = cudaMemcpyAsync(out, s.p, sizeof *out, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return proj_fail(PP_E_CUDA, cudaGetErrorString(e));
     return PP_OK;

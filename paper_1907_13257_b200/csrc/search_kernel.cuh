@@ -238,13 +238,22 @@ struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops
     }
 };
 
-template <int NP>
+// A value ≥ M in a row would index free[] out of range (M ≥ 3): it is
+// replaced by device 0 and the row is flagged, and a flagged row's makespan
+// is PP_INFEASIBLE_MAKESPAN (pp.h, pp_eval_placements).
+template <int M, int NP>
 struct ExplicitGen {                       // rows of a [count][K] uint8 array
     const uint8_t *row[NP];
     const uint32_t *orig;
+    uint32_t bad[NP];
     __device__ __forceinline__ void refresh(uint32_t) {}
     __device__ __forceinline__ void sub(uint32_t) {}
-    __device__ __forceinline__ uint32_t dev(int k, uint32_t p, uint32_t, uint32_t) const { return row[k][orig[p]]; }
+    __device__ __forceinline__ uint32_t dev(int k, uint32_t p, uint32_t, uint32_t) {
+        const uint32_t v = row[k][orig[p]];
+        const bool ok = v < (uint32_t)M;
+        bad[k] |= ok ? 0u : 1u;
+        return ok ? v : 0u;
+    }
 };
 
 // -------------------------------------------------- shared-memory access
@@ -1009,12 +1018,18 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
             schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
                                               smem_base + P.off_cls, P.tau);
         } else {
-            ExplicitGen<NP> g;
+            ExplicitGen<M, NP> g;
 #pragma unroll
-            for (int k = 0; k < NP; k++) g.row[k] = P.g_place + (idx[k] - P.begin) * (uint64_t)P.K;
+            for (int k = 0; k < NP; k++) {
+                g.row[k] = P.g_place + (idx[k] - P.begin) * (uint64_t)P.K;
+                g.bad[k] = 0;
+            }
             g.orig = orig;
             schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
                                               smem_base + P.off_cls, P.tau);
+#pragma unroll
+            for (int k = 0; k < NP; k++)
+                if (g.bad[k]) mk[k] = kInfeasible;
         }
 #pragma unroll
         for (int k = 0; k < NP; k++) {
@@ -1085,12 +1100,11 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
     __shared__ uint64_t mk_s, idx_s;
     __shared__ int improve;
     uint64_t *s = U.s;
+    __shared__ int move;
     if (threadIdx.x == 0) {
         uint64_t mk, idx;
-        if (U.multi) {
-            uint64_t key = s[SC_KEY_GLOBAL];
-            uint64_t m = key >> 3;
-            mk = (m == ((1ull << 61) - 1)) ? kInfeasible : m;
+        if (U.multi) {   // the exchanged winner (protocol.h)
+            mk = proto::key_makespan(s[SC_KEY_GLOBAL]);
             idx = s[SC_IDX_GLOBAL];
         } else {
             mk = s[SC_LOCAL_MK];
@@ -1098,9 +1112,11 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
         }
         mk_s = mk;
         idx_s = idx;
-        improve = (U.round == 0) || (mk < s[SC_BEST_MK]);
+        improve = idx != proto::kNone && ((U.round == 0) || (mk < s[SC_BEST_MK]));
+        move = proto::moves_base(idx);
     }
     __syncthreads();
+    if (idx_s == proto::kNone) return;   // no candidate anywhere (cannot happen for count ≥ 1)
     const uint64_t ii[1] = {idx_s};
     for (uint32_t p = threadIdx.x; p < U.K; p += blockDim.x) {
         uint32_t d;
@@ -1127,7 +1143,7 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
     OpRec *ops = reinterpret_cast<OpRec *>(U.image);
     for (uint32_t p = threadIdx.x; p < U.K8; p += blockDim.x) {
         const uint8_t d = p < U.K ? U.winner[p] : 0;
-        if (GEN == GEN_PERTURB) {
+        if (GEN == GEN_PERTURB && move) {
             const uint32_t w = half_group_word(U.winner, p, U.K);
             if (p < U.K) U.base[p] = d;
             ops[p].base = d | w;

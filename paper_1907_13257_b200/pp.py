@@ -124,6 +124,11 @@ SIGNATURES = {
     "pp_comm_destroy": ([C.c_void_p], None),
     "pp_argmin_allreduce": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "pp_rank_slice": ([C.c_uint64, C.c_int, C.c_int, P(C.c_uint64), P(C.c_uint64)], None),
+    "pp_comm_set_timeout": ([C.c_void_p, C.c_uint64], C.c_int),
+    "pp_round_key": ([C.c_uint64, C.c_uint64, C.c_int], C.c_uint64),
+    "pp_round_contrib": ([C.c_uint64, C.c_uint64, C.c_int], C.c_uint64),
+    "pp_round_moves_base": ([C.c_uint64], C.c_int),
+    "pp_round_exchange_host": ([C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, P(C.c_uint64)], C.c_int),
     "pp_pack_key": ([C.c_uint64, C.c_int], C.c_uint64),
     "pp_key_makespan": ([C.c_uint64], C.c_uint64),
     "pp_key_rank": ([C.c_uint64], C.c_int),
@@ -414,6 +419,9 @@ class Comm:
         _check(lib().pp_argmin_allreduce(dfg._h, self._h, _dptr(best), _stream(stream)))
         return best
 
+    def set_timeout(self, ms):
+        _check(lib().pp_comm_set_timeout(self._h, ms))
+
     def close(self):
         if getattr(self, "_h", None):
             lib().pp_comm_destroy(self._h)
@@ -440,6 +448,38 @@ def rank_slice(count, rank, world):
 
 def pack_key(makespan, rank):
     return int(lib().pp_pack_key(makespan, rank))
+
+
+def round_key(makespan, index, rank):
+    return int(lib().pp_round_key(makespan, index, rank))
+
+
+def round_contrib(key_global, local_index, rank):
+    return int(lib().pp_round_contrib(key_global, local_index, rank))
+
+
+def round_moves_base(win_index) -> bool:
+    return bool(lib().pp_round_moves_base(win_index))
+
+
+ALLREDUCE_MIN_U64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, P(C.c_uint64))
+
+
+def round_exchange_host(local_makespan, local_index, rank, allreduce_min):
+    """One round's cross-rank argmin exchange run by the library's own protocol
+    code (csrc/protocol.h) with a host collective: allreduce_min(int) -> int
+    must return the minimum over ranks (e.g. torch.distributed over gloo).
+    Returns (makespan, index) of the global winner."""
+    def cb(_ctx, x, out):
+        try:
+            out[0] = int(allreduce_min(int(x)))
+            return 0
+        except Exception:   # reported as PP_E_NCCL by the library
+            return 1
+    fn = ALLREDUCE_MIN_U64(cb)
+    win = (C.c_uint64 * 2)()
+    _check(lib().pp_round_exchange_host(local_makespan, local_index, rank, C.cast(fn, C.c_void_p), None, win))
+    return int(win[0]), int(win[1])
 
 
 def key_makespan(key):

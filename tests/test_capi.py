@@ -130,3 +130,53 @@ def test_no_cpu_fallback(pp):
     with pytest.raises(pp.PPError) as e:
         pp.Dfg(synth.toy12())
     assert e.value.code == -6
+
+
+def _threaded_exchange(pp, locals_):
+    """Every rank's pp_round_exchange_host at once (one thread per rank), with
+    an in-process min all-reduce built on a barrier."""
+    import threading
+    world = len(locals_)
+    bar = threading.Barrier(world)
+    vals = [None] * world
+    out = [None] * world
+
+    def worker(r):
+        def allreduce_min(x):
+            vals[r] = x
+            bar.wait()
+            m = min(vals)
+            bar.wait()
+            return m
+        out[r] = pp.round_exchange_host(locals_[r][0], locals_[r][1], r, allreduce_min)
+
+    ts = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return out
+
+
+def test_round_exchange_protocol(pp):
+    INF = pp.INFEASIBLE
+    # the lexicographic (makespan, global index) winner, for any rank layout
+    assert _threaded_exchange(pp, [(7, 3), (5, 40), (5, 90)]) == [(5, 40)] * 3
+    assert _threaded_exchange(pp, [(9, 0), (9, 50)]) == [(9, 0)] * 2
+    # empty slice on rank 0 and every real candidate infeasible: the empty
+    # slice must not win (ADVICE r1: index 2^64-1 would move the base)
+    assert _threaded_exchange(pp, [(INF, INF), (INF, 0), (INF, 1)]) == [(INF, 0)] * 3
+    assert _threaded_exchange(pp, [(INF, INF), (12, 1)]) == [(12, 1)] * 2
+    assert pp.round_key(5, INF, 3) == INF and pp.round_key(5, 0, 3) == pp.pack_key(5, 3)
+    assert pp.round_contrib(pp.round_key(5, 9, 2), 9, 2) == 9 and pp.round_contrib(pp.round_key(5, 9, 2), 4, 1) == INF
+    assert pp.round_contrib(INF, 4, 0) == INF
+    # the base moves iff the winner is not candidate 0 (= the base)
+    assert not pp.round_moves_base(0) and not pp.round_moves_base(INF) and pp.round_moves_base(17)
+
+
+def test_round_exchange_callback_failure(pp):
+    def bad(_x):
+        raise RuntimeError("peer died")
+    with pytest.raises(pp.PPError) as e:
+        pp.round_exchange_host(5, 1, 0, bad)
+    assert e.value.code == -7

@@ -2,10 +2,11 @@
 (SURVEY.md §8(e)): contiguous rank slices, the packed (makespan << 3 | rank)
 min key, the winner-index exchange, and the NCCL unique-id hand-off.
 
-The per-slice argmin here is the oracle's (no GPU on this box); slicing, key
-packing and decoding are the product's exported host functions, and the
-collectives follow the order of capi.cpp (min all-reduce of the key, then min
-all-reduce of the winner's index).  The result must not depend on the number
+The per-slice argmin here is the oracle's (no GPU on this box); slicing, the
+exchange (key packing, both min all-reduces, decoding) and the base-move rule
+are the product's own code: pp_round_exchange_host runs the protocol.h
+template that pp_search_best instantiates with NCCL, here with a gloo
+collective.  The result must not depend on the number
 of ranks (GPU-count invariance)."""
 import os
 import socket
@@ -28,7 +29,20 @@ def _free_port():
     return p
 
 
+def _u64_min_gloo(x):
+    """min over ranks of a u64 through a signed int64 gloo all-reduce
+    (x ^ 2^63 preserves the order)."""
+    v = x ^ (1 << 63)
+    t = torch.tensor([v - (1 << 64) if v >= 1 << 63 else v], dtype=torch.int64)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return (int(t.item()) % (1 << 64)) ^ (1 << 63)
+
+
 def _sharded_search(rank, world, spec_name, M, gen, seed, count, rounds, tau):
+    """pp_search_best's round loop with the oracle's per-slice argmin (no GPU
+    here): the slice, the exchange and the base-move rule are the library's
+    own code (pp_rank_slice, pp_round_exchange_host → csrc/protocol.h, the
+    same template the NCCL path instantiates; pp_round_moves_base)."""
     import oracle as O
     import synth
     import paper_1907_13257_b200 as pp
@@ -41,16 +55,12 @@ def _sharded_search(rank, world, spec_name, M, gen, seed, count, rounds, tau):
         if e > b:
             mk, idx = od.round(M, gen, seed + r, tau, base, b, e)
         else:
-            mk, idx = pp.INFEASIBLE, pp.INFEASIBLE
-        key = torch.tensor([pp.pack_key(mk, rank)], dtype=torch.int64)
-        dist.all_reduce(key, op=dist.ReduceOp.MIN)
-        k = int(key.item())
-        contrib = torch.tensor([idx if pp.key_rank(k) == rank else I64_MAX], dtype=torch.int64)
-        dist.all_reduce(contrib, op=dist.ReduceOp.MIN)
-        wmk, widx = pp.key_makespan(k), int(contrib.item())
+            mk, idx = pp.INFEASIBLE, pp.INFEASIBLE          # empty slice
+        wmk, widx = pp.round_exchange_host(mk, idx, rank, _u64_min_gloo)
         if best is None or wmk < best[0]:
             best = (wmk, widx, r)
-        base = O.gen(od.K, M, gen, seed + r, tau, base, widx)   # every rank moves to the winner
+        if gen == O.GEN_PERTURB and pp.round_moves_base(widx):
+            base = O.gen(od.K, M, gen, seed + r, tau, base, widx)   # every rank moves to the winner
     return best
 
 
@@ -71,7 +81,8 @@ def _worker(rank, world, port, cases, out):
 CASES = [("toy12", 2, 0, 0, 4096, 1, 0),          # GRAY exhaustive
          ("toy12", 3, 2, 17, 301, 4, 40),         # PERTURB rounds, ragged slices
          ("random", 4, 1, 99, 1001, 1, 0),        # RANDOM
-         ("biglstm", 2, 2, 5, 203, 3, 16)]
+         ("biglstm", 2, 2, 5, 203, 3, 16),
+         ("toy12", 4, 2, 3, 2, 3, 128)]            # count < world at 3 ranks: rank 0's slice is empty
 
 
 @pytest.mark.parametrize("world", [2, 3])

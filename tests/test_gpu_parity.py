@@ -68,6 +68,27 @@ def test_eval_placements_paper_dfgs(dfgs, M):
         assert got[0] == od.t1
 
 
+@pytest.mark.parametrize("M", [2, 3, 4, 8])
+def test_eval_placements_out_of_range_rows(dfgs, M):
+    """A row holding a value ≥ M is reported infeasible and touches nothing
+    else: the valid rows around it (same warps) keep their exact makespans
+    (free[] indexed past the lane's M slots)."""
+    rng = np.random.default_rng(100 + M)
+    spec, g, od = dfgs["inception_v3"]
+    count = 515
+    pl = rng.integers(0, M, size=(count, g.K), dtype=np.uint8)
+    bad = rng.choice(count, 40, replace=False)
+    for i in bad:
+        pl[i, rng.integers(0, g.K)] = rng.integers(M, 256)
+    got = pp.u64(g.eval_placements(M, torch.as_tensor(pl, device="cuda")))
+    for i in range(count):
+        want = pp.INFEASIBLE if i in set(bad.tolist()) else od.makespan(M, pl[i])
+        assert int(got[i]) == want, i
+    ex = pp.u64(pp.Dfg(synth.toy12()).eval_exact(M, torch.as_tensor(
+        np.array([[0] * 11 + [M], [0] * 12], dtype=np.uint8), device="cuda"))[0])
+    assert int(ex[0]) == pp.INFEASIBLE and int(ex[1]) == O.Dfg.from_spec(synth.toy12()).t1
+
+
 @pytest.mark.parametrize("gen", [O.GEN_RANDOM, O.GEN_PERTURB])
 @pytest.mark.parametrize("M", [2, 3, 4, 8])
 def test_eval_generated_paper_dfgs(dfgs, gen, M):

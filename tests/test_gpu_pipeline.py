@@ -76,6 +76,11 @@ def test_errors():
         g.pipeline_search(13, MICRO)            # more stages than ops
     with pytest.raises(pp.PPError):
         g.pipeline_search(2, [0])
+    # the u64 pipeline arithmetic is range-checked: a per-op
+    # overhead that would wrap is PP_E_RANGE, not a silent overflow
+    with pytest.raises(pp.PPError) as e:
+        g.pipeline_search(2, [65536], overhead=2**50)
+    assert e.value.code == -3
 
 
 @pytest.mark.parametrize("overhead", [1, 5_000_000])
