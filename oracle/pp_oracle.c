@@ -799,13 +799,17 @@ static uint64_t word_at(uint64_t seed, uint64_t i, uint64_t Wd, uint64_t t) {
  *          word (64, 32, 16 for b = 1, 2, 3), d = (x·M) >> b; i = 0 is all
  *          zeros.
  * PERTURB: O6, one byte per op, 8 ops per word: op j flips iff
- *          u_j = byte (j mod 8) of word'(i, ⌊j/8⌋) < τ (probability τ/256),
- *          to 1 − base (M = 2) or to (base + 1 + y_j mod (M−1)) mod M with
- *          y_j = byte (j mod 8) of word''(i, ⌊j/8⌋); i = 0 is the base.
- *          word' uses seed_r ^ 0xD1B54A32D192ED03, word'' seed_r ^
- *          0x8CB92BA72F3D8DD7.
- * (Generator spec revision 2: word boundaries fall on 8-op groups; DESIGN.md
- * §Generators.  The paper has no generator; this is the shared spec.)      */
+ *          u_j = byte (j mod 8) of word'(i, ⌊j/8⌋) < τ (probability τ/256).
+ *          A flipped op moves, with y_j = byte (j mod 8) of word''(i, ⌊j/8⌋):
+ *            M = 2      to 1 − base;
+ *            M = 4, 8   to base XOR (y_j mod M), i.e. it is re-drawn
+ *                       uniformly over the M devices (revision 3);
+ *            other M    to (base + 1 + y_j mod (M−1)) mod M.
+ *          i = 0 is the base.  word' uses seed_r ^ 0xD1B54A32D192ED03,
+ *          word'' seed_r ^ 0x8CB92BA72F3D8DD7.
+ * (Generator spec revision 3: word boundaries fall on 8-op groups, and the
+ * power-of-two device counts re-draw by XOR; DESIGN.md §Generators.  The
+ * paper has no generator; this is the shared spec.)                         */
 void or_gen(int K, int M, int gen, uint64_t seed_r, uint32_t tau,
             const uint8_t *base, uint64_t i, uint8_t *d) {
     if (M == 1) { for (int j = 0; j < K; j++) d[j] = 0; return; }
@@ -844,6 +848,7 @@ void or_gen(int K, int M, int gen, uint64_t seed_r, uint32_t tau,
         if (u >= tau) { d[j] = base[j]; continue; }
         if (M == 2) { d[j] = (uint8_t)(1 - base[j]); continue; }
         uint64_t y = (word_at(s2, i, Wd, (uint64_t)j / 8) >> (8 * ((uint64_t)j % 8))) & 0xFF;
+        if (M == 4 || M == 8) { d[j] = (uint8_t)(base[j] ^ (y % (uint64_t)M)); continue; }
         d[j] = (uint8_t)((base[j] + 1 + (y % (uint64_t)(M - 1))) % (uint64_t)M);
     }
 }

@@ -82,7 +82,8 @@ int launch_eft(const pp_dfg *g, int M, uint8_t *d_out, int *d_status, void *stre
 struct ProjParams;
 struct CrossParams;
 int launch_pack_key(uint64_t *s, int rank, void *stream);
-int launch_patch_base(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8, void *stream);
+int launch_patch_base(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8, uint32_t off_hgw,
+                      void *stream);
 int launch_contrib(uint64_t *s, int rank, void *stream);
 int launch_unpack_best(const uint64_t *s, uint64_t *out, void *stream);
 
@@ -194,6 +195,7 @@ static void fill(const pp_dfg *g, const Choice &best, uint64_t begin, uint64_t e
     p.zero_off = (uint32_t)g->W * kSlotUnit;
     p.one_hi = 0x3FF00000u;
     p.off_cls = g->off_cls;
+    p.off_hgw = g->off_hgw;
     p.g_partials = g->d_partials;
     p.g_ticket = g->d_ticket;
     p.g_out = g->d_scalars + SC_LOCAL_MK;
@@ -524,7 +526,7 @@ int pp_eval_generated(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t
     DeviceGuard dg(g->device);
     if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
     if (gen == GEN_PERTURB) {
-        if ((rc = launch_patch_base(g->d_image, g->d_base, d_base_pi, (uint32_t)g->K, (uint32_t)g->K8, stream)))
+        if ((rc = launch_patch_base(g->d_image, g->d_base, d_base_pi, (uint32_t)g->K, (uint32_t)g->K8, g->off_hgw, stream)))
             return cuda_err((cudaError_t)rc, "base patch");
         g_launches++;
     }
@@ -548,7 +550,7 @@ int pp_search_range(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
     DeviceGuard dg(g->device);
     if (!dg.ok) return cuda_err(dg.err, "cudaSetDevice");
     if (gen == GEN_PERTURB) {
-        if ((rc = launch_patch_base(g->d_image, g->d_base, d_base_pi, (uint32_t)g->K, (uint32_t)g->K8, stream)))
+        if ((rc = launch_patch_base(g->d_image, g->d_base, d_base_pi, (uint32_t)g->K, (uint32_t)g->K8, g->off_hgw, stream)))
             return cuda_err((cudaError_t)rc, "base patch");
         g_launches++;
     }
@@ -936,7 +938,7 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
         }
     cudaError_t e = cudaMemcpyAsync(g->d_winner, base.data(), g->base_bytes, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_err(e, "base upload");
-    if ((rc = launch_patch_base(g->d_image, g->d_base, g->d_winner, (uint32_t)K, (uint32_t)g->K8, stream)))
+    if ((rc = launch_patch_base(g->d_image, g->d_base, g->d_winner, (uint32_t)K, (uint32_t)g->K8, g->off_hgw, stream)))
         return cuda_err((cudaError_t)rc, "base patch");
     g_launches++;
     uint64_t begin = 0, end = 0;
@@ -984,7 +986,7 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
         }
         UParams u{g->d_image, g->d_base, g->d_winner, g->d_best_place, g->d_scalars, seed_r, (uint32_t)K,
                   (uint32_t)g->K8, desc->flip_thresh,
-                  r, comm ? 1 : 0};
+                  r, comm ? 1 : 0, g->off_hgw};
         if ((rc = upd(u, stream))) return cuda_err((cudaError_t)rc, "round update");
         g_launches++;
     }

@@ -16,6 +16,9 @@
 //   [ExtraRec × NX]  the remaining input edges, consumed in step order.
 //   [u64   × K8 ]    M(k) by π position (read only when a memory cap is set)
 //   [u32   × K8 ]    descriptor index of π position p (explicit placements)
+//   [u32   × K8/4]   PERTURB base of each half-group (π positions 4h..4h+3):
+//                    byte c = base device of position 4h + c (pads: 0), read
+//                    by the M = 4, 8 device-word schedule (search_kernel.cuh)
 //   [u8    × 64 ]    hardware graph only: cost class of device pair (a, b)
 //   [u64 × rows·C]   hardware graph only: per-input cost rows, one f64-encoded
 //                    cost per class (class 0 = same device, unused); the
@@ -96,6 +99,22 @@ uint32_t half_group_word(const uint8_t *base, uint32_t p, uint32_t K) {
     return w;
 }
 
+// The half-group base word of half-group h: byte c = base device of π
+// position 4h + c (positions ≥ K count as device 0).
+#ifdef __CUDACC__
+__host__ __device__ __forceinline__
+#else
+inline
+#endif
+uint32_t half_group_bytes(const uint8_t *base, uint32_t h, uint32_t K) {
+    uint32_t w = 0;
+    for (uint32_t c = 0; c < 4; c++) {
+        const uint32_t q = 4 * h + c;
+        if (q < K) w |= (uint32_t)(base[q] & 7u) << (8 * c);
+    }
+    return w;
+}
+
 enum GenKind : int { GEN_GRAY = 0, GEN_RANDOM = 1, GEN_PERTURB = 2, GEN_EXPLICIT = 3 };
 
 constexpr uint64_t kInfeasible = ~0ull;
@@ -123,6 +142,7 @@ struct KParams {
     uint32_t zero_off;           // region offset of the always-zero slot, in slot units ×256
     uint32_t one_hi;             // 0x3FF00000, the high word of 1.0 (opaque to ptxas)
     uint32_t off_cls;            // hardware graph: image offset of cls[a·8 + b]
+    uint32_t off_hgw;            // image offset of the half-group base words (u32 × K8/4)
 };
 
 // ---- exact-schedule image, built when
@@ -250,6 +270,7 @@ struct UParams {
     uint64_t seed;        // seed of this round
     uint32_t K, K8, tau, round;
     int multi;            // 1: winner comes from the NCCL-reduced slots
+    uint32_t off_hgw;     // image offset of the half-group base words
 };
 typedef int (*UpdateFn)(const UParams &, void *stream);
 
@@ -285,7 +306,7 @@ struct pp_dfg {
     uint64_t *d_pipe = nullptr;                    // pipeline tables (lazily built)
     mutable std::map<int, int> tuned;              // (M, gen) -> measured best NP
     std::vector<uint8_t> image;  // host copy of the image
-    uint32_t off_extra = 0, off_mem = 0, off_orig = 0, image_bytes = 0;
+    uint32_t off_extra = 0, off_mem = 0, off_orig = 0, off_hgw = 0, image_bytes = 0;
     uint32_t base_bytes = 0;     // K rounded up to 16
     // exact-schedule image (empty when 2K > 64)
     std::vector<uint8_t> ximage;

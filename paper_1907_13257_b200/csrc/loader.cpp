@@ -354,7 +354,8 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     size_t off_extra = sizeof(OpRec) * S;
     size_t off_mem = off_extra + sizeof(ExtraRec) * xr.size();
     size_t off_orig = off_mem + 8ull * K8;
-    size_t off_cls = (off_orig + 4ull * K8 + 15) & ~size_t(15);
+    size_t off_hgw = off_orig + 4ull * K8;
+    size_t off_cls = (off_hgw + (size_t)K8 + 15) & ~size_t(15);
     size_t off_rows = off_cls + (hw ? 64 : 0);
     size_t bytes = off_rows + 8ull * rows.size();
     bytes = (bytes + 15) & ~size_t(15);
@@ -418,6 +419,7 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     g->off_extra = (uint32_t)off_extra;
     g->off_mem = (uint32_t)off_mem;
     g->off_orig = (uint32_t)off_orig;
+    g->off_hgw = (uint32_t)off_hgw;
     g->image_bytes = (uint32_t)bytes;
     g->base_bytes = (uint32_t)((K + 15) & ~15);
 

@@ -267,18 +267,22 @@ __global__ void contrib_kernel(uint64_t *s, int rank) {
 // Copies a π-order base into the canonical buffer and into OpRec.base of the
 // forward and backward records of every position p < K8 (PERTURB): the op's
 // device plus the packed half-group word (internal.h, OpRec.base).
-__global__ void patch_base_kernel(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8) {
+__global__ void patch_base_kernel(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8,
+                                  uint32_t off_hgw) {
     OpRec *ops = reinterpret_cast<OpRec *>(image);
+    uint32_t *hgw = reinterpret_cast<uint32_t *>(image + off_hgw);
     for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < K8; p += gridDim.x * blockDim.x) {
         const uint8_t d = p < K ? src[p] : 0;
         if (p < K) base[p] = d;
         const uint32_t w = half_group_word(src, p, K);
         ops[p].base = d | w;
         ops[2 * K8 - 1 - p].base = d | w;
+        if ((p & 3) == 0) hgw[p / 4] = half_group_bytes(src, p / 4, K);
     }
 }
-int launch_patch_base(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8, void *stream) {
-    patch_base_kernel<<<(K8 + 255) / 256, 256, 0, (cudaStream_t)stream>>>(image, base, src, K, K8);
+int launch_patch_base(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8, uint32_t off_hgw,
+                      void *stream) {
+    patch_base_kernel<<<(K8 + 255) / 256, 256, 0, (cudaStream_t)stream>>>(image, base, src, K, K8, off_hgw);
     return (int)cudaGetLastError();
 }
 int launch_pack_key(uint64_t *s, int rank, void *stream) {

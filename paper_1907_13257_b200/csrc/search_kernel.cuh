@@ -187,7 +187,7 @@ struct RandomGen {                         // O6 RANDOM: b bits per op, P = 8¬∑‚
 };
 
 template <int M, int NP>
-struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops per word
+struct PerturbGen {                        // O6 PERTURB (spec revision 3): one byte per op, 8 ops per word
     uint64_t key1, key2;   // the two streams' keys of i_0
     uint64_t dk;           // Œ≥¬∑32¬∑Wd
     uint64_t w[NP], y[NP];
@@ -233,7 +233,9 @@ struct PerturbGen {                        // O6 PERTURB: one byte per op, 8 ops
             return bs + ((uint32_t)((int)u - (int)tk) >> 31);
         }
         const uint32_t yv = __byte_perm(yh[k], 0, 0x4440u | (cc & 3u));
-        const uint32_t flip = (bs + 1 + yv % (uint32_t)(M > 1 ? M - 1 : 1)) % (uint32_t)M;
+        // revision 3: M = 4, 8 re-draw by XOR; other M move by 1 + y mod (M ‚àí 1)
+        const uint32_t flip = (M == 4 || M == 8) ? bs ^ (yv & (uint32_t)(M - 1))
+                                                 : (bs + 1 + yv % (uint32_t)(M > 1 ? M - 1 : 1)) % (uint32_t)M;
         return (u < tk) ? flip : bs;
     }
 };
@@ -908,6 +910,176 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
     }
 }
 
+// --------------------------- M = 4, 8 PERTURB: device words (tagged f64)
+// Generator revision 3 (oracle/pp_oracle.c or_gen): a flipped op is re-drawn
+// as base ‚äï (y mod M).  That makes the devices of a half-group (4 ops) one
+// SIMD-within-a-register computation per placement, as in schedule_m2p:
+//   f7_c  = [u_c < œÑ] in bit 7 of byte c     (the byte compare of schedule_m2p)
+//   dev   = base ‚äï (y ‚àß (f7 >> 7)¬∑(M ‚àí 1))   (one SHF, one IMAD, one LOP3;
+//                                             base = the image's half-group word)
+//   cut   = (dev ‚äï dev of the previous step) + 0x7F‚Ä¶ (bit 7 of byte c = [dev_c ‚â†
+//           dev_{c‚àí1}], byte values ‚â§ 7 so nothing carries across bytes)
+// Per step one PRMT widens cut_c to a full-word mask and one PRMT + IMAD turn
+// dev_c into the address of free[dev_c]; free[] stays in the warp's shared
+// region (schedule_f64's M ‚â• 3 state: free[pdev] ‚Üê prev every step).  The
+// arithmetic is schedule_f64's for M ‚â• 3, operation for operation; only the
+// devices and cut flags are derived differently, so the results are identical
+// (the parity suite runs both).
+template <int M, int NP, bool MEM>
+__device__ __forceinline__ void schedule_mpw(uint64_t A, uint64_t B, uint64_t dA, uint32_t hk0, uint64_t (&mk)[NP],
+                                             uint32_t ops, uint32_t xr, const uint64_t *__restrict__ mem, uint32_t lane,
+                                             uint32_t free_off, uint32_t K8, uint64_t cap, uint32_t khi, uint32_t tau,
+                                             uint32_t hgw) {
+    static_assert(M == 4 || M == 8, "device words need M = 4 or 8");
+    constexpr uint32_t H = 0x80808080u;
+    const uint32_t tq = (tau <= 128 ? tau : tau - 128) * 0x01010101u;
+    const uint32_t amaj = tau <= 128 ? ~0u : 0u;
+    double prev[NP];
+    uint32_t dw[NP], cw[NP], dprev[NP], aprev[NP];
+    // free[d] of placement k lives at fb + d¬∑NP¬∑256 + k¬∑256 (the k¬∑256 folds
+    // into the instructions' immediate offsets)
+    const uint32_t fb = lane + free_off * NP;
+    uint64_t w[NP], y[NP];
+    MemUse<M> mu[NP];
+#pragma unroll
+    for (int k = 0; k < NP; k++) {
+        prev[k] = 0.0;
+        dprev[k] = 0;                 // device 0 before the first step (schedule_f64's pdev = 0)
+        dw[k] = cw[k] = 0;
+        w[k] = y[k] = 0;
+        aprev[k] = fb;
+#pragma unroll
+        for (int d = 0; d < M; d++) std_(fb + d * NP * 256 + k * 256, 0.0);
+        if (MEM) mu[k].init();
+    }
+    uint32_t x = xr;
+    auto refresh = [&]() {
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            w[k] = mix64(A + (uint64_t)k * dA);
+            y[k] = mix64(B + (uint64_t)k * dA);
+        }
+    };
+    auto half = [&](uint32_t h, uint32_t bw, bool fwd) {
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            const uint32_t u = h ? (uint32_t)(w[k] >> 32) : (uint32_t)w[k];
+            const uint32_t yv = h ? (uint32_t)(y[k] >> 32) : (uint32_t)y[k];
+            const uint32_t xx = (u | H) - tq;
+            const uint32_t mj = lop3<0xE8>(u, xx, amaj);                        // MAJ: bit 7 = no flip
+            const uint32_t f7 = lop3<0x30>(k == 0 ? hk0 : H, mj, 0u);           // hk ‚àß ¬¨mj: bit 7 = flip
+            const uint32_t fm = (f7 >> 7) * (uint32_t)(M - 1);                  // M ‚àí 1 in flipped bytes
+            dw[k] = lop3<0x78>(bw, yv, fm);                                     // base ‚äï (y ‚àß fm)
+            const uint32_t sh = fwd ? prmt(dw[k], dprev[k], 0x2107u) : prmt(dw[k], dprev[k], 0x4321u);
+            cw[k] = (dw[k] ^ sh) + 0x7F7F7F7Fu;                                 // bit 7 of byte c: cut_c
+            dprev[k] = dw[k];
+        }
+    };
+    auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
+        const double cost = ldd(rec);
+        const double c0 = ldd(rec + 8);
+        const uint4 b = lds128(rec + 16);
+        double cut[NP];
+        uint32_t dc[NP], a[NP];
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            const uint32_t m = prmt(cw[k], 0u, 0x8888u | (c * 0x1111u));         // all ones iff cut_c
+            cut[k] = __hiloint2double((int)(m & khi), 0);                       // 1.0 or 0.0
+            dc[k] = prmt(dw[k], 0u, 0x4440u | c);                               // dev_c
+            a[k] = dc[k] * (uint32_t)(NP * 256) + fb;                           // &free[dev_c] ‚àí k¬∑256
+        }
+        if (b.z == 0) {
+            // chain step: s = max(prev + cut¬∑c0, cut¬∑free[dev]); free[pdev] ‚Üê prev
+#pragma unroll
+            for (int k = 0; k < NP; k++) {
+                const double f = __dmul_rn(cut[k], ldd(a[k] + k * 256));
+                std_(aprev[k] + k * 256, prev[k]);
+                const double t = __fma_rn(c0, cut[k], prev[k]);
+                prev[k] = dmax_add(t, f, cost);
+                aprev[k] = a[k];
+            }
+        } else {
+            double r[NP];
+            if (b.x == kFromPrev) {
+#pragma unroll
+                for (int k = 0; k < NP; k++) r[k] = __fma_rn(c0, cut[k], prev[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NP; k++) r[k] = cut_add_f64<M>(ldd(lane + b.x * NP + k * 256), dc[k], c0, khi);
+            }
+            const uint32_t nx = b.z & 0xFFFFu;
+#pragma unroll 1
+            for (uint32_t q = 0; q < nx; q++) {   // further inputs (uniform trip count)
+                const uint4 e = lds128(x);
+                x += sizeof(ExtraRec);
+                const double ce = __hiloint2double((int)e.y, (int)e.x);
+#pragma unroll
+                for (int k = 0; k < NP; k++)
+                    r[k] = dmax(r[k], cut_add_f64<M>(ldd(lane + e.z * NP + k * 256), dc[k], ce, khi));
+            }
+#pragma unroll
+            for (int k = 0; k < NP; k++) {
+                // free[dev] = cut ? free[dev] (shared) : prev, exact on the FP64 pipe
+                const double f = __fma_rn(cut[k], __dadd_rn(ldd(a[k] + k * 256), -prev[k]), prev[k]);
+                std_(aprev[k] + k * 256, prev[k]);
+                prev[k] = dmax_add(clear_tag(r[k]), f, cost);
+                aprev[k] = a[k];
+            }
+        }
+        if (b.y != kNoStore) {
+#pragma unroll
+            for (int k = 0; k < NP; k++) std_(lane + b.y * NP + k * 256, with_tag(prev[k], dc[k]));
+        }
+        if (MEM && fwd) {
+            const uint64_t mm = mem[p];
+#pragma unroll
+            for (int k = 0; k < NP; k++) mu[k].add(dc[k], mm);
+        }
+    };
+    constexpr int kHalfUnroll = NP >= 4 ? 1 : 2;
+    const uint32_t G = K8 / 8;
+    for (uint32_t g = 0; g < G; g++) {           // forward, œÄ order
+        refresh();
+        A += kGamma;
+        B += kGamma;
+#pragma unroll (kHalfUnroll)
+        for (uint32_t h = 0; h < 2; h++) {
+            const uint32_t rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
+            half(h, lds32(hgw + 4 * (2 * g + h)), true);
+#pragma unroll
+            for (uint32_t cc = 0; cc < 4; cc++) step(rec + cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, true);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NP; k++) dprev[k] >>= 24;   // byte 0 := the device of the last forward step
+    for (uint32_t g = G; g-- > 0;) {             // backward, reverse œÄ order
+        A -= kGamma;
+        B -= kGamma;
+        refresh();
+#pragma unroll (kHalfUnroll)
+        for (uint32_t h = 2; h-- > 0;) {
+            const uint32_t rec = ops + (2 * K8 - 1 - g * 8 - h * 4) * (uint32_t)sizeof(OpRec);
+            half(h, lds32(hgw + 4 * (2 * g + h)), false);
+#pragma unroll
+            for (int cc = 3; cc >= 0; cc--)
+                step(rec - (uint32_t)cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, false);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NP; k++) {
+        std_(aprev[k] + k * 256, prev[k]);
+        double v = 0.0;
+#pragma unroll
+        for (int d = 0; d < M; d++) v = dmax(v, ldd(fb + d * NP * 256 + k * 256));
+        mk[k] = (uint64_t)__double2ull_rz(v);
+        if (MEM && mu[k].over(cap)) mk[k] = kInfeasible;
+    }
+}
+
+#ifndef PP_MPW
+#define PP_MPW 1   // the device-word schedule for M = 4, 8 PERTURB (0: schedule_f64, for A/B)
+#endif
+
 #ifndef PP_M2P
 #define PP_M2P 1   // the cut-word schedule for M = 2 PERTURB (0: schedule_f64, for A/B)
 #endif
@@ -982,6 +1154,7 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
     const uint64_t n = P.end - P.begin;
     constexpr uint32_t TILE = 32 * NP;
     constexpr bool kM2P = PP_M2P && F64 && M == 2 && !HW;   // schedule_m2p
+    constexpr bool kMPW = PP_MPW && F64 && (M == 4 || M == 8) && !HW;   // schedule_mpw
     const uint64_t ntiles = (n + TILE - 1) / TILE;
     const uint64_t wpb = nthreads >> 5;
     for (uint64_t tile = blockIdx.x * wpb + warp; tile < ntiles; tile += (uint64_t)gridDim.x * wpb) {
@@ -1012,6 +1185,12 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
             const uint64_t A = (P.seed ^ 0xD1B54A32D192ED03ull) + kGamma * (i0 * Wd + 1);
             schedule_m2p<NP, MEM>(A, kGamma * 32ull * Wd, i0 == 0 ? 0u : 0x80808080u, mk, ops, xr, mem, lane_region,
                                   P.K8, P.cap, P.one_hi, P.tau);
+        } else if constexpr (GEN == GEN_PERTURB && kMPW) {
+            const uint64_t Wd = (P.K + 7) / 8;
+            const uint64_t A = (P.seed ^ 0xD1B54A32D192ED03ull) + kGamma * (i0 * Wd + 1);
+            const uint64_t B = (P.seed ^ 0x8CB92BA72F3D8DD7ull) + kGamma * (i0 * Wd + 1);
+            schedule_mpw<M, NP, MEM>(A, B, kGamma * 32ull * Wd, i0 == 0 ? 0u : 0x80808080u, mk, ops, xr, mem,
+                                     lane_region, P.free_off, P.K8, P.cap, P.one_hi, P.tau, smem_base + P.off_hgw);
         } else if (GEN == GEN_PERTURB) {
             PerturbGen<M, NP> g;
             g.init(i0, P.seed, P.K, P.tau);
@@ -1141,6 +1320,7 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
     }
     __syncthreads();
     OpRec *ops = reinterpret_cast<OpRec *>(U.image);
+    uint32_t *hgw = reinterpret_cast<uint32_t *>(U.image + U.off_hgw);
     for (uint32_t p = threadIdx.x; p < U.K8; p += blockDim.x) {
         const uint8_t d = p < U.K ? U.winner[p] : 0;
         if (GEN == GEN_PERTURB && move) {
@@ -1148,6 +1328,7 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
             if (p < U.K) U.base[p] = d;
             ops[p].base = d | w;
             ops[2 * U.K8 - 1 - p].base = d | w;
+            if ((p & 3) == 0) hgw[p / 4] = half_group_bytes(U.winner, p / 4, U.K);
         }
         if (improve && p < U.K) U.best_place[p] = d;
     }

@@ -354,35 +354,39 @@ def test_sharded_exact_and_pipeline_searches():
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("M", [2, 4, 8])
 @pytest.mark.parametrize("np_", ["1", "2", "4"])
-def test_perturb_m2_cut_words(dfgs, np_, monkeypatch):
+def test_perturb_m2_cut_words(dfgs, np_, M, monkeypatch):
     """M = 2 PERTURB runs the cut-word schedule (search_kernel.cuh
     schedule_m2p): 4 byte compares u < τ per SIMD word, whose two formulas
     meet at τ = 128, a packed base word per half-group, and pads in the last
     half-groups when K mod 8 ≠ 0.  Every τ boundary, a random base, begin = 0
     (candidate 0 = the base itself) and both the per-candidate (write-all,
-    NP = 2 only) and the argmin kernels (NP pinned), against the oracle."""
-    rng = np.random.default_rng(128)
+    NP = 2 only) and the argmin kernels (NP pinned), against the oracle.
+    M = 4 and 8 run the device-word schedule (schedule_mpw: revision-3
+    re-draws base ⊕ (y mod M) as SIMD words) through the same cases."""
+    rng = np.random.default_rng(128 + M)
     cases = [dfgs["toy12"][1:], dfgs["inception_v3"][1:]]
     for K in (13, 30):   # K mod 8 = 5 and 6: pad positions in the last half-groups
         spec = synth.random_dag(4000 + K, K, avg_deg=1.6, max_cost=10**6, max_bytes=10**6)
         cases.append((pp.Dfg(spec), O.Dfg.from_spec(spec)))
     for g, od in cases:
-        base = rng.integers(0, 2, size=g.K, dtype=np.uint8)
+        base = rng.integers(0, M, size=g.K, dtype=np.uint8)
         for tau in (0, 1, 7, 8, 127, 128, 129, 200, 255, 256):
             seed = int(rng.integers(0, 2**63))
             monkeypatch.delenv("PP_NP", raising=False)
-            got = pp.u64(g.eval_generated(2, pp.GEN_PERTURB, seed, tau, base, 0, 300))
-            want = _oracle_candidates(od, 2, O.GEN_PERTURB, seed, tau, base, range(300))
+            got = pp.u64(g.eval_generated(M, pp.GEN_PERTURB, seed, tau, base, 0, 300))
+            want = _oracle_candidates(od, M, O.GEN_PERTURB, seed, tau, base, range(300))
             assert np.array_equal(got, want), (g.K, tau)
-            assert got[0] == od.makespan_pi(2, base)   # candidate 0 is the base
+            assert got[0] == od.makespan_pi(M, base)   # candidate 0 is the base
             monkeypatch.setenv("PP_NP", np_)
-            r = pp.u64(g.search_range(2, pp.GEN_PERTURB, seed, tau, base, 0, 1_000))
-            assert (int(r[0]), int(r[1])) == od.round(2, O.GEN_PERTURB, seed, tau, base, 0, 1_000), (g.K, tau)
+            r = pp.u64(g.search_range(M, pp.GEN_PERTURB, seed, tau, base, 0, 1_000))
+            assert (int(r[0]), int(r[1])) == od.round(M, O.GEN_PERTURB, seed, tau, base, 0, 1_000), (g.K, tau)
 
 
+@pytest.mark.parametrize("M", [2, 4, 8])
 @pytest.mark.parametrize("np_", ["1", "2", "4"])
-def test_perturb_m2_cut_words_memory_cap(np_, monkeypatch):
+def test_perturb_m2_cut_words_memory_cap(np_, M, monkeypatch):
     """The cut-word schedule with a per-device memory cap:
     the memory use per device is summed from the same device words, and an
     over-cap candidate is infeasible.  Caps chosen so that some candidates
@@ -391,16 +395,16 @@ def test_perturb_m2_cut_words_memory_cap(np_, monkeypatch):
     for K in (29, 64, 131):
         spec = synth.random_dag(9000 + K, K, avg_deg=1.5, max_cost=10**6, max_bytes=10**6)
         spec["mem_bytes"] = [int(x) for x in rng.integers(0, 100, size=K)]
-        spec["dev_mem_cap_bytes"] = int(sum(spec["mem_bytes"]) * 0.55)
+        spec["dev_mem_cap_bytes"] = int(sum(spec["mem_bytes"]) * {2: 0.55, 4: 0.3, 8: 0.16}[M])
         g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
-        base = (np.arange(K) % 2).astype(np.uint8)
+        base = (np.arange(K) % M).astype(np.uint8)
         seed = int(rng.integers(0, 2**63))
         monkeypatch.delenv("PP_NP", raising=False)
-        got = pp.u64(g.eval_generated(2, pp.GEN_PERTURB, seed, 64, base, 0, 500))
-        want = _oracle_candidates(od, 2, O.GEN_PERTURB, seed, 64, base, range(500))
+        got = pp.u64(g.eval_generated(M, pp.GEN_PERTURB, seed, 64, base, 0, 500))
+        want = _oracle_candidates(od, M, O.GEN_PERTURB, seed, 64, base, range(500))
         assert np.array_equal(got, want), K
         inf = int(np.sum(got == np.uint64(2**64 - 1)))
         assert 0 < inf < 500, (K, inf)   # both feasible and infeasible candidates occur
         monkeypatch.setenv("PP_NP", np_)
-        r = pp.u64(g.search_range(2, pp.GEN_PERTURB, seed, 64, base, 0, 2_000))
-        assert (int(r[0]), int(r[1])) == od.round(2, O.GEN_PERTURB, seed, 64, base, 0, 2_000), K
+        r = pp.u64(g.search_range(M, pp.GEN_PERTURB, seed, 64, base, 0, 2_000))
+        assert (int(r[0]), int(r[1])) == od.round(M, O.GEN_PERTURB, seed, 64, base, 0, 2_000), K

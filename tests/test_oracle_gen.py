@@ -57,20 +57,37 @@ def test_random_index0_and_distribution(M):
                               O.gen(K, M, O.GEN_RANDOM, 99, 0, None, 5))
 
 
-@pytest.mark.parametrize("M", [2, 3, 4, 8])
+def _redraw(M):
+    """revision 3: a flipped op is re-drawn uniformly (XOR) for M = 4, 8"""
+    return M in (4, 8)
+
+
+@pytest.mark.parametrize("M", [2, 3, 4, 5, 8])
 def test_perturb_rules(M):
     K = 150
     rng = np.random.default_rng(M)
     base = rng.integers(0, M, K).astype(np.uint8)
     assert np.array_equal(O.gen(K, M, O.GEN_PERTURB, 7, 255, base, 0), base)      # i = 0 is the base
-    for i in range(1, 30):
+    moved = np.zeros(M)
+    for i in range(1, 200):
         assert np.array_equal(O.gen(K, M, O.GEN_PERTURB, 7, 0, base, i), base)    # τ = 0: no flips
-        d = O.gen(K, M, O.GEN_PERTURB, 7, 256, base, i)                           # τ = 256: all flip
-        assert (d != base).all() and d.max() < M
+        d = O.gen(K, M, O.GEN_PERTURB, 7, 256, base, i)                           # τ = 256: every op flips
+        assert d.max() < M
         if M == 2:
             assert np.array_equal(d, 1 - base)
+        if _redraw(M):
+            moved += np.bincount(d ^ base, minlength=M)                           # XOR offset of the re-draw
+        else:
+            assert (d != base).all()
+            moved += np.bincount((d.astype(int) - base) % M, minlength=M)         # offset 1 .. M−1
+    freq = moved / moved.sum()
+    if _redraw(M):
+        assert np.allclose(freq, 1 / M, atol=0.01)        # re-drawn uniformly over the M devices
+    elif M > 2:
+        assert freq[0] == 0 and np.allclose(freq[1:], 1 / (M - 1), atol=0.015)
+    change = (M - 1) / M if _redraw(M) else 1.0
     flips = sum(int((O.gen(K, M, O.GEN_PERTURB, 11, 32, base, i) != base).sum()) for i in range(1, 300))
-    assert abs(flips / (299 * K) - 32 / 256) < 0.01                               # rate τ/256
+    assert abs(flips / (299 * K) - change * 32 / 256) < 0.01                      # rate τ/256 · P(change)
 
 
 def test_m1_is_all_zero():
@@ -113,3 +130,76 @@ def test_perturb_layout_pinned_by_published_vector(tau):
     d = O.gen(K, M, O.GEN_PERTURB, seed_r, tau, base, 1)
     u = [(SM64_2ND >> (8 * j)) & 0xFF for j in range(8)]
     assert [int(x) for x in d] == [1 - int(base[j]) if u[j] < tau else int(base[j]) for j in range(8)]
+
+
+# Layout pins for the remaining branches (VERDICT r1 "what's weak" #1): more
+# than one word per candidate, the non-power-of-two RANDOM map (x·M) >> b, and
+# the PERTURB y-stream for M ≥ 3.  Each seed puts a word of the stream at a
+# published SplitMix64 state, so the expected devices come from the literal.
+SM64_1ST = 6457827717110365317
+GAMMA = 0x9E3779B97F4A7C15
+C2 = 0x8CB92BA72F3D8DD7
+
+
+def test_random_two_words_per_candidate():
+    # K = 80, M = 2: P = 64 ops per word, Wd = 2; candidate 1 reads words
+    # i·Wd + t + 1 = 3 and 4, i.e. states seed + 3γ and seed + 4γ.  With
+    # seed = 1234567 − 2γ these are the published 1st and 2nd outputs (a
+    # transposed index i + t·Wd + 1 = 2, 4 would read the unpublished state
+    # 1234567 itself for word 0).
+    seed = (1234567 - 2 * GAMMA) % 2**64
+    d = O.gen(80, 2, O.GEN_RANDOM, seed, 0, None, 1)
+    want = [(SM64_1ST >> j) & 1 for j in range(64)] + [(SM64_2ND >> j) & 1 for j in range(16)]
+    assert [int(x) for x in d] == want
+    # M = 4 (P = 32, Wd = 3 at K = 80): words 4, 5, 6 of candidate 1
+    seed = (1234567 - 3 * GAMMA) % 2**64
+    d = O.gen(80, 4, O.GEN_RANDOM, seed, 0, None, 1)
+    words = [SM64_1ST, SM64_2ND, SM64_3RD]
+    assert [int(x) for x in d] == [(words[j // 32] >> (2 * (j % 32))) & 3 for j in range(80)]
+
+
+@pytest.mark.parametrize("M", [3, 5, 6, 7])
+def test_random_non_power_of_two_map(M):
+    # b = ⌈log2 M⌉ bit fields of the 2nd output, mapped by (x·M) >> b
+    b = (M - 1).bit_length()
+    P = 8 * (8 // b)
+    K = P                              # Wd = 1
+    d = O.gen(K, M, O.GEN_RANDOM, 1234567, 0, None, 1)
+    x = [(SM64_2ND >> (b * j)) & ((1 << b) - 1) for j in range(K)]
+    assert [int(v) for v in d] == [(v * M) >> b for v in x]
+    if M == 3:                         # the map {0,1,2,3} → {0,0,1,2}
+        assert [(v * 3) >> 2 for v in range(4)] == [0, 0, 1, 2]
+
+
+@pytest.mark.parametrize("M", [3, 4, 5, 8])
+def test_perturb_y_stream_pinned(M):
+    # τ = 256 (every op flips); seed_r chosen so that the y-stream's seed is
+    # 1234567, so y_j = byte j of the 2nd published output (K = 8, Wd = 1)
+    K = 8
+    seed_r = 1234567 ^ C2
+    base = np.array([0, 1, 2, 0, 1, 2, 0, 1], dtype=np.uint8) % M
+    d = O.gen(K, M, O.GEN_PERTURB, seed_r, 256, base, 1)
+    y = [(SM64_2ND >> (8 * j)) & 0xFF for j in range(8)]
+    if M in (4, 8):                    # revision 3: base XOR (y mod M)
+        want = [int(base[j]) ^ (y[j] % M) for j in range(8)]
+    else:                              # (base + 1 + y mod (M−1)) mod M
+        want = [(int(base[j]) + 1 + y[j] % (M - 1)) % M for j in range(8)]
+    assert [int(v) for v in d] == want
+    # the u-stream decides which ops flip: with τ = 0 none does
+    assert np.array_equal(O.gen(K, M, O.GEN_PERTURB, seed_r, 0, base, 1), base)
+
+
+def test_perturb_two_words_per_candidate():
+    # K = 16, Wd = 2: candidate 1 reads u-words 3 and 4 → the 1st and 2nd
+    # outputs when the u-stream's seed is 1234567 − 2γ (M = 2, τ = 128)
+    seed_r = ((1234567 - 2 * GAMMA) % 2**64) ^ C1
+    base = np.array([j % 2 for j in range(16)], dtype=np.uint8)
+    d = O.gen(16, 2, O.GEN_PERTURB, seed_r, 128, base, 1)
+    u = [(SM64_1ST >> (8 * j)) & 0xFF for j in range(8)] + [(SM64_2ND >> (8 * j)) & 0xFF for j in range(8)]
+    assert [int(x) for x in d] == [1 - int(base[j]) if u[j] < 128 else int(base[j]) for j in range(16)]
+    # and the y-stream's second word for M = 8 (τ = 256)
+    seed_r = ((1234567 - 2 * GAMMA) % 2**64) ^ C2
+    base8 = np.array([j % 8 for j in range(16)], dtype=np.uint8)
+    d = O.gen(16, 8, O.GEN_PERTURB, seed_r, 256, base8, 1)
+    y = [(SM64_1ST >> (8 * j)) & 0xFF for j in range(8)] + [(SM64_2ND >> (8 * j)) & 0xFF for j in range(8)]
+    assert [int(x) for x in d] == [int(base8[j]) ^ (y[j] % 8) for j in range(16)]
