@@ -200,7 +200,10 @@ def run_reference(args):
                                        f"{args.workload}-shaped DFG per step (the GPU step runs {rounds} x {args.count}) "
                                        f"+ projection N=1..{args.nmax} + crossover"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "crossover_n_star": x.n_star}
+            "sample_result": {"T_M_ps": r.best_makespan_ps, "crossover_n_star": x.n_star,
+                              "note": f"from the {n_step}-candidate sample above, not the full "
+                                      f"{rounds} x {args.count} search: it differs from the GPU arm's full-size "
+                                      f"result, which the GPU line's 'parity' key checks against the oracle"}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -218,6 +221,59 @@ def config_dict(args, spec, per_step=None):
             "projection": f"M in {{1,{args.M}}}, N=1..{args.nmax}, EQ5, ring AR on",
             "l2": "flushed between timed steps (256 MiB write); inputs live on-chip",
             **({"hardware_graph": HW_GRAPHS[args.hw]} if args.hw != "none" else {})}
+
+
+# ------------------------------------------------------------ parity leg
+def parity_check(args, spec, r, x, cells_np, mode):
+    """The GPU step's result against the CPU oracle (oracle/), outside the
+    timed region: T_M, the winning index, round and placement, every
+    projection cell, N* and N* vs the best DP.  mode "live" re-runs the full
+    search with the oracle, its rounds sliced over the host's threads
+    (tools/oracle_fullsize.py, the same driver that wrote the golden file);
+    mode "golden" compares with tests/golden/fullsize_r02.json (written by
+    that driver from oracle/ alone) when it holds this exact search."""
+    import importlib.util
+    import oracle as O
+    from synth import configs
+    out = {"mode": mode}
+    t = time.perf_counter()
+    od = O.Dfg.from_spec(spec)
+    gen_name = args.gen
+    if mode == "live":
+        import concurrent.futures as cf
+        sp = importlib.util.spec_from_file_location("oracle_fullsize", os.path.join(ROOT, "tools", "oracle_fullsize.py"))
+        F = importlib.util.module_from_spec(sp)
+        sp.loader.exec_module(F)
+        threads = os.cpu_count() or 1
+        base = od.eft(args.M) if (gen_name == "perturb" and args.base == "eft") else None
+        gens = {"perturb": O.GEN_PERTURB, "random": O.GEN_RANDOM}
+        with cf.ThreadPoolExecutor(max_workers=threads) as pool:
+            want = F.sliced_search(pool, od, args.M, gens[gen_name], SEED, args.count, args.rounds,
+                                   args.tau if gen_name == "perturb" else 0, base, 4 * threads)
+        out["reference"] = f"oracle/ live, rounds sliced over {threads} host threads"
+    else:
+        key = configs.search_key(args.workload, args.M, gen_name, args.count, args.rounds, tau=args.tau, seed=SEED,
+                                 base=args.base)
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "fullsize_r02.json")))["searches"]
+        if key not in gold:
+            return {"mode": mode, "reference": f"no golden entry for {key}"}
+        want = gold[key]
+        out["reference"] = f"tests/golden/fullsize_r02.json[{key}] (written from oracle/ by tools/oracle_fullsize.py)"
+    out["T_M"] = r.best_makespan_ps == want["T_M"]
+    out["best_index"] = r.best_index == want["best_index"]
+    out["best_round"] = r.best_round == want["best_round"]
+    out["placement"] = "".join(map(str, r.placement)) == want["placement"]
+    sc = scenario(args, od.t1, od.grad_bytes)
+    oc = O.Scenario.from_spec(sc).project([1, args.M], [od.t1, want["T_M"]], args.nmax)
+    ox = O.crossover(oc, [1, args.M], args.nmax)
+    got = cells_np.reshape(-1)
+    out["cells"] = all(((int(c["C_hi"]) << 64 | int(c["C_lo"])), int(c["feasible"])) == (o.C, o.feasible)
+                       if o.feasible else int(c["feasible"]) == 0 for c, o in zip(got, oc))
+    out["n_star"] = x.n_star == ox.n_star
+    out["n_star_vs_best_dp"] = x.n_star_vs_best_dp == ox.n_star_vs_best_dp
+    out["all"] = all(v for k, v in out.items() if isinstance(v, bool))
+    out["oracle_s"] = round(time.perf_counter() - t, 1)
+    return out
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -257,7 +313,7 @@ def run_pp(args):
                           stream=stream)
         cells = pp.project_e2e(sc, [1, M], [g.t1, r.best_makespan_ps], args.nmax, device=local, stream=stream)
         x = pp.crossover(cells, [1, M], args.nmax, best_m=False, stream=stream)
-        return r, x
+        return r, x, cells
 
     for _ in range(args.warmup):
         step()
@@ -321,7 +377,8 @@ def run_pp(args):
         kern_avg_s = (kern_ms_max / max(1, kern_n)) / 1e3
         achieved_ops = ops * per_launch / kern_avg_s
         achieved_smem = smem_b * per_launch / kern_avg_s
-        r, x = results[-1]
+        r, x, cells = results[-1]
+        cells_np = pp.cells_to_numpy(cells)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
@@ -347,6 +404,9 @@ def run_pp(args):
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                                     "sample": f"first {n} {args.gen.upper()} candidates of round 0 of the same "
                                               f"stream, {dt:.1f} s, single thread (nproc={os.cpu_count()})"}
+        if args.parity != "off":
+            mode = args.parity if args.parity != "auto" else ("live" if world == 1 else "golden")
+            line["parity"] = parity_check(args, spec, r, x, cells_np, mode)
         print(json.dumps(line), flush=True)
     g.close()
     if comm is not None:
@@ -374,6 +434,9 @@ def main():
                     help="evaluate on a general hardware graph instead of the uniform link")
     ap.add_argument("--ref-sample", type=int, default=200_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parity", default="auto", choices=["auto", "live", "golden", "off"],
+                    help="check the step's result against the oracle: live (full oracle run over the host's "
+                         "threads), golden (the committed oracle golden), auto = live at N=1, golden at N>1")
     args = ap.parse_args()
     if args.gen == "random":
         args.rounds = 1

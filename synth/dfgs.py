@@ -223,32 +223,42 @@ def inception_v3(batch=64, profile=PAPER_PROFILE):
 # ------------------------------------------------------------------ GNMT
 def gnmt(batch=128, chunks=18, steps_per_chunk=3, hidden=1024, vocab=32000, profile=PAPER_PROFILE):
     """GNMT-shaped: 4 encoder + 4 decoder LSTM layers × `chunks` time chunks
-    (PAPER.md:230), two embeddings, per-chunk attention and projection, a
-    chained loss.  Ops numbered time-major (chunk by chunk)."""
+    (PAPER.md:230), per-chunk attention over all encoder outputs and
+    projection, a chained loss.  Ops numbered time-major (chunk by chunk).
+
+    The embedding lookup of a chunk's tokens is part of its layer-0 LSTM op
+    (cost and parameters), which reads the chunk's token slice of the input
+    directly: a separate embedding op shared by every chunk would be a
+    18-way fan-out whose backward waits for all 18 chunks — a data input has
+    no gradient, and it kept 18 extra finish times live (W 38 → 22; DESIGN.md
+    §4).  The attention's 18-way fan-in (enc_concat) and fan-out (every
+    decoder chunk attends to all encoder outputs) is the model's, so W = 22
+    remains."""
     b = _Builder(profile, batch)
     B, H, T = batch, hidden, steps_per_chunk
     lstm_flops = 2 * B * 4 * H * (H + H) * T
     act = B * T * H
     state = 2 * B * H
-    emb_e = b.elementwise("enc_emb", B * T * chunks, act * chunks, params=vocab * H)
+    emb_flops = 2 * B * T * H          # the lookup's gather (per chunk)
     enc = [[None] * chunks for _ in range(4)]
     for t in range(chunks):
         for l in range(4):
-            ins = [emb_e if l == 0 else enc[l - 1][t]]
-            k = b.compute(f"enc{l}/t{t}", lstm_flops, act, params=(8 * H * H) if t == 0 else 0,
+            ins = [] if l == 0 else [enc[l - 1][t]]
+            k = b.compute(f"enc{l}/t{t}", lstm_flops + (emb_flops if l == 0 else 0), act,
+                          params=((8 * H * H) if t == 0 else 0) + ((vocab * H) if (t == 0 and l == 0) else 0),
                           inputs=ins)
             if t > 0:
                 b.edge(enc[l][t - 1], k, nbytes=state * b.db)
             enc[l][t] = k
     enc_cat = b.elementwise("enc_concat", act * chunks, act * chunks, inputs=[enc[3][t] for t in range(chunks)])
-    emb_d = b.elementwise("dec_emb", B * T * chunks, act * chunks, params=vocab * H)
     dec = [[None] * chunks for _ in range(4)]
     loss_prev = None
     for t in range(chunks):
         for l in range(4):
-            ins = [emb_d if l == 0 else dec[l - 1][t]]
-            k = b.compute(f"dec{l}/t{t}", lstm_flops if l == 0 else 2 * B * 4 * H * 3 * H * T, act,
-                          params=(8 * H * H) if t == 0 else 0, inputs=ins)
+            ins = [] if l == 0 else [dec[l - 1][t]]
+            k = b.compute(f"dec{l}/t{t}", (lstm_flops + emb_flops) if l == 0 else 2 * B * 4 * H * 3 * H * T, act,
+                          params=((8 * H * H) if t == 0 else 0) + ((vocab * H) if (t == 0 and l == 0) else 0),
+                          inputs=ins)
             if t > 0:
                 b.edge(dec[l][t - 1], k, nbytes=state * b.db)
             if l >= 1:
@@ -270,16 +280,20 @@ def gnmt(batch=128, chunks=18, steps_per_chunk=3, hidden=1024, vocab=32000, prof
 def biglstm(batch=128, chunks=30, steps_per_chunk=1, hidden=8192, proj=1024, emb=1024,
             sampled_softmax=8192, profile=PAPER_PROFILE):
     """BigLSTM-shaped: embedding 1024 → 2 × LSTM 8192 with 1024 projection →
-    (sampled) softmax; time-major chunks; chained loss."""
+    (sampled) softmax; time-major chunks; chained loss.
+
+    Each chunk's embedding lookup reads its own token slice of the input (a
+    source op): one input op feeding all 30 chunks would have no gradient to
+    compute yet a backward waiting on all 30 chunks, keeping 30 finish times
+    live (W 32 → 3)."""
     b = _Builder(profile, batch)
     B, H, P, T = batch, hidden, proj, steps_per_chunk
-    inp = b.elementwise("input", B * T * chunks, B * T * chunks)
     l1 = [None] * chunks
     l2 = [None] * chunks
     loss_prev = None
     lstm_flops = (2 * B * 4 * H * (emb + P) + 2 * B * H * P) * T
     for t in range(chunks):
-        e = b.elementwise(f"emb/t{t}", B * T * emb, B * T * emb, inputs=[inp],
+        e = b.elementwise(f"emb/t{t}", B * T * emb, B * T * emb, inputs=[],
                           params=(800_000 * emb) if t == 0 else 0)
         k1 = b.compute(f"lstm1/t{t}", lstm_flops, B * T * P,
                        params=(4 * H * (emb + P) + H * P) if t == 0 else 0, inputs=[e])
