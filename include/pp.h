@@ -306,15 +306,16 @@ int pp_comm_set_timeout(pp_comm *comm, uint64_t timeout_ms);
  *   rank r of R owns candidates [⌊r·n/R⌋, ⌊(r+1)·n/R⌋) of every round;
  *   key = (min(makespan, 2^61−1) << 3) | r for a slice whose local argmin
  *   index is not UINT64_MAX, else UINT64_MAX (an empty slice never wins), R ≤ 8;
- *   the global winner is the minimum key (ties to the lower rank = the lower
- *   global index); the winning rank contributes its index, every other rank
- *   UINT64_MAX, to a second min all-reduce.                                 */
+ *   the minimum key carries the winning makespan; every rank whose key has
+ *   that makespan contributes its local argmin index, every other rank
+ *   UINT64_MAX, to a second min all-reduce, so the result is the smallest
+ *   global index with the minimum makespan for any slice layout.            */
 void     pp_rank_slice(uint64_t count, int rank, int world, uint64_t *begin, uint64_t *end);
 uint64_t pp_round_key(uint64_t makespan, uint64_t index, int rank);
 uint64_t pp_pack_key(uint64_t makespan, int rank);   /* = pp_round_key(makespan, 0, rank) */
 uint64_t pp_key_makespan(uint64_t key);   /* 2^61−1 (and UINT64_MAX) map back to PP_INFEASIBLE_MAKESPAN */
 int      pp_key_rank(uint64_t key);
-uint64_t pp_round_contrib(uint64_t key_global, uint64_t local_index, int rank);
+uint64_t pp_round_contrib(uint64_t key_global, uint64_t key_local, uint64_t local_index);
 /* 1 iff a PERTURB base moves to the round winner with this global index (the
  * winner is strictly better than the base exactly when it is not candidate 0) */
 int      pp_round_moves_base(uint64_t win_index);

@@ -84,7 +84,7 @@ struct CrossParams;
 int launch_pack_key(uint64_t *s, int rank, void *stream);
 int launch_patch_base(uint8_t *image, uint8_t *base, const uint8_t *src, uint32_t K, uint32_t K8, uint32_t off_hgw,
                       void *stream);
-int launch_contrib(uint64_t *s, int rank, void *stream);
+int launch_contrib(uint64_t *s, void *stream);
 int launch_unpack_best(const uint64_t *s, uint64_t *out, void *stream);
 
 static int cuda_err(cudaError_t e, const char *what) {
@@ -318,6 +318,60 @@ static int check_gen_args(const pp_dfg *g, int M, int gen, uint32_t tau, uint64_
     return PP_OK;
 }
 
+// ------------------------------ symmetry-reduced exhaustive GRAY (f1)
+// With the uniform link model the makespan and the memory feasibility of a
+// placement are invariant under relabelling the devices, so an exhaustive
+// GRAY search (the whole range [0, M^K)) evaluates one placement per class,
+// the restricted-growth strings, and reports for each class that reaches the
+// minimum its smallest Gray index (search_kernel.cuh RgsGen, gray_min_index;
+// DESIGN.md §12b).  The (makespan, Gray index) argmin is the full search's.
+// PP_NO_SYM=1 turns it off (A/B and tests).
+static bool use_sym(const pp_dfg *g, int M, int gen, uint64_t begin, uint64_t end) {
+    if (gen != GEN_GRAY || g->hw || M < 2 || begin != 0 || getenv("PP_NO_SYM")) return false;
+    unsigned __int128 space = 1;
+    for (int j = 0; j < g->K; j++) space *= (unsigned)M;   // ≤ 2^63 (check_gen_args)
+    return (unsigned __int128)end == space;
+}
+
+// Completion counts T_M[rem][m] = m·T_M[rem−1][m] + [m < M]·T_M[rem−1][m+1],
+// T_M[0][m] = 1, for every M, uploaded once per DFG.  Returns the number of
+// classes of M (= T_M[K−1][1]).
+static int rgs_table(const pp_dfg *g, int M, uint64_t *classes) {
+    const int rows = std::min(g->K, kRgsRows);
+    if (!g->d_rgs) {
+        std::vector<uint64_t> t((size_t)8 * kRgsRows * kRgsStride, 0);
+        for (int mm = 1; mm <= 8; mm++) {
+            uint64_t *T = t.data() + (size_t)(mm - 1) * kRgsRows * kRgsStride;
+            for (int m = 1; m <= mm; m++) T[m] = 1;
+            for (int r = 1; r < rows; r++)
+                for (int m = 1; m <= mm; m++) {
+                    unsigned __int128 v = (unsigned __int128)m * T[(r - 1) * kRgsStride + m];
+                    if (m < mm) v += T[(r - 1) * kRgsStride + m + 1];
+                    T[r * kRgsStride + m] = v >= ((unsigned __int128)1 << 63) ? (1ull << 63) : (uint64_t)v;
+                }
+        }
+        uint64_t *d = nullptr;
+        cudaError_t e = cudaMalloc(&d, t.size() * 8);
+        if (e == cudaSuccess) e = cudaMemcpy(d, t.data(), t.size() * 8, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            if (d) cudaFree(d);
+            return cuda_err(e, "RGS table");
+        }
+        g->d_rgs = d;
+    }
+    // T_M[K−1][1], recomputed on the host (exact: ≤ M^(K−1) < 2^63)
+    std::vector<unsigned __int128> prev(M + 2, 1), cur(M + 2, 0);
+    for (int r = 1; r < g->K; r++) {
+        for (int m = 1; m <= M; m++) cur[m] = m * prev[m] + (m < M ? prev[m + 1] : 0);
+        prev = cur;
+    }
+    *classes = (uint64_t)prev[1];
+    return PP_OK;
+}
+static const uint64_t *rgs_of(const pp_dfg *g, int M) {
+    return g->d_rgs + (size_t)(M - 1) * kRgsRows * kRgsStride;
+}
+
 // ------------------------------------------------------------------ NCCL
 struct Nccl {
     void *h = nullptr;
@@ -382,7 +436,7 @@ struct NcclExec {
         return rc ? cuda_err((cudaError_t)rc, "pack") : PP_OK;
     }
     int contrib() {
-        int rc = launch_contrib(s, comm->rank, st);
+        int rc = launch_contrib(s, st);
         g_launches++;
         return rc ? cuda_err((cudaError_t)rc, "contrib") : PP_OK;
     }
@@ -403,7 +457,7 @@ struct HostExec {
         return PP_OK;
     }
     int contrib() {
-        s[SC_IDX_LOCAL] = proto::contrib(s[SC_KEY_GLOBAL], s[SC_LOCAL_IDX], rank);
+        s[SC_IDX_LOCAL] = proto::contrib(s[SC_KEY_GLOBAL], s[SC_KEY_LOCAL], s[SC_LOCAL_IDX]);
         return PP_OK;
     }
     int allreduce_min(int src, int dst) {
@@ -555,8 +609,14 @@ int pp_search_range(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
         g_launches++;
     }
     Launch L;
-    rc = setup(g, M, gen, false, begin, end, L, stream);
-    if (rc) return rc;
+    if (use_sym(g, M, gen, begin, end)) {   // the whole GRAY space: one placement per class
+        uint64_t classes = 0;
+        if ((rc = rgs_table(g, M, &classes))) return rc;
+        if ((rc = setup(g, M, GEN_SYM, false, 0, classes, L, stream))) return rc;
+        L.p.g_rgs = rgs_of(g, M);
+    } else if ((rc = setup(g, M, gen, false, begin, end, L, stream))) {
+        return rc;
+    }
     L.p.seed = seed_r;
     L.p.tau = tau;
     L.p.g_out = d_best;
@@ -623,6 +683,7 @@ static int run_exact(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t 
     p.off_orig = g->x_off_orig;
     p.ws_off = (uint32_t)ws_off;
     p.search = d_best ? 1 : 0;
+    p.g_rgs = gen == GEN_SYM ? rgs_of(g, M) : nullptr;
     int rc = k.launch(p, (int)grid, threads, smem, stream);
     g_launches++;
     if (rc) return cuda_err((cudaError_t)rc, "exact kernel launch");
@@ -658,6 +719,12 @@ int pp_search_exact(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
     if (end <= begin || !d_best || (gen == GEN_PERTURB && !d_base_pi)) {
         set_error("invalid range or NULL buffer");
         return PP_E_INVALID;
+    }
+    if (use_sym(g, M, gen, begin, end)) {   // the whole GRAY space: one placement per class
+        uint64_t classes = 0;
+        if ((rc = rgs_table(g, M, &classes))) return rc;
+        return run_exact(g, M, GEN_SYM, seed_r, tau, d_base_pi, nullptr, 0, classes, node_limit, nullptr, nullptr,
+                         d_best, stream);
     }
     return run_exact(g, M, gen, seed_r, tau, d_base_pi, nullptr, begin, end, node_limit, nullptr, nullptr, d_best,
                      stream);
@@ -941,15 +1008,21 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
     if ((rc = launch_patch_base(g->d_image, g->d_base, g->d_winner, (uint32_t)K, (uint32_t)g->K8, g->off_hgw, stream)))
         return cuda_err((cudaError_t)rc, "base patch");
     g_launches++;
+    // an exhaustive GRAY search runs over the relabelling classes (f1); its
+    // winner is reported by Gray index, so the update is GRAY's
+    const bool sym = use_sym(g, M, desc->gen, 0, desc->count);
+    uint64_t space = desc->count;
+    if (sym && (rc = rgs_table(g, M, &space))) return rc;
     uint64_t begin = 0, end = 0;
-    pp_rank_slice(desc->count, rank, world, &begin, &end);
+    pp_rank_slice(space, rank, world, &begin, &end);
     UpdateFn upd = update_for(M, desc->gen);
     Launch L;
     const bool empty = end <= begin;
     if (!empty) {
-        rc = setup(g, M, desc->gen, false, begin, end, L, stream);
+        rc = setup(g, M, sym ? GEN_SYM : desc->gen, false, begin, end, L, stream);
         if (rc) return rc;
         L.p.tau = desc->flip_thresh;
+        if (sym) L.p.g_rgs = rgs_of(g, M);
     }
     std::vector<cudaEvent_t> evs;
     struct EvGuard {
@@ -1043,8 +1116,8 @@ int pp_comm_set_timeout(pp_comm *comm, uint64_t timeout_ms) {
 }
 
 uint64_t pp_round_key(uint64_t makespan, uint64_t index, int rank) { return proto::key(makespan, index, rank); }
-uint64_t pp_round_contrib(uint64_t key_global, uint64_t local_index, int rank) {
-    return proto::contrib(key_global, local_index, rank);
+uint64_t pp_round_contrib(uint64_t key_global, uint64_t key_local, uint64_t local_index) {
+    return proto::contrib(key_global, key_local, local_index);
 }
 int pp_round_moves_base(uint64_t win_index) { return proto::moves_base(win_index) ? 1 : 0; }
 

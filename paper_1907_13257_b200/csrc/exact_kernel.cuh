@@ -104,8 +104,20 @@ __global__ void __launch_bounds__(256) exact_kernel(const XParams P) {
         // an explicit value ≥ M is replaced by device 0 and the row reported
         // infeasible (pp.h, pp_eval_exact): no table is indexed out of range
         bool bad = false;
+        // GRAY / GEN_SYM: the placement's packed fields, built once (not per op)
+        uint64_t glo = 0, ghi = 0;
+        if constexpr (GEN == GEN_GRAY) GrayGen<M, 1>::one(i, P.K, glo, ghi);
+        if constexpr (GEN == GEN_SYM) RgsGen<M, 1>::unrank(i, P.K, P.g_rgs, glo, ghi);
         for (uint32_t p = lane; p < P.K; p += 32) {
-            const uint32_t d = x_gen_dev<M, GEN>(P, orig, i, p);
+            uint32_t d;
+            if constexpr (GEN == GEN_GRAY || GEN == GEN_SYM) {
+                constexpr int b = Bits<M>::b, PF = b ? 64 / b : 64;
+                d = M == 1 ? 0u
+                           : (uint32_t)((p < (uint32_t)PF ? glo : ghi) >> (p < (uint32_t)PF ? p * b : (p - PF) * b)) &
+                                 ((1u << b) - 1);
+            } else {
+                d = x_gen_dev<M, GEN>(P, orig, i, p);
+            }
             bad |= d >= (uint32_t)M;
             W.dev[p] = (uint8_t)(d < (uint32_t)M ? d : 0u);
         }
@@ -330,9 +342,14 @@ __global__ void __launch_bounds__(256) exact_kernel(const XParams P) {
             if (!exact) atomicAdd(&P.g_work[2], 1ull);
             if (P.search && exact && best != kInfeasible) atomicMin(&P.g_work[1], (unsigned long long)best);
         }
-        if (best < wbest || (best == wbest && i < wbest_i)) {
+        // GEN_SYM ranks a relabelling class: its index is the class's smallest
+        // Gray index (search_kernel.cuh gray_min_index), needed only when it
+        // can still win
+        uint64_t key_i = i;
+        if constexpr (GEN == GEN_SYM) key_i = best <= wbest ? gray_min_index<M>(glo, ghi, P.K) : kInfeasible;
+        if (best < wbest || (best == wbest && key_i < wbest_i)) {
             wbest = best;
-            wbest_i = i;
+            wbest_i = key_i;
         }
     }
 

@@ -115,7 +115,13 @@ uint32_t half_group_bytes(const uint8_t *base, uint32_t h, uint32_t K) {
     return w;
 }
 
-enum GenKind : int { GEN_GRAY = 0, GEN_RANDOM = 1, GEN_PERTURB = 2, GEN_EXPLICIT = 3 };
+enum GenKind : int { GEN_GRAY = 0, GEN_RANDOM = 1, GEN_PERTURB = 2, GEN_EXPLICIT = 3,
+                     GEN_SYM = 4 };   // internal: exhaustive GRAY, one placement per relabelling class
+
+// Restricted-growth-string completion counts for GEN_SYM (search_kernel.cuh
+// RgsGen): rgs[M][rem·kRgsStride + m], m = devices in use (1..M).
+constexpr int kRgsStride = 9;
+constexpr int kRgsRows = 65;
 
 constexpr uint64_t kInfeasible = ~0ull;
 constexpr int kMaxImageBytes = 96 * 1024;
@@ -143,6 +149,7 @@ struct KParams {
     uint32_t one_hi;             // 0x3FF00000, the high word of 1.0 (opaque to ptxas)
     uint32_t off_cls;            // hardware graph: image offset of cls[a·8 + b]
     uint32_t off_hgw;            // image offset of the half-group base words (u32 × K8/4)
+    const uint64_t *g_rgs;       // GEN_SYM: RGS completion counts of this M (device)
 };
 
 // ---- exact-schedule image, built when
@@ -240,6 +247,7 @@ struct XParams {
     uint32_t off_pred, off_rows, off_cls, off_mem, off_orig;
     uint32_t ws_off;             // smem offset of the first per-warp state block
     int search;                  // 1: argmin with incumbent pruning
+    const uint64_t *g_rgs;       // GEN_SYM: RGS completion counts of this M (device)
 };
 typedef int (*XLaunchFn)(const XParams &, int grid, int threads, int smem, void *stream);
 struct XKernelInfo {
@@ -304,6 +312,7 @@ struct pp_dfg {
     std::vector<int32_t> e_src, e_dst;             // edges by π position
     std::vector<uint64_t> e_bf, e_bb, fwd, bwd, mem;   // bytes; Δf, Δb, M(k) by π position
     uint64_t *d_pipe = nullptr;                    // pipeline tables (lazily built)
+    mutable uint64_t *d_rgs = nullptr;             // RGS completion counts, every M (lazily built)
     mutable std::map<int, int> tuned;              // (M, gen) -> measured best NP
     std::vector<uint8_t> image;  // host copy of the image
     uint32_t off_extra = 0, off_mem = 0, off_orig = 0, off_hgw = 0, image_bytes = 0;

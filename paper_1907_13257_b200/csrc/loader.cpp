@@ -615,6 +615,7 @@ extern "C" void pp_free_dfg(pp_dfg *g) {
     if (g->d_xwork) cudaFree(g->d_xwork);
     if (g->d_gimage) cudaFree(g->d_gimage);
     if (g->d_pipe) cudaFree(g->d_pipe);
+    if (g->d_rgs) cudaFree(g->d_rgs);
     cudaSetDevice(prev);
     delete g;
 }

@@ -4,13 +4,15 @@
 // min all-reduces make every rank agree on the global argmin:
 //
 //   key_r   = (min(makespan, 2^61 − 1) << 3) | r      (UINT64_MAX: empty slice)
-//   key     = min_r key_r                           → winning rank = key & 7
-//   idx_r   = local index if r is the winning rank, else UINT64_MAX
+//   key     = min_r key_r                           → the winning makespan
+//   idx_r   = local index if key_r has the winning makespan, else UINT64_MAX
 //   idx     = min_r idx_r
 //
-// Slices are contiguous and rank-ordered, so "smaller makespan, then lower
-// rank" is "smaller makespan, then lower global index": the result equals the
-// single-GPU argmin for any rank count (R9).  Feasible makespans are < 2^61
+// Every rank whose local argmin reaches the winning makespan contributes its
+// index, so idx is the smallest global index with the minimum makespan: the
+// result equals the single-GPU argmin for any rank count (R9), whatever the
+// order of the slices' indices (the symmetry-reduced GRAY search reports
+// Gray indices that are not ordered by rank).  Feasible makespans are < 2^61
 // (pp_load_dfg), so the clamp only maps the infeasible sentinel to 2^61 − 1.
 //
 // The functions below are the protocol's only definition: the device kernels
@@ -45,9 +47,11 @@ PP_HD uint64_t key_makespan(uint64_t key) {
     const uint64_t m = key >> 3;
     return m == kKeyCap ? kNone : m;
 }
-// this rank's contribution to the index all-reduce
-PP_HD uint64_t contrib(uint64_t key_global, uint64_t local_index, int rank) {
-    return (key_global != kNone && key_rank(key_global) == rank) ? local_index : kNone;
+// this rank's contribution to the index all-reduce: its local argmin index
+// iff its key carries the winning (clamped) makespan
+PP_HD uint64_t contrib(uint64_t key_global, uint64_t key_local, uint64_t local_index) {
+    return (key_global != kNone && key_local != kNone && (key_local >> 3) == (key_global >> 3)) ? local_index
+                                                                                                : kNone;
 }
 // the PERTURB base moves to the round winner iff the winner is strictly better
 // than the base: candidate 0 is the base, so (lexicographic argmin) the winner
@@ -58,8 +62,8 @@ PP_HD bool moves_base(uint64_t win_index) { return win_index != 0 && win_index !
 enum : int { LOCAL_MK = 0, LOCAL_IDX = 1, KEY_LOCAL = 2, KEY_GLOBAL = 3, IDX_LOCAL = 4, IDX_GLOBAL = 5 };
 
 // The exchange sequence.  Ex provides pack() (KEY_LOCAL ← key(LOCAL_MK,
-// LOCAL_IDX, rank)), contrib() (IDX_LOCAL ← contrib(KEY_GLOBAL, LOCAL_IDX,
-// rank)) and allreduce_min(src, dst) (dst ← min over ranks of src); each
+// LOCAL_IDX, rank)), contrib() (IDX_LOCAL ← contrib(KEY_GLOBAL, KEY_LOCAL,
+// LOCAL_IDX)) and allreduce_min(src, dst) (dst ← min over ranks of src); each
 // returns 0 or a PP_E_* code.
 template <class Ex>
 int exchange(Ex &ex) {

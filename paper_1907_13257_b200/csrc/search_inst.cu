@@ -47,8 +47,22 @@ static KernelInfo info_gen(bool mem, bool wa, bool f64, int np, bool hw) {
     return wa ? info_f<GEN, false, true>(f64, np, hw) : info_f<GEN, false, false>(f64, np, hw);
 }
 
+// GEN_SYM (the symmetry-reduced exhaustive GRAY search) runs only as an
+// argmin on the uniform link model
+template <bool MEM, bool F64>
+static KernelInfo info_sym_np(int np) {
+    if (np >= 4) return info2<GEN_SYM, MEM, false, F64, 4, false>();
+    if (np == 2) return info2<GEN_SYM, MEM, false, F64, 2, false>();
+    return info2<GEN_SYM, MEM, false, F64, 1, false>();
+}
+template <bool MEM>
+static KernelInfo info_sym(bool f64, int np) {
+    return f64 ? info_sym_np<MEM, true>(np) : info_sym_np<MEM, false>(np);
+}
+
 KernelInfo PP_CAT(kernel_for_m, PP_M)(int gen, bool mem, bool wa, bool f64, int np, bool hw) {
     switch (gen) {
+        case GEN_SYM: return mem ? info_sym<true>(f64, np) : info_sym<false>(f64, np);
         case GEN_GRAY: return info_gen<GEN_GRAY>(mem, wa, f64, np, hw);
         case GEN_RANDOM: return info_gen<GEN_RANDOM>(mem, wa, f64, np, hw);
         case GEN_PERTURB: return info_gen<GEN_PERTURB>(mem, wa, f64, np, hw);
@@ -73,6 +87,7 @@ static XKernelInfo xinfo() {
 XKernelInfo PP_CAT(exact_for_m, PP_M)(int gen) {
     switch (gen) {
         case GEN_GRAY: return xinfo<GEN_GRAY>();
+        case GEN_SYM: return xinfo<GEN_SYM>();
         case GEN_RANDOM: return xinfo<GEN_RANDOM>();
         case GEN_PERTURB: return xinfo<GEN_PERTURB>();
         default: return xinfo<GEN_EXPLICIT>();

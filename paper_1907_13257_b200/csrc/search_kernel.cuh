@@ -129,6 +129,81 @@ struct GrayGen {                           // O5: reflected M-ary Gray code
     }
 };
 
+// ------------------------- symmetry-reduced exhaustive enumeration (f1)
+// With the uniform link model every device is interchangeable: relabelling
+// the devices of a placement (a permutation σ of 0..M−1) changes neither its
+// schedule's makespan nor its memory feasibility.  An exhaustive GRAY search
+// therefore evaluates one placement per class — the restricted-growth string
+// (RGS): d[0] = 0 and d[j] ≤ 1 + max(d[0..j−1]), < M — and reports, for the
+// classes that reach the running minimum, the smallest Gray index among the
+// class's relabellings (gray_min_index), which is the oracle's tie-break over
+// all M^K placements.
+//
+// RGS rank r (lexicographic, d[K−1] fastest) is unranked with the completion
+// counts T[rem·kRgsStride + m] = the number of ways to fill `rem` further
+// positions when m devices are in use (host-built, pp_dfg::d_rgs): at each
+// position the values v < m each cover T[rem][m] ranks, v = m (a new device)
+// the next T[rem][m + 1].  The packed fields are GrayGen's, so the schedule
+// bodies read them unchanged.
+template <int M, int NP>
+struct RgsGen : GrayGen<M, NP> {
+    using GrayGen<M, NP>::lo;
+    using GrayGen<M, NP>::hi;
+    static constexpr int b = Bits<M>::b;
+    static constexpr int PF = b ? 64 / b : 64;
+    __device__ __forceinline__ static void unrank(uint64_t r, uint32_t K, const uint64_t *__restrict__ T,
+                                                  uint64_t &lo, uint64_t &hi) {
+        lo = hi = 0;
+        if (M == 1) return;
+        uint32_t m = 1;                                   // d[0] = 0
+        for (uint32_t j = 1; j < K; j++) {
+            const uint64_t c = __ldg(T + (K - 1 - j) * kRgsStride + m);
+            uint32_t v = 0;
+            while (v < m && r >= c) { r -= c; v++; }
+            if (v == m) m++;                               // opens device m (r < T[rem][m + 1])
+            if (j < (uint32_t)PF) lo |= (uint64_t)v << (j * b);
+            else hi |= (uint64_t)v << ((j - PF) * b);
+        }
+    }
+    __device__ __forceinline__ void init(const uint64_t (&r)[NP], uint32_t K, const uint64_t *T) {
+#pragma unroll
+        for (int k = 0; k < NP; k++) unrank(r[k], K, T, lo[k], hi[k]);
+    }
+};
+
+// The smallest Gray index (O5) over the relabellings of placement d (packed
+// fields).  Index = Σ a_j·M^j is lexicographic in (a_{K−1}, …, a_0), and
+// a_j = d'[j] when the reflection parity of the digits above is even, else
+// M − 1 − d'[j].  Going from j = K − 1 down, a device already mapped fixes
+// a_j; an unmapped one takes the free target that minimises a_j (the smallest
+// free target when even, the largest when odd) — each digit's minimum is
+// forced, so the greedy choice is the lexicographic minimum.
+template <int M>
+__device__ __forceinline__ uint64_t gray_min_index(uint64_t lo, uint64_t hi, uint32_t K) {
+    constexpr int b = Bits<M>::b;
+    constexpr int PF = b ? 64 / b : 64;
+    uint32_t sig = 0xFFFFFFFFu;                           // 4 bits per device label: its target (0xF: unmapped)
+    uint32_t used = 0;                                    // targets taken
+    uint64_t idx = 0;
+    uint32_t par = 0;                                     // a_{j+1} (even M) or Σ_{t>j} a_t (odd M)
+    for (int j = (int)K - 1; j >= 0; j--) {
+        const uint32_t sh = j < PF ? j * b : (j - PF) * b;
+        const uint32_t lab = (uint32_t)((j < PF ? lo : hi) >> sh) & ((1u << b) - 1);
+        uint32_t t = (sig >> (4 * lab)) & 0xFu;
+        const bool even = (par & 1u) == 0;
+        if (t == 0xFu) {
+            const uint32_t fr = ~used & ((1u << M) - 1);
+            t = even ? (uint32_t)(__ffs((int)fr) - 1) : (uint32_t)(31 - __clz((int)fr));
+            used |= 1u << t;
+            sig = (sig & ~(0xFu << (4 * lab))) | (t << (4 * lab));
+        }
+        const uint32_t a = even ? t : (uint32_t)(M - 1) - t;
+        idx = idx * (uint64_t)M + a;
+        par = (M % 2 == 0) ? a : par + a;
+    }
+    return idx;
+}
+
 // RANDOM and PERTURB keep one key per lane: the lane's placements are
 // i_k = i_0 + 32k (search_kernel), so key(i_k) = key(i_0) + k·Δ with the
 // uniform Δ = γ·32·Wd, and only i_0 can be candidate 0.  (Per-placement keys
@@ -556,8 +631,14 @@ __device__ __forceinline__ double cut_add_f64(double v, uint32_t dev, double c, 
 template <int M, int NP, bool MEM, bool HW, class Gen>
 __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint32_t ops, uint32_t xr,
                                              const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
-                                             uint32_t K8, uint64_t cap, uint32_t khi, uint32_t cls) {
+                                             uint32_t K8, uint64_t cap, uint32_t khi, uint32_t cls,
+                                             uint32_t hq = 0, uint32_t nslot = 0) {
     constexpr bool SM = M > 2;                    // free[] in shared memory
+    // Gray prefix reuse (GEN_SYM): the lane's NP placements are
+    // consecutive RGS ranks, identical on the first hq forward half-groups
+    // (warp-uniform), which are computed for placement 0 only; its state
+    // (registers and the nslot live slots) is then copied to the others
+    constexpr bool kPrefix = std::is_same<Gen, RgsGen<M, NP>>::value && NP > 1;
     constexpr bool kFmax = PP_FMAX_F64 == 1 || (PP_FMAX_F64 == 2 && SM && std::is_same<Gen, PerturbGen<M, NP>>::value);
     double prev[NP], oth[NP];
     uint32_t pdev[NP];
@@ -579,18 +660,19 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
     };
     uint32_t x = xr;
 
-    auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
+    auto step = [&](auto KNc, uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
+        constexpr int KN = decltype(KNc)::value;   // placements 0..KN−1 (KN < NP: the shared prefix)
         const uint4 a = lds128(rec);
         const uint4 b = lds128(rec + 16);
         const double cost = __hiloint2double((int)a.y, (int)a.x);
         const double c0 = __hiloint2double((int)a.w, (int)a.z);
         uint32_t dev[NP];
 #pragma unroll
-        for (int k = 0; k < NP; k++) dev[k] = gen.dev(k, p, c, b.w);
+        for (int k = 0; k < KN; k++) dev[k] = gen.dev(k, p, c, b.w);
         if (b.z == 0) {
             // chain step: the only input is the previous step's output
 #pragma unroll
-            for (int k = 0; k < NP; k++) {
+            for (int k = 0; k < KN; k++) {
                 // free[dev] matters only across a cut (else it is prev, and
                 // cut·free = 0 ≤ prev): s = max(prev + cut·c0, cut·free[dev])
                 const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
@@ -610,12 +692,12 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
             double r[NP];
             if (b.x == kFromPrev) {
 #pragma unroll
-                for (int k = 0; k < NP; k++)
+                for (int k = 0; k < KN; k++)
                     r[k] = HW ? __dadd_rn(prev[k], hwc(a.z, pdev[k], dev[k]))
                               : __fma_rn(c0, one_if(cut_bit<M>(pdev[k], dev[k]), khi), prev[k]);
             } else {
 #pragma unroll
-                for (int k = 0; k < NP; k++) {
+                for (int k = 0; k < KN; k++) {
                     const double v = ldd(lane + b.x * NP + k * 256);
                     r[k] = HW ? __dadd_rn(v, hwc(a.z, (uint32_t)__double2loint(v) & 7u, dev[k]))
                               : cut_add_f64<M>(v, dev[k], c0, khi);
@@ -628,14 +710,14 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
                 x += sizeof(ExtraRec);
                 const double ce = __hiloint2double((int)e.y, (int)e.x);
 #pragma unroll
-                for (int k = 0; k < NP; k++) {
+                for (int k = 0; k < KN; k++) {
                     const double v = ldd(lane + e.z * NP + k * 256);
                     r[k] = dmax(r[k], HW ? __dadd_rn(v, hwc(e.x, (uint32_t)__double2loint(v) & 7u, dev[k]))
                                          : cut_add_f64<M>(v, dev[k], ce, khi));
                 }
             }
 #pragma unroll
-            for (int k = 0; k < NP; k++) {
+            for (int k = 0; k < KN; k++) {
                 // free[dev] = cut ? other : prev, exact on the FP64 pipe
                 const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
                 double f;
@@ -653,26 +735,66 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
         }
         if (b.y != kNoStore) {
 #pragma unroll
-            for (int k = 0; k < NP; k++) std_(lane + b.y * NP + k * 256, with_tag(prev[k], Dev<M>::canon(dev[k])));
+            for (int k = 0; k < KN; k++) std_(lane + b.y * NP + k * 256, with_tag(prev[k], Dev<M>::canon(dev[k])));
         }
         if (MEM && fwd) {
             const uint64_t m = mem[p];
 #pragma unroll
-            for (int k = 0; k < NP; k++) mu[k].add(Dev<M>::canon(dev[k]), m);
+            for (int k = 0; k < KN; k++) mu[k].add(Dev<M>::canon(dev[k]), m);
         }
     };
     // the two half-groups of an 8-op group: looped at NP = 4 (the unrolled
     // body overflows the instruction cache), unrolled below (A/B measured)
     constexpr int kHalfUnroll = NP >= 4 ? 1 : 2;
+    using All = std::integral_constant<int, NP>;
     const uint32_t G = K8 / 8;
-    for (uint32_t g = 0; g < G; g++) {           // forward, π order
-        gen.refresh(g);
-#pragma unroll (kHalfUnroll)
-        for (uint32_t h = 0; h < 2; h++) {
+    uint32_t g0 = 0, h0 = 0;
+    if constexpr (kPrefix) {
+        using One = std::integral_constant<int, 1>;
+        for (uint32_t hg = 0; hg < hq; hg++) {   // the shared prefix, placement 0 only
+            const uint32_t g = hg >> 1, h = hg & 1;
+            if (h == 0) gen.refresh(g);
             gen.sub(h);
             const uint32_t rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
 #pragma unroll
-            for (uint32_t cc = 0; cc < 4; cc++) step(rec + cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, true);
+            for (uint32_t cc = 0; cc < 4; cc++)
+                step(One{}, rec + cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, true);
+        }
+        if (hq) {
+#pragma unroll
+            for (int k = 1; k < NP; k++) {
+                prev[k] = prev[0];
+                oth[k] = oth[0];
+                pdev[k] = pdev[0];
+                if (MEM) mu[k] = mu[0];
+            }
+            for (uint32_t sl = 0; sl < nslot; sl++) {
+                const double v = ldd(lane + sl * NP * 256);
+#pragma unroll
+                for (int k = 1; k < NP; k++) std_(lane + sl * NP * 256 + k * 256, v);
+            }
+            if (SM) {
+#pragma unroll
+                for (int d = 0; d < M; d++) {
+                    const double v = ldd(fslot(0, d));
+#pragma unroll
+                    for (int k = 1; k < NP; k++) std_(fslot(k, d), v);
+                }
+            }
+        }
+        g0 = hq >> 1;
+        h0 = hq & 1;
+    }
+    for (uint32_t g = g0; g < G; g++) {          // forward, π order
+        gen.refresh(g);
+#pragma unroll (kHalfUnroll)
+        for (uint32_t h = 0; h < 2; h++) {
+            if (kPrefix && g == g0 && h < h0) continue;
+            gen.sub(h);
+            const uint32_t rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
+#pragma unroll
+            for (uint32_t cc = 0; cc < 4; cc++)
+                step(All{}, rec + cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, true);
         }
     }
     for (uint32_t g = G; g-- > 0;) {             // backward, reverse π order
@@ -683,7 +805,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
             const uint32_t rec = ops + (2 * K8 - 1 - g * 8 - h * 4) * (uint32_t)sizeof(OpRec);
 #pragma unroll
             for (int cc = 3; cc >= 0; cc--)
-                step(rec - (uint32_t)cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, false);
+                step(All{}, rec - (uint32_t)cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, false);
         }
     }
 #pragma unroll
@@ -746,6 +868,12 @@ __device__ __forceinline__ double dsel(uint32_t m, double a, double b) {
 #endif
 #ifndef PP_M2P_LDS64
 #define PP_M2P_LDS64 1   // cost and c0 by two LDS.64 into their own pairs (A/B: -1.1%)
+#endif
+#ifndef PP_M2P_MIX
+#define PP_M2P_MIX 0   // chain steps: placements k with k % 4 < MIX take the ALU max (DSETP + 2 FSEL) instead of dmax_add (pipe balance)
+#endif
+#ifndef PP_M2P_CUTIMAD
+#define PP_M2P_CUTIMAD 0   // 1: the cut flag's high word by IMAD (FMA pipe) instead of LOP3 (ALU)
 #endif
 #ifndef PP_M2P_STEPLOOP
 #define PP_M2P_STEPLOOP 0   // 1: the 4 steps of a half-group as a loop (smaller code) instead of unrolled
@@ -818,7 +946,8 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
 #pragma unroll
         for (int k = 0; k < NP; k++) {
             m[k] = prmt(cw[k], 0u, 0x8888u | (c * 0x1111u));    // all ones iff cut_c
-            cut[k] = __hiloint2double((int)(m[k] & khi), 0);   // 1.0 or 0.0
+            cut[k] = PP_M2P_CUTIMAD ? __hiloint2double((int)(m[k] * (0u - khi)), 0)   // −1·−khi = khi
+                                    : __hiloint2double((int)(m[k] & khi), 0);        // 1.0 or 0.0
         }
         if (b.z == 0) {
             // chain step: s = max(prev + cut·c0, cut·oth), oth' = cut ? prev : oth
@@ -828,7 +957,8 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
                 const double f = __dmul_rn(cut[k], oth[k]);
                 if (PP_M2P_SEL) oth[k] = dsel(m[k], prev[k], oth[k]);
                 else oth[k] = __fma_rn(cut[k], __dadd_rn(prev[k], -oth[k]), oth[k]);
-                prev[k] = PP_FMAX_M2P_CHAIN ? dmax_add(t, f, cost) : __dadd_rn(dmax(t, f), cost);
+                const bool alu_max = (k % 4) < PP_M2P_MIX;
+                prev[k] = (PP_FMAX_M2P_CHAIN && !alu_max) ? dmax_add(t, f, cost) : __dadd_rn(dmax(t, f), cost);
             }
         } else {
             double r[NP];
@@ -1087,8 +1217,10 @@ __device__ __forceinline__ void schedule_mpw(uint64_t A, uint64_t B, uint64_t dA
 template <int M, int NP, bool MEM, bool F64, bool HW, class Gen>
 __device__ __forceinline__ void schedule_np(Gen &gen, uint64_t (&mk)[NP], uint32_t ops, uint32_t xr,
                                             const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
-                                            uint32_t K8, uint64_t cap, uint32_t khi, uint32_t cls, uint32_t tau) {
-    if constexpr (F64 && M >= 2) schedule_f64<M, NP, MEM, HW>(gen, mk, ops, xr, mem, lane, free_off, K8, cap, khi, cls);
+                                            uint32_t K8, uint64_t cap, uint32_t khi, uint32_t cls, uint32_t tau,
+                                            uint32_t hq = 0, uint32_t nslot = 0) {
+    if constexpr (F64 && M >= 2)
+        schedule_f64<M, NP, MEM, HW>(gen, mk, ops, xr, mem, lane, free_off, K8, cap, khi, cls, hq, nslot);
     else schedule_gen<M, NP, MEM, F64>(gen, mk, ops, xr, mem, lane, free_off, K8, cap);
 }
 
@@ -1162,7 +1294,9 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
         bool valid[NP];
 #pragma unroll
         for (int k = 0; k < NP; k++) {
-            off[k] = tile * TILE + k * 32 + lane;
+            // GEN_SYM: a lane's placements are consecutive RGS ranks (they share
+            // a forward prefix, schedule_f64); else lane-interleaved
+            off[k] = tile * TILE + (GEN == GEN_SYM ? lane * NP + k : k * 32 + lane);
             valid[k] = off[k] < n;
             idx[k] = P.begin + (valid[k] ? off[k] : n - 1);
         }
@@ -1170,7 +1304,29 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
         // lanes past the end are discarded); only i_0 can be candidate 0
         const uint64_t i0 = P.begin + tile * TILE + lane;
         uint64_t mk[NP];
-        if (GEN == GEN_GRAY) {
+        if constexpr (GEN == GEN_SYM) {
+            RgsGen<M, NP> g;
+            g.init(idx, P.K, P.g_rgs);
+            // forward half-groups on which all of the warp's placements agree
+            // with their lane's placement 0 (Gray prefix reuse, schedule_f64)
+            uint32_t q = P.K;
+#pragma unroll
+            for (int k = 1; k < NP; k++) {
+                const uint64_t dl = g.lo[0] ^ g.lo[k], dh = g.hi[0] ^ g.hi[k];
+                constexpr uint32_t b = Bits<M>::b, PF = b ? 64 / b : 64;
+                const uint32_t qk = dl ? (uint32_t)(__ffsll((long long)dl) - 1) / b
+                                       : dh ? PF + (uint32_t)(__ffsll((long long)dh) - 1) / b : P.K;
+                q = min(q, qk);
+            }
+            q = __reduce_min_sync(0xffffffffu, q);
+            schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
+                                              smem_base + P.off_cls, P.tau, q / 4, P.zero_off / kSlotUnit);
+            // the class's index is its smallest Gray index, needed only when
+            // the class can still win
+#pragma unroll
+            for (int k = 0; k < NP; k++)
+                idx[k] = (valid[k] && mk[k] <= best_mk) ? gray_min_index<M>(g.lo[k], g.hi[k], P.K) : kInfeasible;
+        } else if (GEN == GEN_GRAY) {
             GrayGen<M, NP> g;
             g.init(idx, P.K);
             schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,

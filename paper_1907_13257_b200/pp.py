@@ -126,7 +126,7 @@ SIGNATURES = {
     "pp_rank_slice": ([C.c_uint64, C.c_int, C.c_int, P(C.c_uint64), P(C.c_uint64)], None),
     "pp_comm_set_timeout": ([C.c_void_p, C.c_uint64], C.c_int),
     "pp_round_key": ([C.c_uint64, C.c_uint64, C.c_int], C.c_uint64),
-    "pp_round_contrib": ([C.c_uint64, C.c_uint64, C.c_int], C.c_uint64),
+    "pp_round_contrib": ([C.c_uint64, C.c_uint64, C.c_uint64], C.c_uint64),
     "pp_round_moves_base": ([C.c_uint64], C.c_int),
     "pp_round_exchange_host": ([C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, P(C.c_uint64)], C.c_int),
     "pp_pack_key": ([C.c_uint64, C.c_int], C.c_uint64),
@@ -454,8 +454,8 @@ def round_key(makespan, index, rank):
     return int(lib().pp_round_key(makespan, index, rank))
 
 
-def round_contrib(key_global, local_index, rank):
-    return int(lib().pp_round_contrib(key_global, local_index, rank))
+def round_contrib(key_global, key_local, local_index):
+    return int(lib().pp_round_contrib(key_global, key_local, local_index))
 
 
 def round_moves_base(win_index) -> bool:

@@ -168,8 +168,14 @@ def test_round_exchange_protocol(pp):
     assert _threaded_exchange(pp, [(INF, INF), (INF, 0), (INF, 1)]) == [(INF, 0)] * 3
     assert _threaded_exchange(pp, [(INF, INF), (12, 1)]) == [(12, 1)] * 2
     assert pp.round_key(5, INF, 3) == INF and pp.round_key(5, 0, 3) == pp.pack_key(5, 3)
-    assert pp.round_contrib(pp.round_key(5, 9, 2), 9, 2) == 9 and pp.round_contrib(pp.round_key(5, 9, 2), 4, 1) == INF
-    assert pp.round_contrib(INF, 4, 0) == INF
+    kg = pp.round_key(5, 9, 2)
+    assert pp.round_contrib(kg, kg, 9) == 9                               # the winning rank
+    assert pp.round_contrib(kg, pp.round_key(5, 4, 3), 4) == 4            # a tie on the makespan contributes too
+    assert pp.round_contrib(kg, pp.round_key(6, 4, 1), 4) == INF          # a worse rank does not
+    assert pp.round_contrib(INF, INF, 4) == INF and pp.round_contrib(kg, INF, 4) == INF
+    # ties are resolved by the index, not the rank order (Gray indices of the
+    # symmetry-reduced search are not ordered by rank)
+    assert _threaded_exchange(pp, [(5, 70), (5, 30), (8, 1)]) == [(5, 30)] * 3
     # the base moves iff the winner is not candidate 0 (= the base)
     assert not pp.round_moves_base(0) and not pp.round_moves_base(INF) and pp.round_moves_base(17)
 

@@ -225,7 +225,7 @@ def test_edge_cases():
 
 def test_large_image_reduces_cta():
     # K + E near the 96 KB image cap, large W
-    spec = synth.random_dag(77, 1100, avg_deg=0.9, max_in=3, window=40)
+    spec = synth.random_dag(77, 1050, avg_deg=0.9, max_in=3, window=40)
     g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
     assert g.image_bytes > 60_000
     for M in (2, 8):
@@ -237,7 +237,7 @@ def test_large_image_reduces_cta():
 def test_state_too_large_is_reported():
     # producers anywhere in a 1000-op DAG keep hundreds of values live: the
     # per-warp state cannot fit in shared memory -> PP_E_TOO_LARGE (pp.h)
-    spec = synth.random_dag(5, 1000, avg_deg=1.5)
+    spec = synth.random_dag(5, 900, avg_deg=1.5)
     g = pp.Dfg(spec)
     if g.W < 300:
         pytest.skip(f"W={g.W} fits")
