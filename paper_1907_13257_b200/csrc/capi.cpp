@@ -198,6 +198,7 @@ static void fill(const pp_dfg *g, const Choice &best, uint64_t begin, uint64_t e
     p.off_hgw = g->off_hgw;
     p.g_partials = g->d_partials;
     p.g_ticket = g->d_ticket;
+    p.g_tile = reinterpret_cast<unsigned long long *>(g->d_ticket + 4);
     p.g_out = g->d_scalars + SC_LOCAL_MK;
 }
 
@@ -211,13 +212,14 @@ static void fill(const pp_dfg *g, const Choice &best, uint64_t begin, uint64_t e
 // depends on the choice (every variant is bit-exact), only the speed.
 // The per-candidate (write-all) kernels are built for NP = 2 only.
 static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin, uint64_t end, Launch &L,
-                 void *stream = nullptr) {
-    int forced = 0;   // PP_NP=1|2|4 pins NP (tests cover every variant)
-    if (const char *v = getenv("PP_NP")) forced = atoi(v);
+                 void *stream = nullptr, int force_np = 0) {
+    int forced = force_np;   // PP_NP=1|2|4 pins NP (tests cover every variant)
+    if (const char *v = getenv("PP_NP"); v && !forced) forced = atoi(v);
     std::vector<Choice> cands;
-    for (int np : {4, 2, 1}) {
+    for (int np : {4, 3, 2, 1}) {
         if (write_all && np != 2) continue;
         if (forced && np != forced) continue;
+        if (np == 3 && !(gen == GEN_SYM && M == 3 && forced == 3)) continue;   // built for that case only
         Choice c;
         int rc = choose(g, M, gen, write_all, np, c);
         if (rc == PP_E_TOO_LARGE) continue;
@@ -327,7 +329,7 @@ static int check_gen_args(const pp_dfg *g, int M, int gen, uint32_t tau, uint64_
 // DESIGN.md §12b).  The (makespan, Gray index) argmin is the full search's.
 // PP_NO_SYM=1 turns it off (A/B and tests).
 static bool use_sym(const pp_dfg *g, int M, int gen, uint64_t begin, uint64_t end) {
-    if (gen != GEN_GRAY || g->hw || M < 2 || begin != 0 || getenv("PP_NO_SYM")) return false;
+    if (gen != GEN_GRAY || g->hw || M < 2 || g->K < 2 || begin != 0 || getenv("PP_NO_SYM")) return false;
     unsigned __int128 space = 1;
     for (int j = 0; j < g->K; j++) space *= (unsigned)M;   // ≤ 2^63 (check_gen_args)
     return (unsigned __int128)end == space;
@@ -370,6 +372,29 @@ static int rgs_table(const pp_dfg *g, int M, uint64_t *classes) {
 }
 static const uint64_t *rgs_of(const pp_dfg *g, int M) {
     return g->d_rgs + (size_t)(M - 1) * kRgsRows * kRgsStride;
+}
+
+// The in-order search kernel enumerates tasks: an RGS prefix of π positions
+// 0..K−2 and a block of NP values of position K−1 (search_kernel.cuh).  NP is
+// fixed first (PP_NP, else M for M ≤ 3 and 4 otherwise: the M values of the
+// last position fill a lane), then tasks = (classes of K−1 positions)·⌈M/NP⌉.
+static int sym_plan(const pp_dfg *g, int M, int *np, uint64_t *tasks) {
+    int n = M <= 3 ? M : 4;
+    if (const char *v = getenv("PP_NP")) {
+        const int e = atoi(v);
+        if (e == 1 || e == 2 || e == 4) n = e;
+    }
+    uint64_t classes = 0;
+    int rc = rgs_table(g, M, &classes);
+    if (rc) return rc;
+    std::vector<unsigned __int128> prev(M + 2, 1), cur(M + 2, 0);
+    for (int r = 1; r < g->K - 1; r++) {   // classes of the K−1 prefix positions
+        for (int m = 1; m <= M; m++) cur[m] = m * prev[m] + (m < M ? prev[m + 1] : 0);
+        prev = cur;
+    }
+    *np = n;
+    *tasks = (uint64_t)prev[1] * (uint64_t)((M + n - 1) / n);
+    return PP_OK;
 }
 
 // ------------------------------------------------------------------ NCCL
@@ -610,9 +635,10 @@ int pp_search_range(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
     }
     Launch L;
     if (use_sym(g, M, gen, begin, end)) {   // the whole GRAY space: one placement per class
-        uint64_t classes = 0;
-        if ((rc = rgs_table(g, M, &classes))) return rc;
-        if ((rc = setup(g, M, GEN_SYM, false, 0, classes, L, stream))) return rc;
+        uint64_t tasks = 0;
+        int np = 0;
+        if ((rc = sym_plan(g, M, &np, &tasks))) return rc;
+        if ((rc = setup(g, M, GEN_SYM, false, 0, tasks, L, stream, np))) return rc;
         L.p.g_rgs = rgs_of(g, M);
     } else if ((rc = setup(g, M, gen, false, begin, end, L, stream))) {
         return rc;
@@ -1012,14 +1038,15 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
     // winner is reported by Gray index, so the update is GRAY's
     const bool sym = use_sym(g, M, desc->gen, 0, desc->count);
     uint64_t space = desc->count;
-    if (sym && (rc = rgs_table(g, M, &space))) return rc;
+    int sym_np = 0;
+    if (sym && (rc = sym_plan(g, M, &sym_np, &space))) return rc;
     uint64_t begin = 0, end = 0;
     pp_rank_slice(space, rank, world, &begin, &end);
     UpdateFn upd = update_for(M, desc->gen);
     Launch L;
     const bool empty = end <= begin;
     if (!empty) {
-        rc = setup(g, M, sym ? GEN_SYM : desc->gen, false, begin, end, L, stream);
+        rc = setup(g, M, sym ? GEN_SYM : desc->gen, false, begin, end, L, stream, sym_np);
         if (rc) return rc;
         L.p.tau = desc->flip_thresh;
         if (sym) L.p.g_rgs = rgs_of(g, M);

@@ -150,6 +150,7 @@ struct KParams {
     uint32_t off_cls;            // hardware graph: image offset of cls[a·8 + b]
     uint32_t off_hgw;            // image offset of the half-group base words (u32 × K8/4)
     const uint64_t *g_rgs;       // GEN_SYM: RGS completion counts of this M (device)
+    unsigned long long *g_tile;  // argmin kernels: next tile (dynamic, reset by the last CTA)
 };
 
 // ---- exact-schedule image, built when

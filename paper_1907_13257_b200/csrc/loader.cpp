@@ -568,7 +568,7 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     if ((ce = cudaMalloc(&g->d_image, bytes)) != cudaSuccess ||
         (ce = cudaMalloc(&g->d_base, 3 * g->base_bytes)) != cudaSuccess ||
         (ce = cudaMalloc(&g->d_partials, sizeof(uint64_t) * 2 * kMaxGrid)) != cudaSuccess ||
-        (ce = cudaMalloc(&g->d_ticket, sizeof(unsigned) * 4)) != cudaSuccess ||
+        (ce = cudaMalloc(&g->d_ticket, sizeof(unsigned) * 8)) != cudaSuccess ||
         (ce = cudaMalloc(&g->d_scalars, sizeof(uint64_t) * scal)) != cudaSuccess) {
         pp_free_dfg(g);
         return cuda_fail(ce);
@@ -589,7 +589,7 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     g->d_best_place = g->d_base + 2 * g->base_bytes;
     if ((ce = cudaMemcpy(g->d_image, g->image.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess ||
         (ce = cudaMemset(g->d_base, 0, 3 * g->base_bytes)) != cudaSuccess ||
-        (ce = cudaMemset(g->d_ticket, 0, sizeof(unsigned) * 4)) != cudaSuccess ||
+        (ce = cudaMemset(g->d_ticket, 0, sizeof(unsigned) * 8)) != cudaSuccess ||
         (ce = cudaMemset(g->d_scalars, 0, sizeof(uint64_t) * scal)) != cudaSuccess) {
         pp_free_dfg(g);
         return cuda_fail(ce);

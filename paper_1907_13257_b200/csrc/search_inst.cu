@@ -51,6 +51,9 @@ static KernelInfo info_gen(bool mem, bool wa, bool f64, int np, bool hw) {
 // argmin on the uniform link model
 template <bool MEM, bool F64>
 static KernelInfo info_sym_np(int np) {
+    if constexpr (PP_M == 3) {   // M = 3: a lane takes the 3 values of the last position
+        if (np == 3) return info2<GEN_SYM, MEM, false, F64, 3, false>();
+    }
     if (np >= 4) return info2<GEN_SYM, MEM, false, F64, 4, false>();
     if (np == 2) return info2<GEN_SYM, MEM, false, F64, 2, false>();
     return info2<GEN_SYM, MEM, false, F64, 1, false>();

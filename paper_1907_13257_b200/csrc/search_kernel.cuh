@@ -151,10 +151,12 @@ struct RgsGen : GrayGen<M, NP> {
     using GrayGen<M, NP>::hi;
     static constexpr int b = Bits<M>::b;
     static constexpr int PF = b ? 64 / b : 64;
-    __device__ __forceinline__ static void unrank(uint64_t r, uint32_t K, const uint64_t *__restrict__ T,
-                                                  uint64_t &lo, uint64_t &hi) {
+    // RGS of K positions with rank r into packed fields; returns the number
+    // of devices it uses
+    __device__ __forceinline__ static uint32_t unrank(uint64_t r, uint32_t K, const uint64_t *__restrict__ T,
+                                                      uint64_t &lo, uint64_t &hi) {
         lo = hi = 0;
-        if (M == 1) return;
+        if (M == 1) return 1;
         uint32_t m = 1;                                   // d[0] = 0
         for (uint32_t j = 1; j < K; j++) {
             const uint64_t c = __ldg(T + (K - 1 - j) * kRgsStride + m);
@@ -164,6 +166,7 @@ struct RgsGen : GrayGen<M, NP> {
             if (j < (uint32_t)PF) lo |= (uint64_t)v << (j * b);
             else hi |= (uint64_t)v << ((j - PF) * b);
         }
+        return m;
     }
     __device__ __forceinline__ void init(const uint64_t (&r)[NP], uint32_t K, const uint64_t *T) {
 #pragma unroll
@@ -679,7 +682,10 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
                 const double t = HW ? __dadd_rn(prev[k], hwc(a.z, pdev[k], dev[k])) : __fma_rn(c0, cut, prev[k]);
                 double f;
                 if (SM) {
-                    f = __dmul_rn(cut, ldd(fslot(k, dev[k])));
+                    // free[dev] is exact across a cut; without one it is
+                    // free[pdev]'s stale shared copy, ≤ prev ≤ t, so the max
+                    // is t either way and no cut factor is needed
+                    f = ldd(fslot(k, dev[k]));
                     std_(fslot(k, pdev[k]), prev[k]);
                 } else {
                     f = __dmul_rn(cut, oth[k]);
@@ -1119,10 +1125,10 @@ __device__ __forceinline__ void schedule_mpw(uint64_t A, uint64_t B, uint64_t dA
             a[k] = dc[k] * (uint32_t)(NP * 256) + fb;                           // &free[dev_c] − k·256
         }
         if (b.z == 0) {
-            // chain step: s = max(prev + cut·c0, cut·free[dev]); free[pdev] ← prev
+            // chain step: s = max(prev + cut·c0, free[dev]); free[pdev] ← prev
 #pragma unroll
             for (int k = 0; k < NP; k++) {
-                const double f = __dmul_rn(cut[k], ldd(a[k] + k * 256));
+                const double f = ldd(a[k] + k * 256);   // stale (≤ prev ≤ t) unless cut: no cut factor
                 std_(aprev[k] + k * 256, prev[k]);
                 const double t = __fma_rn(c0, cut[k], prev[k]);
                 prev[k] = dmax_add(t, f, cost);
@@ -1287,16 +1293,25 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
     constexpr uint32_t TILE = 32 * NP;
     constexpr bool kM2P = PP_M2P && F64 && M == 2 && !HW;   // schedule_m2p
     constexpr bool kMPW = PP_MPW && F64 && (M == 4 || M == 8) && !HW;   // schedule_mpw
-    const uint64_t ntiles = (n + TILE - 1) / TILE;
+    // GEN_SYM: a unit is a task (one RGS prefix × a block of NP last-position
+    // values), one per lane, so a tile is 32 tasks
+    const uint64_t ntiles = (n + (GEN == GEN_SYM ? 31 : TILE - 1)) / (GEN == GEN_SYM ? 32 : TILE);
     const uint64_t wpb = nthreads >> 5;
-    for (uint64_t tile = blockIdx.x * wpb + warp; tile < ntiles; tile += (uint64_t)gridDim.x * wpb) {
+    // argmin kernels take tiles from a global counter (a warp that runs ahead
+    // takes more, so no warp idles at the closing barrier while others still
+    // have a static share left); the write-all kernels stride statically
+    auto next_tile = [&](uint64_t t) -> uint64_t {
+        if (WRITE_ALL) return t + (uint64_t)gridDim.x * wpb;
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(P.g_tile, 1ull);
+        return (uint64_t)__shfl_sync(0xffffffffu, v, 0);
+    };
+    for (uint64_t tile = WRITE_ALL ? blockIdx.x * wpb + warp : next_tile(0); tile < ntiles; tile = next_tile(tile)) {
         uint64_t off[NP], idx[NP];
         bool valid[NP];
 #pragma unroll
         for (int k = 0; k < NP; k++) {
-            // GEN_SYM: a lane's placements are consecutive RGS ranks (they share
-            // a forward prefix, schedule_f64); else lane-interleaved
-            off[k] = tile * TILE + (GEN == GEN_SYM ? lane * NP + k : k * 32 + lane);
+            off[k] = tile * (GEN == GEN_SYM ? 32 : TILE) + (GEN == GEN_SYM ? lane : k * 32 + lane);
             valid[k] = off[k] < n;
             idx[k] = P.begin + (valid[k] ? off[k] : n - 1);
         }
@@ -1305,22 +1320,29 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
         const uint64_t i0 = P.begin + tile * TILE + lane;
         uint64_t mk[NP];
         if constexpr (GEN == GEN_SYM) {
+            // task t = (prefix rank) · B + block: the lane's placements are the
+            // RGS prefix of π positions 0..K−2 followed by the values
+            // v = block·NP + k at position K−1 (valid iff v < min(m + 1, M),
+            // m = devices the prefix uses).  They share the forward prefix:
+            // ⌊(K−1)/4⌋ half-groups run for placement 0 only (schedule_f64).
+            constexpr uint32_t B = (M + NP - 1) / NP;
+            constexpr uint32_t b = Bits<M>::b, PF = b ? 64 / b : 64;
             RgsGen<M, NP> g;
-            g.init(idx, P.K, P.g_rgs);
-            // forward half-groups on which all of the warp's placements agree
-            // with their lane's placement 0 (Gray prefix reuse, schedule_f64)
-            uint32_t q = P.K;
+            uint64_t plo, phi;
+            const uint32_t m = RgsGen<M, NP>::unrank(idx[0] / B, P.K - 1, P.g_rgs, plo, phi);
+            const uint32_t blk = (uint32_t)(idx[0] % B);
+            const uint32_t j = P.K - 1;
 #pragma unroll
-            for (int k = 1; k < NP; k++) {
-                const uint64_t dl = g.lo[0] ^ g.lo[k], dh = g.hi[0] ^ g.hi[k];
-                constexpr uint32_t b = Bits<M>::b, PF = b ? 64 / b : 64;
-                const uint32_t qk = dl ? (uint32_t)(__ffsll((long long)dl) - 1) / b
-                                       : dh ? PF + (uint32_t)(__ffsll((long long)dh) - 1) / b : P.K;
-                q = min(q, qk);
+            for (int k = 0; k < NP; k++) {
+                const uint32_t v = blk * NP + (uint32_t)k;
+                const bool ok = v < min(m + 1, (uint32_t)M);
+                valid[k] = valid[k] && ok;
+                const uint64_t f = (uint64_t)(ok ? v : 0u);
+                g.lo[k] = plo | (j < PF ? f << (j * b) : 0ull);
+                g.hi[k] = phi | (j < PF ? 0ull : f << ((j - PF) * b));
             }
-            q = __reduce_min_sync(0xffffffffu, q);
             schedule_np<M, NP, MEM, F64, HW>(g, mk, ops, xr, mem, lane_region, P.free_off, P.K8, P.cap, P.one_hi,
-                                              smem_base + P.off_cls, P.tau, q / 4, P.zero_off / kSlotUnit);
+                                              smem_base + P.off_cls, P.tau, (P.K - 1) / 4, P.zero_off / kSlotUnit);
             // the class's index is its smallest Gray index, needed only when
             // the class can still win
 #pragma unroll
@@ -1420,6 +1442,7 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
         P.g_out[0] = best_mk;
         P.g_out[1] = best_i;
         *P.g_ticket = 0;   // ready for the next launch on this stream
+        *P.g_tile = 0;
     }
 }
 

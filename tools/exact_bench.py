@@ -27,6 +27,14 @@ def case(name, spec, M, n):
     e.record()
     torch.cuda.synchronize()
     gpu_s = s.elapsed_time(e) / 1e3
+    # the same search without the relabelling-class reduction (§12b)
+    os.environ["PP_NO_SYM"] = "1"
+    s.record()
+    best_u, idx_u, _ = g.search_exact(M, pp.GEN_GRAY, 0, 0, None, 0, n)
+    e.record()
+    torch.cuda.synchronize()
+    os.environ.pop("PP_NO_SYM", None)
+    unreduced_s = s.elapsed_time(e) / 1e3
     mk, _ = g.eval_exact_generated(M, pp.GEN_GRAY, 0, 0, None, 0, n)
     torch.cuda.synchronize()
     s.record()
@@ -48,7 +56,9 @@ def case(name, spec, M, n):
     print(json.dumps({
         "case": name, "K": len(spec["fwd_ps"]), "M": M, "candidates": n,
         "exact_best_ps": best, "index": idx, "unresolved": unresolved, "in_order_best_ps": inorder,
-        "search_exact_s": gpu_s, "eval_exact_s": eval_s,
+        "search_exact_s": gpu_s, "search_exact_unreduced_s": unreduced_s,
+        "symmetry_speedup": unreduced_s / gpu_s, "same_as_unreduced": (best, idx) == (best_u, idx_u),
+        "eval_exact_s": eval_s,
         "search_exact_per_s": n / gpu_s, "eval_exact_per_s": n / eval_s,
         "oracle_per_s": oracle_n / cpu_s, "oracle_sample": oracle_n,
         "oracle_prefix_parity": sub[:2] == ob,
@@ -60,6 +70,7 @@ def main():
     case("toy12", synth.toy12(), 3, 3**12)
     case("random_dag_K14", synth.random_dag(5, 14, window=4), 2, 2**14)
     case("random_dag_K16", synth.random_dag(6, 16, window=4), 2, 2**16)
+    case("random_dag_K10", synth.random_dag(7, 10, window=4), 4, 4**10)
 
 
 if __name__ == "__main__":
