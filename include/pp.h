@@ -145,8 +145,14 @@ int pp_eval_placements(const pp_dfg *dfg, int M, const uint8_t *d_placements, ui
  *   GRAY    reflected M-ary Gray code of the candidate index over π positions;
  *           index 0 = all on device 0; count ≤ M^K ≤ 2^63 (= M^K: exhaustive)
  *   RANDOM  SplitMix64 words, b = ⌈log2 M⌉ bits per op; index 0 = all zero
- *   PERTURB per op flip of the base with probability flip_thresh/256 to one of
- *           the other M−1 devices; index 0 = the base; round r uses seed+r   */
+ *   PERTURB per op flip with probability flip_thresh/256: M = 2 to the other
+ *           device, M = 4, 8 re-drawn uniformly (base ⊕ y, y mod M), other M
+ *           to one of the other M−1 devices (generator revision 3, DESIGN.md
+ *           §2); index 0 = the base; round r uses seed+r
+ * Exhaustive GRAY (the whole range [0, M^K), uniform link, M ≥ 2, K ≥ 2) is
+ * evaluated one placement per device-relabelling class, with the oracle's
+ * (makespan, Gray index) winner; the
+ * results are those of the full enumeration (PP_NO_SYM=1 runs it unreduced). */
 typedef enum { PP_GEN_GRAY = 0, PP_GEN_RANDOM = 1, PP_GEN_PERTURB = 2 } pp_gen;
 
 typedef struct {
@@ -208,7 +214,10 @@ int pp_eval_exact_generated(const pp_dfg *dfg, int M, int gen, uint64_t seed_r, 
                             uint64_t *d_makespan, uint8_t *d_exact, void *cuda_stream);
 /* Lexicographically smallest (exact makespan, index) over candidates
  * [begin, end) of one round.  Placements whose bound already exceeds the
- * best makespan found so far are abandoned early (they cannot win).
+ * best makespan found so far are abandoned early (they cannot win); the
+ * incumbent starts at the in-order argmin of the same candidates, an upper
+ * bound of the exact optimum (each placement's exact makespan ≤ its
+ * in-order one), so ties at the optimum are never pruned.
  * d_best: device ptr uint64[3] = {makespan, index, number of placements that
  * hit node_limit (0 ⇒ the result is exact)}.  Asynchronous.                 */
 int pp_search_exact(const pp_dfg *dfg, int M, int gen, uint64_t seed_r, uint32_t flip_thresh,
@@ -262,8 +271,8 @@ int pp_eft_place(const pp_dfg *dfg, int M, uint8_t *placement, void *cuda_stream
 /* Full search: per round the candidates are sharded over
  * the ranks of `comm` (contiguous slices, see pp_rank_slice), each GPU takes
  * its slice's argmin, one NCCL min all-reduce of the packed key
- * (pp_pack_key) picks the winning rank, a second min all-reduce delivers the
- * winner's index; PERTURB moves the base to the round winner when it is
+ * (pp_pack_key) gives the winning makespan, a second min all-reduce delivers
+ * the smallest index reaching it (pp_round_contrib); PERTURB moves the base to the round winner when it is
  * strictly better.  comm = NULL: single GPU.  The result is identical for any
  * number of ranks.  Synchronises cuda_stream before returning.
  * Errors: PP_E_INVALID, PP_E_TOO_LARGE (GRAY space), PP_E_INFEASIBLE,

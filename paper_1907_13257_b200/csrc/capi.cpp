@@ -237,6 +237,17 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
             const long a = warps(i) * cands[i].np, b = warps(pick) * cands[pick].np;
             if (a > b || (a == b && warps(i) > warps(pick))) pick = i;
         }
+    } else if (gen == GEN_PERTURB && (M == 4 || M == 8) && g->f64 && !g->hw) {
+        // the device-word schedule (schedule_mpw): NP = 2 when it keeps ≥ 12
+        // warps per SM — the fastest for every BASELINE DFG at M = 4 and 8
+        // (profiles/r02_np_ab.txt) — else the most resident warps
+        constexpr long kWarpMin = 12;
+        bool found = false;
+        for (size_t i = 0; i < cands.size() && !found; i++)
+            if (cands[i].np == 2 && warps(i) >= kWarpMin) { pick = i; found = true; }
+        if (!found)
+            for (size_t i = 1; i < cands.size(); i++)
+                if (warps(i) > warps(pick)) pick = i;
     } else {
         constexpr long kWarpTarget = 20;   // 5 per scheduler
         bool found = false;
@@ -682,6 +693,39 @@ static int run_exact(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t 
     if ((ce = cudaMemsetAsync(g->d_xwork, 0, 4 * sizeof(unsigned long long), st)) != cudaSuccess ||
         (ce = cudaMemsetAsync(g->d_xwork + 1, 0xFF, sizeof(unsigned long long), st)) != cudaSuccess)
         return cuda_err(ce, "exact work counters");
+    if (d_best && gen != GEN_EXPLICIT && !getenv("PP_NO_SEED_INC")) {
+        // Seed the incumbent with the in-order argmin of the same candidates:
+        // every placement's exact makespan is ≤ its in-order one, so the exact
+        // optimum is ≤ that value, and pruning only trees whose bound is
+        // strictly above it keeps every optimal placement (ties included).
+        // The in-order kernel writes {makespan, index} to work[1], work[2];
+        // work[2] (the unresolved count) is cleared again afterwards.
+        const int igen = gen == GEN_SYM ? GEN_GRAY : gen;
+        uint64_t ib = begin, ie = end;
+        int rc;
+        if (gen == GEN_PERTURB) {
+            if ((rc = launch_patch_base(g->d_image, g->d_base, d_base_pi, (uint32_t)g->K, (uint32_t)g->K8,
+                                        g->off_hgw, stream)))
+                return cuda_err((cudaError_t)rc, "base patch");
+            g_launches++;
+        }
+        Launch L;
+        if (gen == GEN_SYM) {   // the classes stand for the whole Gray space
+            int np = 0;
+            if ((rc = sym_plan(g, M, &np, &ie))) return rc;
+            ib = 0;
+            if ((rc = setup(g, M, GEN_SYM, false, ib, ie, L, stream, np))) return rc;
+            L.p.g_rgs = rgs_of(g, M);
+        } else if ((rc = setup(g, M, igen, false, ib, ie, L, stream))) {
+            return rc;
+        }
+        L.p.seed = seed_r;
+        L.p.tau = tau;
+        L.p.g_out = reinterpret_cast<uint64_t *>(g->d_xwork + 1);
+        if ((rc = run(L, stream))) return rc;
+        if ((ce = cudaMemsetAsync(g->d_xwork + 2, 0, sizeof(unsigned long long), st)) != cudaSuccess)
+            return cuda_err(ce, "exact work counters");
+    }
     XParams p{};
     p.g_ximage = g->d_ximage;
     p.g_place = d_place;

@@ -875,6 +875,12 @@ __device__ __forceinline__ double dsel(uint32_t m, double a, double b) {
 #ifndef PP_M2P_LDS64
 #define PP_M2P_LDS64 1   // cost and c0 by two LDS.64 into their own pairs (A/B: -1.1%)
 #endif
+#ifndef PP_DYN_TILES
+#define PP_DYN_TILES 1   // argmin kernels take tiles from a global counter (0: static stride, for A/B)
+#endif
+#ifndef PP_TILE_PREFETCH
+#define PP_TILE_PREFETCH 0   // dynamic tiles: claim the next tile when a tile starts (A/B)
+#endif
 #ifndef PP_M2P_MIX
 #define PP_M2P_MIX 0   // chain steps: placements k with k % 4 < MIX take the ALU max (DSETP + 2 FSEL) instead of dmax_add (pipe balance)
 #endif
@@ -1297,16 +1303,22 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
     // values), one per lane, so a tile is 32 tasks
     const uint64_t ntiles = (n + (GEN == GEN_SYM ? 31 : TILE - 1)) / (GEN == GEN_SYM ? 32 : TILE);
     const uint64_t wpb = nthreads >> 5;
-    // argmin kernels take tiles from a global counter (a warp that runs ahead
-    // takes more, so no warp idles at the closing barrier while others still
-    // have a static share left); the write-all kernels stride statically
-    auto next_tile = [&](uint64_t t) -> uint64_t {
-        if (WRITE_ALL) return t + (uint64_t)gridDim.x * wpb;
+    // Tile schedule: the argmin kernels take tiles from a global counter (reset
+    // by the last CTA), so a warp that runs ahead takes more and none idles at
+    // the closing barrier while others still hold a static share (GNMT M = 2:
+    // +13%, BigLSTM +1.5%, Inception −0.9%; profiles/r02_ab_tiles.txt).  The
+    // write-all kernels stride statically.  PP_TILE_PREFETCH claims the next
+    // tile when a tile starts (A/B).
+    constexpr bool kDyn = !WRITE_ALL && PP_DYN_TILES;
+    auto claim = [&]() -> uint64_t {
         unsigned long long v = 0;
         if (lane == 0) v = atomicAdd(P.g_tile, 1ull);
         return (uint64_t)__shfl_sync(0xffffffffu, v, 0);
     };
-    for (uint64_t tile = WRITE_ALL ? blockIdx.x * wpb + warp : next_tile(0); tile < ntiles; tile = next_tile(tile)) {
+    uint64_t tile = kDyn ? claim() : blockIdx.x * wpb + warp;
+    while (tile < ntiles) {
+        unsigned long long pre = 0;
+        if (kDyn && PP_TILE_PREFETCH && lane == 0) pre = atomicAdd(P.g_tile, 1ull);
         uint64_t off[NP], idx[NP];
         bool valid[NP];
 #pragma unroll
@@ -1398,6 +1410,9 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
                 have = true;
             }
         }
+        if (!kDyn) tile += (uint64_t)gridDim.x * wpb;
+        else if (PP_TILE_PREFETCH) tile = (uint64_t)__shfl_sync(0xffffffffu, pre, 0);
+        else tile = claim();
     }
     if (WRITE_ALL) return;
 

@@ -19,7 +19,11 @@ import synth  # noqa: E402
 
 def case(name, spec, M, n):
     g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
-    g.search_exact(M, pp.GEN_GRAY, 0, 0, None, 0, min(n, 64))   # warm-up
+    g.search_exact(M, pp.GEN_GRAY, 0, 0, None, 0, min(n, 64))   # warm-up (module load, tables)
+    g.search_exact(M, pp.GEN_GRAY, 0, 0, None, 0, n)
+    os.environ["PP_NO_SYM"] = "1"
+    g.search_exact(M, pp.GEN_GRAY, 0, 0, None, 0, n)
+    os.environ.pop("PP_NO_SYM", None)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
