@@ -878,6 +878,9 @@ __device__ __forceinline__ double dsel(uint32_t m, double a, double b) {
 #ifndef PP_DYN_TILES
 #define PP_DYN_TILES 1   // argmin kernels take tiles from a global counter (0: static stride, for A/B)
 #endif
+#ifndef PP_MPW_PREFETCH
+#define PP_MPW_PREFETCH 1   // schedule_mpw: free[dev] of the next step loaded one step ahead (A/B)
+#endif
 #ifndef PP_TILE_PREFETCH
 #define PP_TILE_PREFETCH 0   // dynamic tiles: claim the next tile when a tile starts (A/B)
 #endif
@@ -1117,7 +1120,15 @@ __device__ __forceinline__ void schedule_mpw(uint64_t A, uint64_t B, uint64_t dA
             dprev[k] = dw[k];
         }
     };
+    // free[dev] of the next step of the half-group, loaded at the end of the
+    // current step (after its write-back of free[pdev]), so the shared-memory
+    // latency is off the step's dependency chain.  If the next step stays on
+    // the current device the value is that device's stale copy, which no
+    // step uses (chain: ≤ prev ≤ t; join: the cut factor 0 selects prev).
+    double fn[NP];
     auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
+        const bool pre_in = PP_MPW_PREFETCH && (fwd ? c != 0 : c != 3);    // compile-time (unrolled c)
+        const bool pre_out = PP_MPW_PREFETCH && (fwd ? c != 3 : c != 0);
         const double cost = ldd(rec);
         const double c0 = ldd(rec + 8);
         const uint4 b = lds128(rec + 16);
@@ -1134,7 +1145,7 @@ __device__ __forceinline__ void schedule_mpw(uint64_t A, uint64_t B, uint64_t dA
             // chain step: s = max(prev + cut·c0, free[dev]); free[pdev] ← prev
 #pragma unroll
             for (int k = 0; k < NP; k++) {
-                const double f = ldd(a[k] + k * 256);   // stale (≤ prev ≤ t) unless cut: no cut factor
+                const double f = pre_in ? fn[k] : ldd(a[k] + k * 256);   // stale (≤ prev ≤ t) unless cut: no cut factor
                 std_(aprev[k] + k * 256, prev[k]);
                 const double t = __fma_rn(c0, cut[k], prev[k]);
                 prev[k] = dmax_add(t, f, cost);
@@ -1162,7 +1173,7 @@ __device__ __forceinline__ void schedule_mpw(uint64_t A, uint64_t B, uint64_t dA
 #pragma unroll
             for (int k = 0; k < NP; k++) {
                 // free[dev] = cut ? free[dev] (shared) : prev, exact on the FP64 pipe
-                const double f = __fma_rn(cut[k], __dadd_rn(ldd(a[k] + k * 256), -prev[k]), prev[k]);
+                const double f = __fma_rn(cut[k], __dadd_rn(pre_in ? fn[k] : ldd(a[k] + k * 256), -prev[k]), prev[k]);
                 std_(aprev[k] + k * 256, prev[k]);
                 prev[k] = dmax_add(clear_tag(r[k]), f, cost);
                 aprev[k] = a[k];
@@ -1171,6 +1182,12 @@ __device__ __forceinline__ void schedule_mpw(uint64_t A, uint64_t B, uint64_t dA
         if (b.y != kNoStore) {
 #pragma unroll
             for (int k = 0; k < NP; k++) std_(lane + b.y * NP + k * 256, with_tag(prev[k], dc[k]));
+        }
+        if (pre_out) {
+            const uint32_t cn = fwd ? c + 1 : c - 1;
+#pragma unroll
+            for (int k = 0; k < NP; k++)
+                fn[k] = ldd(prmt(dw[k], 0u, 0x4440u | cn) * (uint32_t)(NP * 256) + fb + k * 256);
         }
         if (MEM && fwd) {
             const uint64_t mm = mem[p];
