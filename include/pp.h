@@ -123,6 +123,21 @@ int  pp_load_dfg(const pp_dfg_desc *desc, const pp_link_desc *link, int cuda_dev
 int  pp_load_dfg_hw(const pp_dfg_desc *desc, const pp_hw_desc *hw, int cuda_device, pp_dfg **out);
 void pp_free_dfg(pp_dfg *dfg);
 int  pp_dfg_get_info(const pp_dfg *dfg, pp_dfg_info *out);
+/* The state tier the DFG runs on, decided at load time:
+ *   PP_TIER_SHARED  image and lane state in shared memory (every kernel);
+ *   PP_TIER_GLOBAL  the image (> 96 KB) or the per-lane state ((W + 1 + M)
+ *                   slots × 8 B; fewer than 4 resident warps per SM would fit)
+ *                   beyond shared memory: the search/eval calls run
+ *                   search_big_kernel (image read from HBM through L1/L2, lane
+ *                   state in a global scratch, tagged-u64 arithmetic) with
+ *                   identical results.  The symmetry-reduced exhaustive search
+ *                   is not used there (the plain Gray order gives the same
+ *                   argmin); hardware graphs are rejected (PP_E_TOO_LARGE).
+ * The environment variable PP_TIER=global, read by pp_load_dfg, forces the
+ * global tier (tests).  Returns the tier, or PP_E_INVALID for NULL.         */
+#define PP_TIER_SHARED 0
+#define PP_TIER_GLOBAL 1
+int  pp_dfg_get_tier(const pp_dfg *dfg);
 /* host ptr pi_out[K]: pi_out[p] = descriptor index of the op at π position p */
 int  pp_dfg_get_pi(const pp_dfg *dfg, int32_t *pi_out);
 

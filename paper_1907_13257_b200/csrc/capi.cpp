@@ -36,7 +36,8 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
 #define PP_DECL_M(m)                                                                   \
     KernelInfo kernel_for_m##m(int gen, bool mem, bool wa, bool f64, int np, bool hw); \
     UpdateFn update_for_m##m(int gen);                                                 \
-    XKernelInfo exact_for_m##m(int gen);
+    XKernelInfo exact_for_m##m(int gen);                                              \
+    KernelInfo big_for_m##m(int gen);
 PP_DECL_M(1) PP_DECL_M(2) PP_DECL_M(3) PP_DECL_M(4) PP_DECL_M(5) PP_DECL_M(6) PP_DECL_M(7) PP_DECL_M(8)
 
 KernelInfo kernel_for(int M, int gen, bool mem, bool wa, bool f64, int np, bool hw) {
@@ -49,6 +50,18 @@ KernelInfo kernel_for(int M, int gen, bool mem, bool wa, bool f64, int np, bool 
         case 6: return kernel_for_m6(gen, mem, wa, f64, np, hw);
         case 7: return kernel_for_m7(gen, mem, wa, f64, np, hw);
         default: return kernel_for_m8(gen, mem, wa, f64, np, hw);
+    }
+}
+KernelInfo big_kernel_for(int M, int gen) {
+    switch (M) {
+        case 1: return big_for_m1(gen);
+        case 2: return big_for_m2(gen);
+        case 3: return big_for_m3(gen);
+        case 4: return big_for_m4(gen);
+        case 5: return big_for_m5(gen);
+        case 6: return big_for_m6(gen);
+        case 7: return big_for_m7(gen);
+        default: return big_for_m8(gen);
     }
 }
 UpdateFn update_for(int M, int gen) {
@@ -211,8 +224,63 @@ static void fill(const pp_dfg *g, const Choice &best, uint64_t begin, uint64_t e
 // call for a (DFG, M, generator) and keeps the fastest.  The result never
 // depends on the choice (every variant is bit-exact), only the speed.
 // The per-candidate (write-all) kernels are built for NP = 2 only.
+// The global-state tier (pp_dfg::big): search_big_kernel with
+// 256-thread CTAs, one placement per lane, and a warp region of
+// (W + 1 + M) slots × 256 B in the DFG's global scratch.  The kernel uses no
+// shared memory beyond its argmin scratch, so the L1 carve-out is maximal.
+// Resident warps: the occupancy limit, unless the live state of all warps
+// would exceed PP_BIG_STATE_MB (default 4096) of scratch.
+static int setup_big(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin, uint64_t end, Launch &L) {
+    if (gen == GEN_SYM) {
+        set_error("symmetry-reduced search needs the shared-memory tier");
+        return PP_E_TOO_LARGE;
+    }
+    L.k = big_kernel_for(M, gen);
+    constexpr int kThreads = 256;
+    const uint64_t region = ((uint64_t)g->W + 1 + (M > 2 ? (uint64_t)M : 0ull)) * kSlotUnit;
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.k.func, kThreads, 0);
+    if (e != cudaSuccess) return cuda_err(e, "occupancy");
+    e = cudaFuncSetAttribute(L.k.func, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute carveout");
+    uint64_t budget = 4096ull << 20;
+    if (const char *v = getenv("PP_BIG_STATE_MB")) budget = std::max<uint64_t>(1, strtoull(v, nullptr, 10)) << 20;
+    const uint64_t fit = budget / (region * (kThreads / 32) * (uint64_t)g->sm_count);
+    per_sm = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)std::max(per_sm, 1), fit));
+    const uint64_t n = end - begin;
+    const uint64_t tiles = (n + 31) / 32;
+    uint64_t grid = std::min<uint64_t>((uint64_t)per_sm * g->sm_count, (tiles + kThreads / 32 - 1) / (kThreads / 32));
+    grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, kMaxGrid));
+    const size_t need = (size_t)grid * (kThreads / 32) * region;
+    pp_dfg *mg = const_cast<pp_dfg *>(g);
+    if (need > mg->state_bytes) {   // stream-ordered like every other per-DFG buffer
+        if (mg->d_state) cudaFree(mg->d_state);
+        mg->d_state = nullptr;
+        mg->state_bytes = 0;
+        if ((e = cudaMalloc(&mg->d_state, need)) != cudaSuccess) return cuda_err(e, "cudaMalloc state");
+        mg->state_bytes = need;
+    }
+    L.threads = kThreads;
+    L.grid = (int)grid;
+    L.smem = 0;
+    L.np = 1;
+    Choice c;
+    c.k = L.k;
+    c.np = 1;
+    c.threads = kThreads;
+    c.ctas = per_sm;
+    c.region = (uint32_t)region;
+    c.slots_off = 0;
+    fill(g, c, begin, end, L);
+    L.grid = (int)grid;
+    L.p.g_state = mg->d_state;
+    L.p.g_makespan = nullptr;   // set by the write-all callers
+    return PP_OK;
+}
+
 static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin, uint64_t end, Launch &L,
                  void *stream = nullptr, int force_np = 0) {
+    if (g->big) return setup_big(g, M, gen, write_all, begin, end, L);
     int forced = force_np;   // PP_NP=1|2|4 pins NP (tests cover every variant)
     if (const char *v = getenv("PP_NP"); v && !forced) forced = atoi(v);
     std::vector<Choice> cands;
@@ -340,7 +408,7 @@ static int check_gen_args(const pp_dfg *g, int M, int gen, uint32_t tau, uint64_
 // DESIGN.md §12b).  The (makespan, Gray index) argmin is the full search's.
 // PP_NO_SYM=1 turns it off (A/B and tests).
 static bool use_sym(const pp_dfg *g, int M, int gen, uint64_t begin, uint64_t end) {
-    if (gen != GEN_GRAY || g->hw || M < 2 || g->K < 2 || begin != 0 || getenv("PP_NO_SYM")) return false;
+    if (gen != GEN_GRAY || g->hw || g->big || M < 2 || g->K < 2 || begin != 0 || getenv("PP_NO_SYM")) return false;
     unsigned __int128 space = 1;
     for (int j = 0; j < g->K; j++) space *= (unsigned)M;   // ≤ 2^63 (check_gen_args)
     return (unsigned __int128)end == space;
@@ -582,6 +650,11 @@ int pp_dfg_get_info(const pp_dfg *g, pp_dfg_info *out) {
     out->t1_ps = g->t1;
     out->grad_bytes = g->grad_bytes;
     return PP_OK;
+}
+
+int pp_dfg_get_tier(const pp_dfg *g) {
+    if (!g) { set_error("NULL argument"); return PP_E_INVALID; }
+    return g->big ? PP_TIER_GLOBAL : PP_TIER_SHARED;
 }
 
 int pp_dfg_get_pi(const pp_dfg *g, int32_t *pi_out) {

@@ -126,6 +126,7 @@ constexpr int kRgsRows = 65;
 constexpr uint64_t kInfeasible = ~0ull;
 constexpr int kMaxImageBytes = 96 * 1024;
 constexpr int kMaxSmemBytes = 227 * 1024;
+constexpr int kTierSmemBytes = 200 * 1024;   // shared-memory tier: image + 4 warps of lane state
 
 // Kernel parameters (by value).
 struct KParams {
@@ -151,6 +152,7 @@ struct KParams {
     uint32_t off_hgw;            // image offset of the half-group base words (u32 × K8/4)
     const uint64_t *g_rgs;       // GEN_SYM: RGS completion counts of this M (device)
     unsigned long long *g_tile;  // argmin kernels: next tile (dynamic, reset by the last CTA)
+    uint8_t *g_state;            // global-state tier: warp regions of the lane state (search_big_kernel)
 };
 
 // ---- exact-schedule image, built when
@@ -294,6 +296,8 @@ struct KernelInfo {
 
 // search_inst.cu (compiled once per M with -DPP_M): kernel_for_m<M>(...)
 KernelInfo kernel_for(int M, int gen, bool mem, bool write_all, bool f64, int np, bool hw);
+// the global-state tier: one kernel per (M, generator), tagged-u64 arithmetic
+KernelInfo big_kernel_for(int M, int gen);
 UpdateFn update_for(int M, int gen);
 
 }  // namespace pp
@@ -303,6 +307,7 @@ struct pp_dfg {
     int K = 0, K8 = 0, E = 0, W = 0;
     bool f64 = false;            // tagged-f64 arithmetic (bound < 2^49) else tagged-u64
     bool hw = false;             // general hardware graph: class-cost rows (pp_load_dfg_hw)
+    bool big = false;            // global-state tier: image or lane state beyond shared memory
     int nd = 0;                  // hardware-graph devices
     uint32_t off_cls = 0;        // image offset of the 8×8 class table
     uint64_t t1 = 0, grad_bytes = 0, cap = 0;
@@ -337,6 +342,8 @@ struct pp_dfg {
     unsigned *d_ticket = nullptr;
     uint64_t *d_scalars = nullptr;    // see capi.cpp (round result, keys, best)
     int sm_count = 0;
+    uint8_t *d_state = nullptr;       // global-state tier scratch (grown on demand)
+    size_t state_bytes = 0;
 };
 
 namespace pp {

@@ -292,6 +292,22 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
         if (!strcmp(a, "int64")) f64 = false;
     }
     if (hw) f64 = true;   // the class-cost rows are f64-encoded
+
+    // ---- tier: the shared-memory tier needs the image plus
+    // at least 4 warps of lane state ((W + 1 + 8) slots × 256 B at one
+    // placement per lane, M ≤ 8) within the SM's shared memory; otherwise the
+    // DFG runs on the global-state tier (search_big_kernel, tagged-u64
+    // arithmetic).  PP_TIER=global forces that tier (tests).
+    size_t n_extra_all = 0;
+    for (int s = 0; s < S; s++) n_extra_all += inputs[s].size() - 1;
+    const size_t image_est = ((sizeof(OpRec) * S + sizeof(ExtraRec) * n_extra_all + 13ull * K8 + 15) & ~size_t(15));
+    bool big = image_est > (size_t)kMaxImageBytes ||
+               ((image_est + 127) & ~size_t(127)) + 4ull * ((size_t)W + 9) * kSlotUnit > (size_t)kTierSmemBytes;
+    if (const char *t = getenv("PP_TIER")) {
+        if (!strcmp(t, "global")) big = true;
+    }
+    if (big && hw) return fail(PP_E_TOO_LARGE, "hardware graphs need the shared-memory tier (image + 4 warps of lane state within 200 KB)");
+    if (big) f64 = false;
     auto enc = [&](uint64_t ps) -> uint64_t {
         if (!f64) return 8ull * ps;
         double x = (double)ps;   // exact: ps < 2^49
@@ -364,7 +380,8 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
         for (auto &o : ops) o.c8 = off_rows + o.c8 * row_bytes;
         for (auto &x : xr) x.c8 = off_rows + x.c8 * row_bytes;
     }
-    if (bytes > (size_t)kMaxImageBytes) return fail(PP_E_TOO_LARGE, "DFG image exceeds 96 KB of shared memory");
+    if (!big && bytes > (size_t)kMaxImageBytes) return fail(PP_E_TOO_LARGE, "DFG image exceeds 96 KB of shared memory");
+    if (bytes >= (size_t)1 << 31) return fail(PP_E_TOO_LARGE, "DFG image exceeds 2 GB");
 
     pp_dfg *g = new pp_dfg();
     g->device = cuda_device;
@@ -373,6 +390,7 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     g->E = E;
     g->W = W;
     g->f64 = f64;
+    g->big = big;
     g->t1 = (uint64_t)t1;
     g->cap = hw ? hw->dev_mem_cap_bytes : link->dev_mem_cap_bytes;
     g->hw = hw != nullptr;
@@ -616,6 +634,7 @@ extern "C" void pp_free_dfg(pp_dfg *g) {
     if (g->d_gimage) cudaFree(g->d_gimage);
     if (g->d_pipe) cudaFree(g->d_pipe);
     if (g->d_rgs) cudaFree(g->d_rgs);
+    if (g->d_state) cudaFree(g->d_state);
     cudaSetDevice(prev);
     delete g;
 }

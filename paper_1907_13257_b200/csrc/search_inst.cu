@@ -74,6 +74,23 @@ KernelInfo PP_CAT(kernel_for_m, PP_M)(int gen, bool mem, bool wa, bool f64, int 
     }
 }
 
+KernelInfo PP_CAT(big_for_m, PP_M)(int gen) {
+    switch (gen) {
+        case GEN_GRAY:
+            return KernelInfo{&launch_search_big<PP_M, GEN_GRAY>,
+                              reinterpret_cast<const void *>(&search_big_kernel<PP_M, GEN_GRAY>)};
+        case GEN_RANDOM:
+            return KernelInfo{&launch_search_big<PP_M, GEN_RANDOM>,
+                              reinterpret_cast<const void *>(&search_big_kernel<PP_M, GEN_RANDOM>)};
+        case GEN_PERTURB:
+            return KernelInfo{&launch_search_big<PP_M, GEN_PERTURB>,
+                              reinterpret_cast<const void *>(&search_big_kernel<PP_M, GEN_PERTURB>)};
+        default:
+            return KernelInfo{&launch_search_big<PP_M, GEN_EXPLICIT>,
+                              reinterpret_cast<const void *>(&search_big_kernel<PP_M, GEN_EXPLICIT>)};
+    }
+}
+
 UpdateFn PP_CAT(update_for_m, PP_M)(int gen) {
     switch (gen) {
         case GEN_GRAY: return &launch_update<PP_M, GEN_GRAY>;

@@ -352,6 +352,25 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
     return v;
 }
 
+// Memory spaces of the generic schedule body (schedule_gen): the shared-
+// memory tier addresses the image and the lane state by 32-bit shared-window
+// addresses; the global-state tier (DFGs whose image or per-lane state does
+// not fit in shared memory, search_big_kernel) by 64-bit global addresses,
+// with the same [slot][lane] layout (a warp's 32 lanes read 256 contiguous
+// bytes) — records through the read-only path, state through L1/L2.
+struct SmemSpace {
+    typedef uint32_t Addr;
+    static __device__ __forceinline__ uint4 rec(Addr a) { return lds128(a); }
+    static __device__ __forceinline__ uint64_t ld(Addr a) { return lds64(a); }
+    static __device__ __forceinline__ void st(Addr a, uint64_t v) { sts64(a, v); }
+};
+struct GmemSpace {
+    typedef uint64_t Addr;
+    static __device__ __forceinline__ uint4 rec(Addr a) { return __ldg(reinterpret_cast<const uint4 *>(a)); }
+    static __device__ __forceinline__ uint64_t ld(Addr a) { return *reinterpret_cast<const uint64_t *>(a); }
+    static __device__ __forceinline__ void st(Addr a, uint64_t v) { *reinterpret_cast<uint64_t *>(a) = v; }
+};
+
 // ---------------------------------------------------------- arithmetic
 // Two exact representations of a tagged finish time (internal.h):
 //   ArithU64: 8·t + device in a u64;
@@ -424,12 +443,14 @@ struct MemUse {
 };
 
 // -------------------------------------------------- NP placements per lane
-// lane: shared address of this lane's entry in its warp region (region +
-// 8·lane); placement k's copy of a slot is at +k·256.
-template <int M, int NP, bool MEM, bool F64, class Gen>
-__device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], uint32_t ops, uint32_t xr,
-                                            const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
+// lane: address of this lane's entry in its warp region (region + 8·lane);
+// placement k's copy of a slot is at +k·256.  S: the memory space of the
+// image and the state (SmemSpace, or GmemSpace for the global-state tier).
+template <int M, int NP, bool MEM, bool F64, class Gen, class S = SmemSpace>
+__device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], typename S::Addr ops, typename S::Addr xr,
+                                            const uint64_t *__restrict__ mem, typename S::Addr lane, uint32_t free_off,
                                             uint32_t K8, uint64_t cap) {
+    typedef typename S::Addr Addr;
     typedef typename std::conditional<F64, ArithF64, ArithU64>::type A;
     typedef typename A::V V;
     V prev[NP], oth[NP];
@@ -441,14 +462,14 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], uint3
         if (MEM) mu[k].init();
         if (M > 2) {
 #pragma unroll
-            for (int d = 0; d < M; d++) sts64(lane + free_off * NP + d * NP * 256 + k * 256, 0);
+            for (int d = 0; d < M; d++) S::st(lane + free_off * NP + d * NP * 256 + k * 256, 0);
         }
     }
-    uint32_t x = xr;
+    Addr x = xr;
 
-    auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
-        const uint4 a = lds128(rec);
-        const uint4 b = lds128(rec + 16);
+    auto step = [&](Addr rec, uint32_t p, uint32_t c, bool fwd) {
+        const uint4 a = S::rec(rec);
+        const uint4 b = S::rec(rec + 16);
         const uint64_t cost = ((uint64_t)a.y << 32) | a.x;
         const uint64_t c0 = ((uint64_t)a.w << 32) | a.z;
         uint32_t dev[NP];
@@ -493,17 +514,17 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], uint3
                 for (int k = 0; k < NP; k++) r[k] = cut_add<A, M>(prev[k], dev[k], c0);
             } else {
 #pragma unroll
-                for (int k = 0; k < NP; k++) r[k] = cut_add<A, M>(A::from_bits(lds64(lane + b.x * NP + k * 256)), dev[k], c0);
+                for (int k = 0; k < NP; k++) r[k] = cut_add<A, M>(A::from_bits(S::ld(lane + b.x * NP + k * 256)), dev[k], c0);
             }
             const uint32_t nx = b.z & 0xFFFFu;
 #pragma unroll 1
             for (uint32_t q = 0; q < nx; q++) {   // further inputs (uniform trip count)
-                const uint4 e = lds128(x);
+                const uint4 e = S::rec(x);
                 x += sizeof(ExtraRec);
                 const uint64_t ce = ((uint64_t)e.y << 32) | e.x;
 #pragma unroll
                 for (int k = 0; k < NP; k++)
-                    r[k] = A::vmax(r[k], cut_add<A, M>(A::from_bits(lds64(lane + e.z * NP + k * 256)), dev[k], ce));
+                    r[k] = A::vmax(r[k], cut_add<A, M>(A::from_bits(S::ld(lane + e.z * NP + k * 256)), dev[k], ce));
             }
 #pragma unroll
             for (int k = 0; k < NP; k++) {
@@ -515,10 +536,10 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], uint3
                     s = A::vmax(r[k], same ? prev[k] : oth[k]);
                     oth[k] = same ? oth[k] : prev[k];
                 } else {
-                    const uint32_t fa = lane + free_off * NP + dev[k] * NP * 256 + k * 256;
-                    s = A::vmax(r[k], A::from_bits(lds64(fa)));
+                    const Addr fa = lane + free_off * NP + dev[k] * NP * 256 + k * 256;
+                    s = A::vmax(r[k], A::from_bits(S::ld(fa)));
                     prev[k] = A::finish(s, dev[k], cost);
-                    sts64(fa, A::to_bits(prev[k]));
+                    S::st(fa, A::to_bits(prev[k]));
                     continue;
                 }
                 prev[k] = A::finish(s, dev[k], cost);
@@ -526,7 +547,7 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], uint3
         }
         if (b.y != kNoStore) {
 #pragma unroll
-            for (int k = 0; k < NP; k++) sts64(lane + b.y * NP + k * 256, A::to_bits(prev[k]));
+            for (int k = 0; k < NP; k++) S::st(lane + b.y * NP + k * 256, A::to_bits(prev[k]));
         }
         if (MEM && fwd) {
             const uint64_t m = mem[p];
@@ -543,7 +564,7 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], uint3
 #pragma unroll (kHalfUnroll)
         for (uint32_t h = 0; h < 2; h++) {
             gen.sub(h);
-            const uint32_t rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
+            const Addr rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
 #pragma unroll
             for (uint32_t cc = 0; cc < 4; cc++) step(rec + cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, true);
         }
@@ -553,10 +574,10 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], uint3
 #pragma unroll (kHalfUnroll)
         for (uint32_t h = 2; h-- > 0;) {
             gen.sub(h);
-            const uint32_t rec = ops + (2 * K8 - 1 - g * 8 - h * 4) * (uint32_t)sizeof(OpRec);
+            const Addr rec = ops + (2 * K8 - 1 - g * 8 - h * 4) * (uint32_t)sizeof(OpRec);
 #pragma unroll
             for (int cc = 3; cc >= 0; cc--)
-                step(rec - (uint32_t)cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, false);
+                step(rec - (Addr)cc * (Addr)sizeof(OpRec), g * 8 + h * 4 + cc, cc, false);
         }
     }
 #pragma unroll
@@ -567,7 +588,7 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], uint3
         } else {
             v = A::from_bits(0);
 #pragma unroll
-            for (int d = 0; d < M; d++) v = A::vmax(v, A::from_bits(lds64(lane + free_off * NP + d * NP * 256 + k * 256)));
+            for (int d = 0; d < M; d++) v = A::vmax(v, A::from_bits(S::ld(lane + free_off * NP + d * NP * 256 + k * 256)));
         }
         mk[k] = A::ps(v);
         if (MEM && mu[k].over(cap)) mk[k] = kInfeasible;
@@ -1257,6 +1278,58 @@ __device__ __forceinline__ bool lex_less(uint64_t m1, uint64_t i1, uint64_t m2, 
     return m1 < m2 || (m1 == m2 && i1 < i2);
 }
 
+// ---- argmin epilogue: warp shuffle → CTA (shared) → grid (the last CTA to
+// finish reduces the per-CTA partials and resets the ticket and tile counter)
+__device__ __forceinline__ void grid_argmin(const KParams &P, uint64_t best_mk, uint64_t best_i, uint64_t *red_mk,
+                                            uint64_t *red_i, bool &is_last) {
+    const uint32_t tid = threadIdx.x;
+    const uint32_t lane = tid & 31, warp = tid >> 5;
+    const uint32_t nthreads = blockDim.x;
+    const uint32_t wpb = nthreads >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t om = __shfl_xor_sync(0xffffffffu, best_mk, o);
+        uint64_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+        if (lex_less(om, oi, best_mk, best_i)) { best_mk = om; best_i = oi; }
+    }
+    if (lane == 0) { red_mk[warp] = best_mk; red_i[warp] = best_i; }
+    __syncthreads();
+    if (tid == 0) {
+        for (uint32_t w = 1; w < wpb; w++)
+            if (lex_less(red_mk[w], red_i[w], best_mk, best_i)) { best_mk = red_mk[w]; best_i = red_i[w]; }
+        P.g_partials[2 * blockIdx.x] = best_mk;
+        P.g_partials[2 * blockIdx.x + 1] = best_i;
+        __threadfence();
+        unsigned t = atomicAdd(P.g_ticket, 1u);
+        is_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    best_mk = kInfeasible;
+    best_i = kInfeasible;
+    for (uint32_t c = tid; c < gridDim.x; c += nthreads) {
+        uint64_t m = __ldcg(P.g_partials + 2 * c), ii = __ldcg(P.g_partials + 2 * c + 1);
+        if (lex_less(m, ii, best_mk, best_i)) { best_mk = m; best_i = ii; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t om = __shfl_xor_sync(0xffffffffu, best_mk, o);
+        uint64_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+        if (lex_less(om, oi, best_mk, best_i)) { best_mk = om; best_i = oi; }
+    }
+    if (lane == 0) { red_mk[warp] = best_mk; red_i[warp] = best_i; }
+    __syncthreads();
+    if (tid == 0) {
+        for (uint32_t w = 1; w < wpb; w++)
+            if (lex_less(red_mk[w], red_i[w], best_mk, best_i)) { best_mk = red_mk[w]; best_i = red_i[w]; }
+        P.g_out[0] = best_mk;
+        P.g_out[1] = best_i;
+        *P.g_ticket = 0;   // ready for the next launch on this stream
+        *P.g_tile = 0;
+    }
+}
+
 // ------------------------------------------------------------------ kernel
 template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64, int NP, bool HW>
 __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(const KParams P) {
@@ -1433,49 +1506,94 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
     }
     if (WRITE_ALL) return;
 
-    // ---- argmin: warp shuffle → CTA (shared) → grid (last CTA)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        uint64_t om = __shfl_xor_sync(0xffffffffu, best_mk, o);
-        uint64_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
-        if (lex_less(om, oi, best_mk, best_i)) { best_mk = om; best_i = oi; }
+    grid_argmin(P, best_mk, best_i, red_mk, red_i, is_last);
+}
+
+// ------------------------------------------------- global-state tier
+// DFGs whose image exceeds the shared-memory budget, or whose per-lane state
+// ((W + 1 + M) slots) leaves fewer than 4 resident warps per SM, run here
+// (pp_dfg::big, decided at load time).  The recurrence is
+// schedule_gen's, operation for operation, on the tagged-u64 arithmetic (the
+// loader encodes such images in u64); only the memory space differs: records
+// are read from the HBM image through the read-only path (every warp reads the
+// same records, so they stay L1/L2-resident), and the lane state is a warp
+// region of the global scratch P.g_state laid out [slot][lane] like the
+// shared one.  One placement per lane; the memory cap is a runtime value
+// (UINT64_MAX when absent) and the per-candidate output a runtime mode
+// (P.g_makespan ≠ nullptr), so one kernel per (M, generator).
+template <int M, int GEN>
+__global__ void __launch_bounds__(256) search_big_kernel(const KParams P) {
+    __shared__ uint64_t red_mk[32], red_i[32];
+    __shared__ bool is_last;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t lane = tid & 31, warp = tid >> 5;
+    const uint64_t wpb = blockDim.x >> 5;
+    const bool write_all = P.g_makespan != nullptr;
+    const uint64_t cap = P.cap ? P.cap : ~0ull;
+    const uint64_t ops = reinterpret_cast<uint64_t>(P.g_image);
+    const uint64_t xr = ops + P.off_extra;
+    const uint64_t *mem = reinterpret_cast<const uint64_t *>(P.g_image + P.off_mem);
+    const uint32_t *orig = reinterpret_cast<const uint32_t *>(P.g_image + P.off_orig);
+    const uint64_t lane_region =
+        reinterpret_cast<uint64_t>(P.g_state) + (blockIdx.x * wpb + warp) * (uint64_t)P.region_bytes + lane * 8u;
+    *reinterpret_cast<uint64_t *>(lane_region + P.zero_off) = 0;   // the always-zero slot
+
+    uint64_t best_mk = kInfeasible, best_i = kInfeasible;
+    const uint64_t n = P.end - P.begin;
+    const uint64_t ntiles = (n + 31) / 32;
+    auto claim = [&]() -> uint64_t {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(P.g_tile, 1ull);
+        return (uint64_t)__shfl_sync(0xffffffffu, v, 0);
+    };
+    uint64_t tile = write_all ? blockIdx.x * wpb + warp : claim();
+    while (tile < ntiles) {
+        const uint64_t off = tile * 32 + lane;
+        const bool valid = off < n;
+        const uint64_t idx = P.begin + (valid ? off : n - 1);
+        const uint64_t i0 = P.begin + tile * 32 + lane;
+        uint64_t mk[1];
+        if constexpr (GEN == GEN_GRAY) {
+            GrayGen<M, 1> g;
+            const uint64_t ii[1] = {idx};
+            g.init(ii, P.K);
+            schedule_gen<M, 1, true, false, GrayGen<M, 1>, GmemSpace>(g, mk, ops, xr, mem, lane_region, P.free_off,
+                                                                       P.K8, cap);
+        } else if constexpr (GEN == GEN_RANDOM) {
+            RandomGen<M, 1> g;
+            g.init(i0, P.seed, P.K);
+            schedule_gen<M, 1, true, false, RandomGen<M, 1>, GmemSpace>(g, mk, ops, xr, mem, lane_region,
+                                                                         P.free_off, P.K8, cap);
+        } else if constexpr (GEN == GEN_PERTURB) {
+            PerturbGen<M, 1> g;
+            g.init(i0, P.seed, P.K, P.tau);
+            schedule_gen<M, 1, true, false, PerturbGen<M, 1>, GmemSpace>(g, mk, ops, xr, mem, lane_region,
+                                                                          P.free_off, P.K8, cap);
+        } else {
+            ExplicitGen<M, 1> g;
+            g.row[0] = P.g_place + (idx - P.begin) * (uint64_t)P.K;
+            g.bad[0] = 0;
+            g.orig = orig;
+            schedule_gen<M, 1, true, false, ExplicitGen<M, 1>, GmemSpace>(g, mk, ops, xr, mem, lane_region,
+                                                                           P.free_off, P.K8, cap);
+            if (g.bad[0]) mk[0] = kInfeasible;
+        }
+        if (write_all) {
+            if (valid) P.g_makespan[off] = mk[0];
+        } else if (valid && lex_less(mk[0], idx, best_mk, best_i)) {
+            best_mk = mk[0];
+            best_i = idx;
+        }
+        tile = write_all ? tile + (uint64_t)gridDim.x * wpb : claim();
     }
-    if (lane == 0) { red_mk[warp] = best_mk; red_i[warp] = best_i; }
-    __syncthreads();
-    if (tid == 0) {
-        for (uint32_t w = 1; w < wpb; w++)
-            if (lex_less(red_mk[w], red_i[w], best_mk, best_i)) { best_mk = red_mk[w]; best_i = red_i[w]; }
-        P.g_partials[2 * blockIdx.x] = best_mk;
-        P.g_partials[2 * blockIdx.x + 1] = best_i;
-        __threadfence();
-        unsigned t = atomicAdd(P.g_ticket, 1u);
-        is_last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-    best_mk = kInfeasible;
-    best_i = kInfeasible;
-    for (uint32_t c = tid; c < gridDim.x; c += nthreads) {
-        uint64_t m = __ldcg(P.g_partials + 2 * c), ii = __ldcg(P.g_partials + 2 * c + 1);
-        if (lex_less(m, ii, best_mk, best_i)) { best_mk = m; best_i = ii; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        uint64_t om = __shfl_xor_sync(0xffffffffu, best_mk, o);
-        uint64_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
-        if (lex_less(om, oi, best_mk, best_i)) { best_mk = om; best_i = oi; }
-    }
-    if (lane == 0) { red_mk[warp] = best_mk; red_i[warp] = best_i; }
-    __syncthreads();
-    if (tid == 0) {
-        for (uint32_t w = 1; w < wpb; w++)
-            if (lex_less(red_mk[w], red_i[w], best_mk, best_i)) { best_mk = red_mk[w]; best_i = red_i[w]; }
-        P.g_out[0] = best_mk;
-        P.g_out[1] = best_i;
-        *P.g_ticket = 0;   // ready for the next launch on this stream
-        *P.g_tile = 0;
-    }
+    if (write_all) return;
+    grid_argmin(P, best_mk, best_i, red_mk, red_i, is_last);
+}
+
+template <int M, int GEN>
+int launch_search_big(const KParams &p, int grid, int threads, int smem, void *stream) {
+    search_big_kernel<M, GEN><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
+    return (int)cudaGetLastError();
 }
 
 // ---------------------------------------------------------- round update

@@ -21,6 +21,7 @@ PP_OK = 0
 ERRORS = {-1: "PP_E_INVALID", -2: "PP_E_CYCLE", -3: "PP_E_RANGE", -4: "PP_E_TOO_LARGE",
           -5: "PP_E_INFEASIBLE", -6: "PP_E_CUDA", -7: "PP_E_NCCL"}
 GEN_GRAY, GEN_RANDOM, GEN_PERTURB = 0, 1, 2
+TIER_SHARED, TIER_GLOBAL = 0, 1   # pp_dfg_get_tier (pp.h)
 INFEASIBLE = (1 << 64) - 1
 
 
@@ -100,6 +101,7 @@ SIGNATURES = {
     "pp_free_dfg": ([C.c_void_p], None),
     "pp_dfg_get_info": ([C.c_void_p, P(DfgInfo)], C.c_int),
     "pp_dfg_get_pi": ([C.c_void_p, P(C.c_int32)], C.c_int),
+    "pp_dfg_get_tier": ([C.c_void_p], C.c_int),
     "pp_eval_placements": ([C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
     "pp_eval_generated": ([C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint64,
                            C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
@@ -250,6 +252,7 @@ class Dfg:
         _check(lib().pp_dfg_get_info(h, C.byref(info)))
         self.K, self.E, self.W = info.num_ops, info.num_edges, info.num_slots
         self.image_bytes, self.t1, self.grad_bytes = info.image_bytes, int(info.t1_ps), int(info.grad_bytes)
+        self.tier = lib().pp_dfg_get_tier(h)   # TIER_SHARED / TIER_GLOBAL (pp.h)
         pi = np.zeros(K, dtype=np.int32)
         _check(lib().pp_dfg_get_pi(h, _ptr(pi, C.c_int32)))
         self.pi = pi

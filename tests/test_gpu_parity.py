@@ -234,18 +234,6 @@ def test_large_image_reduces_cta():
         assert np.array_equal(got, want)
 
 
-def test_state_too_large_is_reported():
-    # producers anywhere in a 1000-op DAG keep hundreds of values live: the
-    # per-warp state cannot fit in shared memory -> PP_E_TOO_LARGE (pp.h)
-    spec = synth.random_dag(5, 900, avg_deg=1.5)
-    g = pp.Dfg(spec)
-    if g.W < 300:
-        pytest.skip(f"W={g.W} fits")
-    with pytest.raises(pp.PPError) as e:
-        g.eval_generated(2, pp.GEN_RANDOM, 1, 0, None, 0, 64)
-    assert e.value.code == -4
-
-
 def test_error_codes_match_oracle():
     base = synth.diamond()
     for bad, code in [(dict(base, edge_src=[0, 0, 1, 3], edge_dst=[1, 2, 3, 1]), -2),
