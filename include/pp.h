@@ -38,8 +38,9 @@ extern "C" {
                                 endpoint, duplicate/negative id      */
 #define PP_E_CYCLE      (-2) /* the DFG has a cycle; message names one cycle's ids  */
 #define PP_E_RANGE      (-3) /* a time bound ≥ 2^61 ps or a u128 product overflow   */
-#define PP_E_TOO_LARGE  (-4) /* GRAY space M^K > 2^63, or the DFG image / per-lane
-                                state does not fit in shared memory                 */
+#define PP_E_TOO_LARGE  (-4) /* GRAY space M^K > 2^63; K > 65535, W + 1 > 4096 or
+                                an image ≥ 2 GB; a hardware graph beyond the
+                                shared-memory tier (pp_dfg_get_tier)                */
 #define PP_E_INFEASIBLE (-5) /* every evaluated candidate violates device memory    */
 #define PP_E_CUDA       (-6) /* CUDA failure or no device                           */
 #define PP_E_NCCL       (-7) /* NCCL unavailable or failed                          */
