@@ -36,9 +36,12 @@ static KernelInfo info_np(int np, bool hw) {
     return info1<GEN, MEM, WA, F64, 1>(hw);
 }
 
+// The shared-memory tier runs the tagged-f64 arithmetic only: a DFG whose
+// time bound needs tagged u64 (≥ 2^49 ps) is placed on the global-state tier
+// at load time (loader.cpp), so f64 is always true here.
 template <int GEN, bool MEM, bool WA>
-static KernelInfo info_f(bool f64, int np, bool hw) {
-    return f64 ? info_np<GEN, MEM, WA, true>(np, hw) : info_np<GEN, MEM, WA, false>(np, hw);
+static KernelInfo info_f(bool, int np, bool hw) {
+    return info_np<GEN, MEM, WA, true>(np, hw);
 }
 
 template <int GEN>
@@ -59,8 +62,8 @@ static KernelInfo info_sym_np(int np) {
     return info2<GEN_SYM, MEM, false, F64, 1, false>();
 }
 template <bool MEM>
-static KernelInfo info_sym(bool f64, int np) {
-    return f64 ? info_sym_np<MEM, true>(np) : info_sym_np<MEM, false>(np);
+static KernelInfo info_sym(bool, int np) {
+    return info_sym_np<MEM, true>(np);
 }
 
 KernelInfo PP_CAT(kernel_for_m, PP_M)(int gen, bool mem, bool wa, bool f64, int np, bool hw) {

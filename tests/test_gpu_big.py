@@ -154,3 +154,20 @@ def test_forced_global_tier_gray(M, monkeypatch):
     space = min(M ** g.K, 60_000)
     r = pp.u64(g.search_range(M, pp.GEN_GRAY, 0, 0, None, 0, space))
     assert (int(r[0]), int(r[1])) == od.round(M, O.GEN_GRAY, 0, 0, None, 0, space)
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 4, 8])
+def test_u64_time_range_runs_global_tier(M):
+    """A DFG whose time bound is ≥ 2^49 ps needs the tagged-u64 arithmetic,
+    which only the global tier runs: every candidate and the
+    range argmin equal the oracle's."""
+    spec = synth.random_dag(4900 + M, 120, avg_deg=1.5, max_cost=10**15, max_bytes=10**9, bw=10**9)
+    g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
+    assert g.tier == pp.TIER_GLOBAL
+    assert od.t1 >= 1 << 49
+    base = np.random.default_rng(M).integers(0, M, size=g.K, dtype=np.uint8)
+    for gen, ogen in [(pp.GEN_RANDOM, O.GEN_RANDOM), (pp.GEN_PERTURB, O.GEN_PERTURB)]:
+        got = pp.u64(g.eval_generated(M, gen, 11, 64, base, 3, 300))
+        assert np.array_equal(got, _cands(od, M, ogen, 11, 64, base, range(3, 303))), gen
+        r = pp.u64(g.search_range(M, gen, 12, 64, base, 0, 5000))
+        assert (int(r[0]), int(r[1])) == od.round(M, ogen, 12, 64, base, 0, 5000)
