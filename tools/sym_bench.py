@@ -40,6 +40,9 @@ if __name__ == "__main__":
     cases = [("toy12", synth.toy12(), M) for M in (2, 3, 4)]
     r16 = synth.random_dag(1616, 16, avg_deg=1.6, max_cost=10**6, max_bytes=10**6)
     cases += [("random_K16", r16, M) for M in (2, 3, 4)]
+    # M = 2 spaces large enough that the launch is not latency-bound (2^24, 2^28)
+    for K in (24, 28):
+        cases.append((f"random_K{K}", synth.random_dag(1600 + K, K, avg_deg=1.6, max_cost=10**6, max_bytes=10**6), 2))
     for name, spec, M in cases:
         g = pp.Dfg(spec)
         K = g.K
