@@ -414,6 +414,14 @@ static bool use_sym(const pp_dfg *g, int M, int gen, uint64_t begin, uint64_t en
     return (unsigned __int128)end == space;
 }
 
+// M = 2: the classes are pairs {d, d̄} (all K digits complemented), and with
+// the reflected binary Gray code d = i ⊕ (i >> 1) the complement of d is the
+// placement of i ⊕ c, c = the inverse Gray code of all ones (bits K−1, K−3,
+// …).  c has bit K−1 set, so each class has exactly one index below 2^(K−1),
+// and it is the class's smaller one: the plain GRAY search over the lower
+// half [0, 2^(K−1)) returns the full search's (makespan, index) argmin at
+// half the work and without the RGS unranking.
+
 // Completion counts T_M[rem][m] = m·T_M[rem−1][m] + [m < M]·T_M[rem−1][m+1],
 // T_M[0][m] = 1, for every M, uploaded once per DFG.  Returns the number of
 // classes of M (= T_M[K−1][1]).
@@ -718,7 +726,9 @@ int pp_search_range(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
         g_launches++;
     }
     Launch L;
-    if (use_sym(g, M, gen, begin, end)) {   // the whole GRAY space: one placement per class
+    if (use_sym(g, M, gen, begin, end) && M == 2) {   // the lower half of the Gray space (half_gray_space)
+        if ((rc = setup(g, M, GEN_GRAY, false, 0, end / 2, L, stream))) return rc;
+    } else if (use_sym(g, M, gen, begin, end)) {   // the whole GRAY space: one placement per class
         uint64_t tasks = 0;
         int np = 0;
         if ((rc = sym_plan(g, M, &np, &tasks))) return rc;
@@ -863,6 +873,9 @@ int pp_search_exact(const pp_dfg *g, int M, int gen, uint64_t seed_r, uint32_t t
         set_error("invalid range or NULL buffer");
         return PP_E_INVALID;
     }
+    if (use_sym(g, M, gen, begin, end) && M == 2)   // the lower half of the Gray space (half_gray_space)
+        return run_exact(g, M, GEN_GRAY, seed_r, tau, d_base_pi, nullptr, 0, end / 2, node_limit, nullptr, nullptr,
+                         d_best, stream);
     if (use_sym(g, M, gen, begin, end)) {   // the whole GRAY space: one placement per class
         uint64_t classes = 0;
         if ((rc = rgs_table(g, M, &classes))) return rc;
@@ -1010,7 +1023,7 @@ int pp_pipeline_range(const pp_dfg *gc, int M, const uint32_t *micro, int nm, ui
     p.nm = (uint32_t)nm;
     p.overhead = overhead_ps;
     for (int j = 0; j < nm; j++) p.micro[j] = micro[j];
-    const int threads = 256;
+    const int threads = pipeline_block_threads(M);
     const uint64_t ranks = (end + nm - 1) / nm - begin / nm;
     uint64_t grid = (uint64_t)g->sm_count * 8;
     const uint64_t want = (ranks + threads - 1) / threads;
@@ -1019,7 +1032,7 @@ int pp_pipeline_range(const pp_dfg *gc, int M, const uint32_t *micro, int nm, ui
     if (grid > (uint64_t)kMaxGrid) grid = kMaxGrid;
     p.block = (ranks + grid * threads - 1) / (grid * threads);
     if (p.block < 1) p.block = 1;
-    rc = launch_pipeline(M, p, (int)grid, threads, stream);
+    rc = launch_pipeline(M, p, (int)grid, stream);
     g_launches++;
     if (rc) return cuda_err((cudaError_t)rc, "pipeline kernel launch");
     return PP_OK;
@@ -1153,8 +1166,9 @@ int pp_search_best(const pp_dfg *g, int M, const pp_search_desc *desc, pp_comm *
     g_launches++;
     // an exhaustive GRAY search runs over the relabelling classes (f1); its
     // winner is reported by Gray index, so the update is GRAY's
-    const bool sym = use_sym(g, M, desc->gen, 0, desc->count);
-    uint64_t space = desc->count;
+    const bool half = use_sym(g, M, desc->gen, 0, desc->count) && M == 2;   // half_gray_space
+    const bool sym = use_sym(g, M, desc->gen, 0, desc->count) && !half;
+    uint64_t space = half ? desc->count / 2 : desc->count;
     int sym_np = 0;
     if (sym && (rc = sym_plan(g, M, &sym_np, &space))) return rc;
     uint64_t begin = 0, end = 0;

@@ -216,7 +216,8 @@ struct PipeParams {
     uint32_t micro[16];
 };
 constexpr int kMaxPipelineK = 1024;
-int launch_pipeline(int M, const PipeParams &p, int grid, int threads, void *stream);
+int launch_pipeline(int M, const PipeParams &p, int grid, void *stream);
+int pipeline_block_threads(int M);   // 256, or 128 when M ≥ 5 (pair columns in shared memory)
 
 // per-warp branch-and-bound state of the exact kernel (shared memory)
 struct XWarp {

@@ -32,12 +32,46 @@ __device__ __forceinline__ bool plex_less(uint64_t m1, uint64_t i1, uint64_t m2,
     return m1 < m2 || (m1 == m2 && i1 < i2);
 }
 
+// Per-candidate stage-pair values (a < b): forward/backward bytes and their
+// per-micro-batch transfer costs.  M ≤ 4 keeps them in registers; M ≥ 5
+// (up to 28 pairs × 4 u64) in a per-thread shared-memory column
+// [value][pair][thread] after the binomial table, with 128-thread CTAs — in
+// registers they needed 255 registers and ~1 KB of spills at M = 8.
 template <int M>
-__global__ void __launch_bounds__(256) pipeline_kernel(const PipeParams P) {
-    extern __shared__ __align__(16) uint64_t binom[];   // [(K+1)·8]: C(n, k), k < 8
+constexpr bool kPairsInSmem = M >= 5;
+template <int M>
+constexpr int kPairs = M * (M - 1) / 2;
+template <int M>
+__host__ __device__ constexpr int pair_index(int a, int b) {   // a < b
+    return a * (2 * M - a - 1) / 2 + (b - a - 1);
+}
+template <int M>
+__host__ __device__ constexpr int pipeline_threads() { return kPairsInSmem<M> ? 128 : 256; }
+
+template <int M, bool SMEM = kPairsInSmem<M>>
+struct PairStore {
+    uint64_t v[4][kPairs<M> > 0 ? kPairs<M> : 1];
+    __device__ __forceinline__ void init(uint64_t *) {}
+    __device__ __forceinline__ uint64_t &operator()(int arr, int a, int b) { return v[arr][pair_index<M>(a, b)]; }
+};
+template <int M>
+struct PairStore<M, true> {
+    uint64_t *base;
+    __device__ __forceinline__ void init(uint64_t *col) { base = col; }
+    __device__ __forceinline__ uint64_t &operator()(int arr, int a, int b) {
+        return base[(uint32_t)(arr * kPairs<M> + pair_index<M>(a, b)) * pipeline_threads<M>()];
+    }
+};
+enum : int { kDf = 0, kDb = 1, kCf = 2, kCb = 3 };
+
+template <int M>
+__global__ void __launch_bounds__(pipeline_threads<M>()) pipeline_kernel(const PipeParams P) {
+    extern __shared__ __align__(16) uint64_t binom[];   // [(K+1)·8]: C(n, k), k < 8; then the pair columns
     __shared__ uint64_t red_mk[8], red_i[8];
     __shared__ bool is_last;
     const uint32_t K = P.K, K1 = P.K + 1;
+    PairStore<M> pv;
+    pv.init(binom + (size_t)K1 * 8 + threadIdx.x);
     for (uint32_t t = threadIdx.x; t < K1 * 8; t += blockDim.x) binom[t] = P.g_binom[t];
     __syncthreads();
 
@@ -78,30 +112,25 @@ __global__ void __launch_bounds__(256) pipeline_kernel(const PipeParams P) {
                 sb[s] = P.g_pb[st[s + 1]] - P.g_pb[st[s]];
                 if (P.cap && P.g_pm[st[s + 1]] - P.g_pm[st[s]] > P.cap) infeasible = true;
             }
-            // bytes and edge counts between stages (a < b)
-            uint64_t Df[M][M], Db[M][M];
-            bool has[M][M];
+            // bytes and edge counts between stages (a < b); has: bit a·8 + b
+            uint64_t has = 0;
 #pragma unroll
             for (int a = 0; a < M; a++)
 #pragma unroll
-                for (int b = 0; b < M; b++) {
-                    has[a][b] = false;
-                    Df[a][b] = Db[a][b] = 0;
-                    if (a < b) {
-                        has[a][b] = q2(P.g_qc, K1, st[a], st[a + 1], st[b], st[b + 1]) != 0;
-                        if (has[a][b]) {
-                            Df[a][b] = q2(P.g_qf, K1, st[a], st[a + 1], st[b], st[b + 1]);
-                            Db[a][b] = q2(P.g_qb, K1, st[a], st[a + 1], st[b], st[b + 1]);
-                        }
-                    }
+                for (int b = a + 1; b < M; b++) {
+                    const bool h = q2(P.g_qc, K1, st[a], st[a + 1], st[b], st[b + 1]) != 0;
+                    has |= (uint64_t)h << (a * 8 + b);
+                    pv(kDf, a, b) = h ? q2(P.g_qf, K1, st[a], st[a + 1], st[b], st[b + 1]) : 0;
+                    pv(kDb, a, b) = h ? q2(P.g_qb, K1, st[a], st[a + 1], st[b], st[b + 1]) : 0;
                 }
+            auto has_ab = [&](int a, int b) { return (has >> (a * 8 + b)) & 1; };
             for (uint32_t j = 0; j < nm; j++) {
                 const uint64_t idx = r * nm + j;
                 if (idx < P.begin || idx >= P.end) continue;
                 uint64_t mk = kInfeasible;
                 if (!infeasible) {
                     const uint64_t m = P.micro[j];
-                    uint64_t tf[M], tb[M], cf[M][M], cb[M][M];
+                    uint64_t tf[M], tb[M];
 #pragma unroll
                     for (int s = 0; s < M; s++) {
                         const uint64_t ov = (uint64_t)(st[s + 1] - st[s]) * P.overhead;
@@ -112,11 +141,10 @@ __global__ void __launch_bounds__(256) pipeline_kernel(const PipeParams P) {
 #pragma unroll
                     for (int a = 0; a < M; a++)
 #pragma unroll
-                        for (int b = 0; b < M; b++) {
-                            cf[a][b] = cb[a][b] = 0;
-                            if (a < b && has[a][b]) {
-                                cf[a][b] = (uint64_t)(((u128)Df[a][b] * 1000000000000ull + den - 1) / den) + P.lat;
-                                cb[a][b] = (uint64_t)(((u128)Db[a][b] * 1000000000000ull + den - 1) / den) + P.lat;
+                        for (int b = a + 1; b < M; b++) {
+                            if (has_ab(a, b)) {
+                                pv(kCf, a, b) = (uint64_t)(((u128)pv(kDf, a, b) * 1000000000000ull + den - 1) / den) + P.lat;
+                                pv(kCb, a, b) = (uint64_t)(((u128)pv(kDb, a, b) * 1000000000000ull + den - 1) / den) + P.lat;
                             }
                         }
                     uint64_t F[M], B[M];
@@ -128,7 +156,7 @@ __global__ void __launch_bounds__(256) pipeline_kernel(const PipeParams P) {
                             uint64_t v = F[s];                     // previous micro-batch on device s
 #pragma unroll
                             for (int a = 0; a < s; a++)
-                                if (has[a][s]) v = max(v, F[a] + cf[a][s]);
+                                if (has_ab(a, s)) v = max(v, F[a] + pv(kCf, a, s));
                             F[s] = v + tf[s];
                         }
                     }
@@ -140,7 +168,7 @@ __global__ void __launch_bounds__(256) pipeline_kernel(const PipeParams P) {
                             uint64_t v = B[s];
 #pragma unroll
                             for (int b = s + 1; b < M; b++)
-                                if (has[s][b]) v = max(v, B[b] + cb[s][b]);
+                                if (has_ab(s, b)) v = max(v, B[b] + pv(kCb, s, b));
                             B[s] = v + tb[s];
                         }
                     }
@@ -209,17 +237,33 @@ static int launch_m(const PipeParams &p, int grid, int threads, size_t smem, voi
     return (int)cudaGetLastError();
 }
 
-int launch_pipeline(int M, const PipeParams &p, int grid, int threads, void *stream) {
-    const size_t smem = (size_t)(p.K + 1) * 8 * sizeof(uint64_t);
+int pipeline_block_threads(int M) {
     switch (M) {
-        case 1: return launch_m<1>(p, grid, threads, smem, stream);
-        case 2: return launch_m<2>(p, grid, threads, smem, stream);
-        case 3: return launch_m<3>(p, grid, threads, smem, stream);
-        case 4: return launch_m<4>(p, grid, threads, smem, stream);
-        case 5: return launch_m<5>(p, grid, threads, smem, stream);
-        case 6: return launch_m<6>(p, grid, threads, smem, stream);
-        case 7: return launch_m<7>(p, grid, threads, smem, stream);
-        default: return launch_m<8>(p, grid, threads, smem, stream);
+        case 5: return pipeline_threads<5>();
+        case 6: return pipeline_threads<6>();
+        case 7: return pipeline_threads<7>();
+        case 8: return pipeline_threads<8>();
+        default: return pipeline_threads<1>();
+    }
+}
+
+template <int M>
+static int launch_m(const PipeParams &p, int grid, void *stream) {
+    const size_t smem = (size_t)(p.K + 1) * 8 * sizeof(uint64_t) +
+                        (kPairsInSmem<M> ? (size_t)4 * kPairs<M> * pipeline_threads<M>() * sizeof(uint64_t) : 0);
+    return launch_m<M>(p, grid, pipeline_threads<M>(), smem, stream);
+}
+
+int launch_pipeline(int M, const PipeParams &p, int grid, void *stream) {
+    switch (M) {
+        case 1: return launch_m<1>(p, grid, stream);
+        case 2: return launch_m<2>(p, grid, stream);
+        case 3: return launch_m<3>(p, grid, stream);
+        case 4: return launch_m<4>(p, grid, stream);
+        case 5: return launch_m<5>(p, grid, stream);
+        case 6: return launch_m<6>(p, grid, stream);
+        case 7: return launch_m<7>(p, grid, stream);
+        default: return launch_m<8>(p, grid, stream);
     }
 }
 

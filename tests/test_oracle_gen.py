@@ -203,3 +203,18 @@ def test_perturb_two_words_per_candidate():
     d = O.gen(16, 8, O.GEN_PERTURB, seed_r, 256, base8, 1)
     y = [(SM64_1ST >> (8 * j)) & 0xFF for j in range(8)] + [(SM64_2ND >> (8 * j)) & 0xFF for j in range(8)]
     assert [int(x) for x in d] == [int(base8[j]) ^ (y[j] % 8) for j in range(16)]
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 7, 12])
+def test_gray_m2_complement_pairs(K):
+    """The identity behind the M = 2 half-space exhaustive search (capi.cpp
+    half_gray_space): complementing every digit of GRAY
+    candidate i gives candidate i ^ c, c = bits K−1, K−3, …; c has bit K−1,
+    so every {d, d̄} class has exactly one index below 2^(K−1)."""
+    c = sum(1 << j for j in range(K - 1, -1, -2))
+    assert c >> (K - 1) == 1
+    for i in range(2 ** K):
+        d = O.gen(K, 2, O.GEN_GRAY, 0, 0, None, i)
+        dc = O.gen(K, 2, O.GEN_GRAY, 0, 0, None, i ^ c)
+        assert np.array_equal(dc, 1 - d)
+        assert (i < 2 ** (K - 1)) != ((i ^ c) < 2 ** (K - 1))
