@@ -37,7 +37,7 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     KernelInfo kernel_for_m##m(int gen, bool mem, bool wa, bool f64, int np, bool hw); \
     UpdateFn update_for_m##m(int gen);                                                 \
     XKernelInfo exact_for_m##m(int gen);                                              \
-    KernelInfo big_for_m##m(int gen);
+    KernelInfo big_for_m##m(int gen, bool f64);
 PP_DECL_M(1) PP_DECL_M(2) PP_DECL_M(3) PP_DECL_M(4) PP_DECL_M(5) PP_DECL_M(6) PP_DECL_M(7) PP_DECL_M(8)
 
 KernelInfo kernel_for(int M, int gen, bool mem, bool wa, bool f64, int np, bool hw) {
@@ -52,16 +52,16 @@ KernelInfo kernel_for(int M, int gen, bool mem, bool wa, bool f64, int np, bool 
         default: return kernel_for_m8(gen, mem, wa, f64, np, hw);
     }
 }
-KernelInfo big_kernel_for(int M, int gen) {
+KernelInfo big_kernel_for(int M, int gen, bool f64) {
     switch (M) {
-        case 1: return big_for_m1(gen);
-        case 2: return big_for_m2(gen);
-        case 3: return big_for_m3(gen);
-        case 4: return big_for_m4(gen);
-        case 5: return big_for_m5(gen);
-        case 6: return big_for_m6(gen);
-        case 7: return big_for_m7(gen);
-        default: return big_for_m8(gen);
+        case 1: return big_for_m1(gen, f64);
+        case 2: return big_for_m2(gen, f64);
+        case 3: return big_for_m3(gen, f64);
+        case 4: return big_for_m4(gen, f64);
+        case 5: return big_for_m5(gen, f64);
+        case 6: return big_for_m6(gen, f64);
+        case 7: return big_for_m7(gen, f64);
+        default: return big_for_m8(gen, f64);
     }
 }
 UpdateFn update_for(int M, int gen) {
@@ -235,7 +235,7 @@ static int setup_big(const pp_dfg *g, int M, int gen, bool write_all, uint64_t b
         set_error("symmetry-reduced search needs the shared-memory tier");
         return PP_E_TOO_LARGE;
     }
-    L.k = big_kernel_for(M, gen);
+    L.k = big_kernel_for(M, gen, g->f64);
     constexpr int kThreads = 256;
     const uint64_t region = ((uint64_t)g->W + 1 + (M > 2 ? (uint64_t)M : 0ull)) * kSlotUnit;
     int per_sm = 0;

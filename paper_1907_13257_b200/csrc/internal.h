@@ -297,8 +297,8 @@ struct KernelInfo {
 
 // search_inst.cu (compiled once per M with -DPP_M): kernel_for_m<M>(...)
 KernelInfo kernel_for(int M, int gen, bool mem, bool write_all, bool f64, int np, bool hw);
-// the global-state tier: one kernel per (M, generator), tagged-u64 arithmetic
-KernelInfo big_kernel_for(int M, int gen);
+// the global-state tier: one kernel per (M, generator, arithmetic)
+KernelInfo big_kernel_for(int M, int gen, bool f64);
 UpdateFn update_for(int M, int gen);
 
 }  // namespace pp

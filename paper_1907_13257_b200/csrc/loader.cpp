@@ -296,9 +296,9 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     // ---- tier: the shared-memory tier needs the image plus
     // at least 4 warps of lane state ((W + 1 + 8) slots × 256 B at one
     // placement per lane, M ≤ 8) within the SM's shared memory; otherwise the
-    // DFG runs on the global-state tier (search_big_kernel, tagged-u64
-    // arithmetic), as does a DFG whose time bound needs tagged u64 (≥ 2^49
-    // ps).  PP_TIER=global forces that tier (tests).
+    // DFG runs on the global-state tier (search_big_kernel), as does a DFG
+    // whose time bound needs tagged u64 (≥ 2^49 ps; the shared tier is built
+    // for tagged f64 only).  PP_TIER=global forces that tier (tests).
     size_t n_extra_all = 0;
     for (int s = 0; s < S; s++) n_extra_all += inputs[s].size() - 1;
     const size_t image_est = ((sizeof(OpRec) * S + sizeof(ExtraRec) * n_extra_all + 13ull * K8 + 15) & ~size_t(15));
@@ -309,7 +309,6 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     }
     if (!f64 && !hw) big = true;   // the shared tier is built for tagged f64 only
     if (big && hw) return fail(PP_E_TOO_LARGE, "hardware graphs need the shared-memory tier (image + 4 warps of lane state within 200 KB)");
-    if (big) f64 = false;
     auto enc = [&](uint64_t ps) -> uint64_t {
         if (!f64) return 8ull * ps;
         double x = (double)ps;   // exact: ps < 2^49

@@ -77,22 +77,21 @@ KernelInfo PP_CAT(kernel_for_m, PP_M)(int gen, bool mem, bool wa, bool f64, int 
     }
 }
 
-KernelInfo PP_CAT(big_for_m, PP_M)(int gen) {
+template <int GEN, bool F64>
+static KernelInfo big_info() {
+    return KernelInfo{&launch_search_big<PP_M, GEN, F64>,
+                      reinterpret_cast<const void *>(&search_big_kernel<PP_M, GEN, F64>)};
+}
+template <bool F64>
+static KernelInfo big_gen(int gen) {
     switch (gen) {
-        case GEN_GRAY:
-            return KernelInfo{&launch_search_big<PP_M, GEN_GRAY>,
-                              reinterpret_cast<const void *>(&search_big_kernel<PP_M, GEN_GRAY>)};
-        case GEN_RANDOM:
-            return KernelInfo{&launch_search_big<PP_M, GEN_RANDOM>,
-                              reinterpret_cast<const void *>(&search_big_kernel<PP_M, GEN_RANDOM>)};
-        case GEN_PERTURB:
-            return KernelInfo{&launch_search_big<PP_M, GEN_PERTURB>,
-                              reinterpret_cast<const void *>(&search_big_kernel<PP_M, GEN_PERTURB>)};
-        default:
-            return KernelInfo{&launch_search_big<PP_M, GEN_EXPLICIT>,
-                              reinterpret_cast<const void *>(&search_big_kernel<PP_M, GEN_EXPLICIT>)};
+        case GEN_GRAY: return big_info<GEN_GRAY, F64>();
+        case GEN_RANDOM: return big_info<GEN_RANDOM, F64>();
+        case GEN_PERTURB: return big_info<GEN_PERTURB, F64>();
+        default: return big_info<GEN_EXPLICIT, F64>();
     }
 }
+KernelInfo PP_CAT(big_for_m, PP_M)(int gen, bool f64) { return f64 ? big_gen<true>(gen) : big_gen<false>(gen); }
 
 UpdateFn PP_CAT(update_for_m, PP_M)(int gen) {
     switch (gen) {

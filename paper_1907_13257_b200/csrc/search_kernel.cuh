@@ -363,12 +363,16 @@ struct SmemSpace {
     static __device__ __forceinline__ uint4 rec(Addr a) { return lds128(a); }
     static __device__ __forceinline__ uint64_t ld(Addr a) { return lds64(a); }
     static __device__ __forceinline__ void st(Addr a, uint64_t v) { sts64(a, v); }
+    static __device__ __forceinline__ double ldd(Addr a) { return __longlong_as_double((long long)lds64(a)); }
+    static __device__ __forceinline__ void std(Addr a, double v) { sts64(a, (uint64_t)__double_as_longlong(v)); }
 };
 struct GmemSpace {
     typedef uint64_t Addr;
     static __device__ __forceinline__ uint4 rec(Addr a) { return __ldg(reinterpret_cast<const uint4 *>(a)); }
     static __device__ __forceinline__ uint64_t ld(Addr a) { return *reinterpret_cast<const uint64_t *>(a); }
     static __device__ __forceinline__ void st(Addr a, uint64_t v) { *reinterpret_cast<uint64_t *>(a) = v; }
+    static __device__ __forceinline__ double ldd(Addr a) { return *reinterpret_cast<const double *>(a); }
+    static __device__ __forceinline__ void std(Addr a, double v) { *reinterpret_cast<double *>(a) = v; }
 };
 
 // ---------------------------------------------------------- arithmetic
@@ -652,11 +656,13 @@ __device__ __forceinline__ double cut_add_f64(double v, uint32_t dev, double c, 
 // Hardware graph (HW): a record's cost field is the image offset of its cost
 // row; the transfer a → b costs row[cls[a][b]], class 0 (a = b) costing 0, so
 // an input is simply v + row[cls[tag(v)][dev]] (no cut flag needed).
-template <int M, int NP, bool MEM, bool HW, class Gen>
-__device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint32_t ops, uint32_t xr,
-                                             const uint64_t *__restrict__ mem, uint32_t lane, uint32_t free_off,
-                                             uint32_t K8, uint64_t cap, uint32_t khi, uint32_t cls,
+template <int M, int NP, bool MEM, bool HW, class Gen, class S = SmemSpace>
+__device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], typename S::Addr ops, typename S::Addr xr,
+                                             const uint64_t *__restrict__ mem, typename S::Addr lane,
+                                             uint32_t free_off, uint32_t K8, uint64_t cap, uint32_t khi, uint32_t cls,
                                              uint32_t hq = 0, uint32_t nslot = 0) {
+    typedef typename S::Addr Addr;
+    static_assert(!HW || std::is_same<S, SmemSpace>::value, "hardware graphs run on the shared tier");
     constexpr bool SM = M > 2;                    // free[] in shared memory
     // Gray prefix reuse (GEN_SYM): the lane's NP placements are
     // consecutive RGS ranks, identical on the first hq forward half-groups
@@ -675,19 +681,19 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
         if (MEM) mu[k].init();
         if (SM) {
 #pragma unroll
-            for (int d = 0; d < M; d++) std_(lane + free_off * NP + d * NP * 256 + k * 256, 0.0);
+            for (int d = 0; d < M; d++) S::std(lane + free_off * NP + d * NP * 256 + k * 256, 0.0);
         }
     }
-    auto fslot = [&](int k, uint32_t d) { return lane + free_off * NP + d * NP * 256 + k * 256; };
+    auto fslot = [&](int k, uint32_t d) -> Addr { return lane + free_off * NP + d * NP * 256 + k * 256; };
     auto hwc = [&](uint32_t row, uint32_t a, uint32_t b) {   // cost of a transfer a → b
-        return ldd(ops + row + 8 * lds8(cls + Dev<M>::canon(a) * 8 + Dev<M>::canon(b)));
+        return S::ldd(ops + row + 8 * lds8(cls + Dev<M>::canon(a) * 8 + Dev<M>::canon(b)));
     };
-    uint32_t x = xr;
+    Addr x = xr;
 
-    auto step = [&](auto KNc, uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
+    auto step = [&](auto KNc, Addr rec, uint32_t p, uint32_t c, bool fwd) {
         constexpr int KN = decltype(KNc)::value;   // placements 0..KN−1 (KN < NP: the shared prefix)
-        const uint4 a = lds128(rec);
-        const uint4 b = lds128(rec + 16);
+        const uint4 a = S::rec(rec);
+        const uint4 b = S::rec(rec + 16);
         const double cost = __hiloint2double((int)a.y, (int)a.x);
         const double c0 = __hiloint2double((int)a.w, (int)a.z);
         uint32_t dev[NP];
@@ -706,8 +712,8 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
                     // free[dev] is exact across a cut; without one it is
                     // free[pdev]'s stale shared copy, ≤ prev ≤ t, so the max
                     // is t either way and no cut factor is needed
-                    f = ldd(fslot(k, dev[k]));
-                    std_(fslot(k, pdev[k]), prev[k]);
+                    f = S::ldd(fslot(k, dev[k]));
+                    S::std(fslot(k, pdev[k]), prev[k]);
                 } else {
                     f = __dmul_rn(cut, oth[k]);
                     oth[k] = __fma_rn(cut, __dadd_rn(prev[k], -oth[k]), oth[k]);   // cut ? prev : oth
@@ -725,7 +731,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
             } else {
 #pragma unroll
                 for (int k = 0; k < KN; k++) {
-                    const double v = ldd(lane + b.x * NP + k * 256);
+                    const double v = S::ldd(lane + b.x * NP + k * 256);
                     r[k] = HW ? __dadd_rn(v, hwc(a.z, (uint32_t)__double2loint(v) & 7u, dev[k]))
                               : cut_add_f64<M>(v, dev[k], c0, khi);
                 }
@@ -733,12 +739,12 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
             const uint32_t nx = b.z & 0xFFFFu;
 #pragma unroll 1
             for (uint32_t q = 0; q < nx; q++) {   // further inputs (uniform trip count)
-                const uint4 e = lds128(x);
+                const uint4 e = S::rec(x);
                 x += sizeof(ExtraRec);
                 const double ce = __hiloint2double((int)e.y, (int)e.x);
 #pragma unroll
                 for (int k = 0; k < KN; k++) {
-                    const double v = ldd(lane + e.z * NP + k * 256);
+                    const double v = S::ldd(lane + e.z * NP + k * 256);
                     r[k] = dmax(r[k], HW ? __dadd_rn(v, hwc(e.x, (uint32_t)__double2loint(v) & 7u, dev[k]))
                                          : cut_add_f64<M>(v, dev[k], ce, khi));
                 }
@@ -749,8 +755,8 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
                 const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
                 double f;
                 if (SM) {
-                    f = __fma_rn(cut, __dadd_rn(ldd(fslot(k, dev[k])), -prev[k]), prev[k]);
-                    std_(fslot(k, pdev[k]), prev[k]);
+                    f = __fma_rn(cut, __dadd_rn(S::ldd(fslot(k, dev[k])), -prev[k]), prev[k]);
+                    S::std(fslot(k, pdev[k]), prev[k]);
                 } else {
                     const double d = __dadd_rn(prev[k], -oth[k]);
                     f = __fma_rn(-cut, d, prev[k]);
@@ -762,7 +768,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
         }
         if (b.y != kNoStore) {
 #pragma unroll
-            for (int k = 0; k < KN; k++) std_(lane + b.y * NP + k * 256, with_tag(prev[k], Dev<M>::canon(dev[k])));
+            for (int k = 0; k < KN; k++) S::std(lane + b.y * NP + k * 256, with_tag(prev[k], Dev<M>::canon(dev[k])));
         }
         if (MEM && fwd) {
             const uint64_t m = mem[p];
@@ -782,7 +788,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
             const uint32_t g = hg >> 1, h = hg & 1;
             if (h == 0) gen.refresh(g);
             gen.sub(h);
-            const uint32_t rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
+            const Addr rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
 #pragma unroll
             for (uint32_t cc = 0; cc < 4; cc++)
                 step(One{}, rec + cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, true);
@@ -796,16 +802,16 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
                 if (MEM) mu[k] = mu[0];
             }
             for (uint32_t sl = 0; sl < nslot; sl++) {
-                const double v = ldd(lane + sl * NP * 256);
+                const double v = S::ldd(lane + sl * NP * 256);
 #pragma unroll
-                for (int k = 1; k < NP; k++) std_(lane + sl * NP * 256 + k * 256, v);
+                for (int k = 1; k < NP; k++) S::std(lane + sl * NP * 256 + k * 256, v);
             }
             if (SM) {
 #pragma unroll
                 for (int d = 0; d < M; d++) {
-                    const double v = ldd(fslot(0, d));
+                    const double v = S::ldd(fslot(0, d));
 #pragma unroll
-                    for (int k = 1; k < NP; k++) std_(fslot(k, d), v);
+                    for (int k = 1; k < NP; k++) S::std(fslot(k, d), v);
                 }
             }
         }
@@ -818,7 +824,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
         for (uint32_t h = 0; h < 2; h++) {
             if (kPrefix && g == g0 && h < h0) continue;
             gen.sub(h);
-            const uint32_t rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
+            const Addr rec = ops + (g * 8 + h * 4) * (uint32_t)sizeof(OpRec);
 #pragma unroll
             for (uint32_t cc = 0; cc < 4; cc++)
                 step(All{}, rec + cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, true);
@@ -829,10 +835,10 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
 #pragma unroll (kHalfUnroll)
         for (uint32_t h = 2; h-- > 0;) {
             gen.sub(h);
-            const uint32_t rec = ops + (2 * K8 - 1 - g * 8 - h * 4) * (uint32_t)sizeof(OpRec);
+            const Addr rec = ops + (2 * K8 - 1 - g * 8 - h * 4) * (uint32_t)sizeof(OpRec);
 #pragma unroll
             for (int cc = 3; cc >= 0; cc--)
-                step(All{}, rec - (uint32_t)cc * (uint32_t)sizeof(OpRec), g * 8 + h * 4 + cc, cc, false);
+                step(All{}, rec - (Addr)cc * (Addr)sizeof(OpRec), g * 8 + h * 4 + cc, cc, false);
         }
     }
 #pragma unroll
@@ -840,7 +846,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], uint3
         double v = prev[k];
         if (SM) {
 #pragma unroll
-            for (int d = 0; d < M; d++) v = dmax(v, ldd(fslot(k, d)));   // stale free[pdev] ≤ prev
+            for (int d = 0; d < M; d++) v = dmax(v, S::ldd(fslot(k, d)));   // stale free[pdev] ≤ prev
         } else {
             v = dmax(v, oth[k]);
         }
@@ -1510,18 +1516,30 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
 }
 
 // ------------------------------------------------- global-state tier
+// the schedule body of the global tier: schedule_f64 when the image is
+// f64-encoded (time bound < 2^49 ps) and M ≥ 2, else schedule_gen
+template <int M, bool F64, class Gen>
+__device__ __forceinline__ void big_schedule(Gen &g, uint64_t (&mk)[1], uint64_t ops, uint64_t xr,
+                                             const uint64_t *__restrict__ mem, uint64_t lane, const KParams &P,
+                                             uint64_t cap) {
+    if constexpr (F64 && M >= 2)
+        schedule_f64<M, 1, true, false, Gen, GmemSpace>(g, mk, ops, xr, mem, lane, P.free_off, P.K8, cap, P.one_hi, 0);
+    else
+        schedule_gen<M, 1, true, F64, Gen, GmemSpace>(g, mk, ops, xr, mem, lane, P.free_off, P.K8, cap);
+}
+
 // DFGs whose image exceeds the shared-memory budget, or whose per-lane state
 // ((W + 1 + M) slots) leaves fewer than 4 resident warps per SM, run here
 // (pp_dfg::big, decided at load time).  The recurrence is
-// schedule_gen's, operation for operation, on the tagged-u64 arithmetic (the
-// loader encodes such images in u64); only the memory space differs: records
+// schedule_f64's (f64-encoded image) or schedule_gen's (tagged u64, time bound
+// ≥ 2^49 ps), operation for operation; only the memory space differs: records
 // are read from the HBM image through the read-only path (every warp reads the
 // same records, so they stay L1/L2-resident), and the lane state is a warp
 // region of the global scratch P.g_state laid out [slot][lane] like the
 // shared one.  One placement per lane; the memory cap is a runtime value
 // (UINT64_MAX when absent) and the per-candidate output a runtime mode
 // (P.g_makespan ≠ nullptr), so one kernel per (M, generator).
-template <int M, int GEN>
+template <int M, int GEN, bool F64>
 __global__ void __launch_bounds__(256) search_big_kernel(const KParams P) {
     __shared__ uint64_t red_mk[32], red_i[32];
     __shared__ bool is_last;
@@ -1557,25 +1575,21 @@ __global__ void __launch_bounds__(256) search_big_kernel(const KParams P) {
             GrayGen<M, 1> g;
             const uint64_t ii[1] = {idx};
             g.init(ii, P.K);
-            schedule_gen<M, 1, true, false, GrayGen<M, 1>, GmemSpace>(g, mk, ops, xr, mem, lane_region, P.free_off,
-                                                                       P.K8, cap);
+            big_schedule<M, F64>(g, mk, ops, xr, mem, lane_region, P, cap);
         } else if constexpr (GEN == GEN_RANDOM) {
             RandomGen<M, 1> g;
             g.init(i0, P.seed, P.K);
-            schedule_gen<M, 1, true, false, RandomGen<M, 1>, GmemSpace>(g, mk, ops, xr, mem, lane_region,
-                                                                         P.free_off, P.K8, cap);
+            big_schedule<M, F64>(g, mk, ops, xr, mem, lane_region, P, cap);
         } else if constexpr (GEN == GEN_PERTURB) {
             PerturbGen<M, 1> g;
             g.init(i0, P.seed, P.K, P.tau);
-            schedule_gen<M, 1, true, false, PerturbGen<M, 1>, GmemSpace>(g, mk, ops, xr, mem, lane_region,
-                                                                          P.free_off, P.K8, cap);
+            big_schedule<M, F64>(g, mk, ops, xr, mem, lane_region, P, cap);
         } else {
             ExplicitGen<M, 1> g;
             g.row[0] = P.g_place + (idx - P.begin) * (uint64_t)P.K;
             g.bad[0] = 0;
             g.orig = orig;
-            schedule_gen<M, 1, true, false, ExplicitGen<M, 1>, GmemSpace>(g, mk, ops, xr, mem, lane_region,
-                                                                           P.free_off, P.K8, cap);
+            big_schedule<M, F64>(g, mk, ops, xr, mem, lane_region, P, cap);
             if (g.bad[0]) mk[0] = kInfeasible;
         }
         if (write_all) {
@@ -1590,9 +1604,9 @@ __global__ void __launch_bounds__(256) search_big_kernel(const KParams P) {
     grid_argmin(P, best_mk, best_i, red_mk, red_i, is_last);
 }
 
-template <int M, int GEN>
+template <int M, int GEN, bool F64>
 int launch_search_big(const KParams &p, int grid, int threads, int smem, void *stream) {
-    search_big_kernel<M, GEN><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
+    search_big_kernel<M, GEN, F64><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
     return (int)cudaGetLastError();
 }
 
