@@ -237,7 +237,7 @@ static int setup_big(const pp_dfg *g, int M, int gen, bool write_all, uint64_t b
     }
     L.k = big_kernel_for(M, gen, g->f64);
     constexpr int kThreads = 256;
-    const uint64_t region = ((uint64_t)g->W + 1 + (M > 2 ? (uint64_t)M : 0ull)) * kSlotUnit;
+    const uint64_t region = ((uint64_t)g->W + 1 + (M > 2 ? (uint64_t)M : 0ull)) * kSlotUnit * big_np(M);
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.k.func, kThreads, 0);
     if (e != cudaSuccess) return cuda_err(e, "occupancy");
@@ -248,7 +248,7 @@ static int setup_big(const pp_dfg *g, int M, int gen, bool write_all, uint64_t b
     const uint64_t fit = budget / (region * (kThreads / 32) * (uint64_t)g->sm_count);
     per_sm = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)std::max(per_sm, 1), fit));
     const uint64_t n = end - begin;
-    const uint64_t tiles = (n + 31) / 32;
+    const uint64_t tiles = (n + 32 * big_np(M) - 1) / (32 * big_np(M));
     uint64_t grid = std::min<uint64_t>((uint64_t)per_sm * g->sm_count, (tiles + kThreads / 32 - 1) / (kThreads / 32));
     grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, kMaxGrid));
     const size_t need = (size_t)grid * (kThreads / 32) * region;
@@ -263,10 +263,10 @@ static int setup_big(const pp_dfg *g, int M, int gen, bool write_all, uint64_t b
     L.threads = kThreads;
     L.grid = (int)grid;
     L.smem = 0;
-    L.np = 1;
+    L.np = big_np(M);
     Choice c;
     c.k = L.k;
-    c.np = 1;
+    c.np = big_np(M);
     c.threads = kThreads;
     c.ctas = per_sm;
     c.region = (uint32_t)region;

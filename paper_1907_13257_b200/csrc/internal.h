@@ -297,7 +297,12 @@ struct KernelInfo {
 
 // search_inst.cu (compiled once per M with -DPP_M): kernel_for_m<M>(...)
 KernelInfo kernel_for(int M, int gen, bool mem, bool write_all, bool f64, int np, bool hw);
-// the global-state tier: one kernel per (M, generator, arithmetic)
+// the global-state tier: one kernel per (M, generator, arithmetic), big_np(M)
+// placements per lane
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr int big_np(int M) { return M <= 2 ? 2 : 1; }
 KernelInfo big_kernel_for(int M, int gen, bool f64);
 UpdateFn update_for(int M, int gen);
 

@@ -1518,29 +1518,24 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
 // ------------------------------------------------- global-state tier
 // the schedule body of the global tier: schedule_f64 when the image is
 // f64-encoded (time bound < 2^49 ps) and M ≥ 2, else schedule_gen
-template <int M, bool F64, class Gen>
-__device__ __forceinline__ void big_schedule(Gen &g, uint64_t (&mk)[1], uint64_t ops, uint64_t xr,
+// placements per lane on the global tier: big_np(M) (internal.h; A/B in
+// profiles/r02_big_bench_np.txt: NP = 2 is faster at M ≤ 2, NP = 1 at M ≥ 3,
+// where NP = 2 needs 122–128 registers and halves the resident warps)
+template <int M, bool F64, int NP, class Gen>
+__device__ __forceinline__ void big_schedule(Gen &g, uint64_t (&mk)[NP], uint64_t ops, uint64_t xr,
                                              const uint64_t *__restrict__ mem, uint64_t lane, const KParams &P,
                                              uint64_t cap) {
     if constexpr (F64 && M >= 2)
-        schedule_f64<M, 1, true, false, Gen, GmemSpace>(g, mk, ops, xr, mem, lane, P.free_off, P.K8, cap, P.one_hi, 0);
+        schedule_f64<M, NP, true, false, Gen, GmemSpace>(g, mk, ops, xr, mem, lane, P.free_off, P.K8, cap, P.one_hi,
+                                                         0);
     else
-        schedule_gen<M, 1, true, F64, Gen, GmemSpace>(g, mk, ops, xr, mem, lane, P.free_off, P.K8, cap);
+        schedule_gen<M, NP, true, F64, Gen, GmemSpace>(g, mk, ops, xr, mem, lane, P.free_off, P.K8, cap);
 }
 
-// DFGs whose image exceeds the shared-memory budget, or whose per-lane state
-// ((W + 1 + M) slots) leaves fewer than 4 resident warps per SM, run here
-// (pp_dfg::big, decided at load time).  The recurrence is
-// schedule_f64's (f64-encoded image) or schedule_gen's (tagged u64, time bound
-// ≥ 2^49 ps), operation for operation; only the memory space differs: records
-// are read from the HBM image through the read-only path (every warp reads the
-// same records, so they stay L1/L2-resident), and the lane state is a warp
-// region of the global scratch P.g_state laid out [slot][lane] like the
-// shared one.  One placement per lane; the memory cap is a runtime value
-// (UINT64_MAX when absent) and the per-candidate output a runtime mode
-// (P.g_makespan ≠ nullptr), so one kernel per (M, generator).
 template <int M, int GEN, bool F64>
 __global__ void __launch_bounds__(256) search_big_kernel(const KParams P) {
+    constexpr int NP = big_np(M);
+    constexpr uint32_t TILE = 32 * NP;
     __shared__ uint64_t red_mk[32], red_i[32];
     __shared__ bool is_last;
     const uint32_t tid = threadIdx.x;
@@ -1554,11 +1549,13 @@ __global__ void __launch_bounds__(256) search_big_kernel(const KParams P) {
     const uint32_t *orig = reinterpret_cast<const uint32_t *>(P.g_image + P.off_orig);
     const uint64_t lane_region =
         reinterpret_cast<uint64_t>(P.g_state) + (blockIdx.x * wpb + warp) * (uint64_t)P.region_bytes + lane * 8u;
-    *reinterpret_cast<uint64_t *>(lane_region + P.zero_off) = 0;   // the always-zero slot
+#pragma unroll
+    for (int k = 0; k < NP; k++)   // the always-zero slot
+        *reinterpret_cast<uint64_t *>(lane_region + P.zero_off * NP + k * 256) = 0;
 
     uint64_t best_mk = kInfeasible, best_i = kInfeasible;
     const uint64_t n = P.end - P.begin;
-    const uint64_t ntiles = (n + 31) / 32;
+    const uint64_t ntiles = (n + TILE - 1) / TILE;
     auto claim = [&]() -> uint64_t {
         unsigned long long v = 0;
         if (lane == 0) v = atomicAdd(P.g_tile, 1ull);
@@ -1566,44 +1563,56 @@ __global__ void __launch_bounds__(256) search_big_kernel(const KParams P) {
     };
     uint64_t tile = write_all ? blockIdx.x * wpb + warp : claim();
     while (tile < ntiles) {
-        const uint64_t off = tile * 32 + lane;
-        const bool valid = off < n;
-        const uint64_t idx = P.begin + (valid ? off : n - 1);
-        const uint64_t i0 = P.begin + tile * 32 + lane;
-        uint64_t mk[1];
-        if constexpr (GEN == GEN_GRAY) {
-            GrayGen<M, 1> g;
-            const uint64_t ii[1] = {idx};
-            g.init(ii, P.K);
-            big_schedule<M, F64>(g, mk, ops, xr, mem, lane_region, P, cap);
-        } else if constexpr (GEN == GEN_RANDOM) {
-            RandomGen<M, 1> g;
-            g.init(i0, P.seed, P.K);
-            big_schedule<M, F64>(g, mk, ops, xr, mem, lane_region, P, cap);
-        } else if constexpr (GEN == GEN_PERTURB) {
-            PerturbGen<M, 1> g;
-            g.init(i0, P.seed, P.K, P.tau);
-            big_schedule<M, F64>(g, mk, ops, xr, mem, lane_region, P, cap);
-        } else {
-            ExplicitGen<M, 1> g;
-            g.row[0] = P.g_place + (idx - P.begin) * (uint64_t)P.K;
-            g.bad[0] = 0;
-            g.orig = orig;
-            big_schedule<M, F64>(g, mk, ops, xr, mem, lane_region, P, cap);
-            if (g.bad[0]) mk[0] = kInfeasible;
+        // the lane's placements i_0 + 32k (search_kernel's layout)
+        uint64_t off[NP], idx[NP];
+        bool valid[NP];
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            off[k] = tile * TILE + k * 32 + lane;
+            valid[k] = off[k] < n;
+            idx[k] = P.begin + (valid[k] ? off[k] : n - 1);
         }
-        if (write_all) {
-            if (valid) P.g_makespan[off] = mk[0];
-        } else if (valid && lex_less(mk[0], idx, best_mk, best_i)) {
-            best_mk = mk[0];
-            best_i = idx;
+        const uint64_t i0 = P.begin + tile * TILE + lane;
+        uint64_t mk[NP];
+        if constexpr (GEN == GEN_GRAY) {
+            GrayGen<M, NP> g;
+            g.init(idx, P.K);
+            big_schedule<M, F64, NP>(g, mk, ops, xr, mem, lane_region, P, cap);
+        } else if constexpr (GEN == GEN_RANDOM) {
+            RandomGen<M, NP> g;
+            g.init(i0, P.seed, P.K);
+            big_schedule<M, F64, NP>(g, mk, ops, xr, mem, lane_region, P, cap);
+        } else if constexpr (GEN == GEN_PERTURB) {
+            PerturbGen<M, NP> g;
+            g.init(i0, P.seed, P.K, P.tau);
+            big_schedule<M, F64, NP>(g, mk, ops, xr, mem, lane_region, P, cap);
+        } else {
+            ExplicitGen<M, NP> g;
+#pragma unroll
+            for (int k = 0; k < NP; k++) {
+                g.row[k] = P.g_place + (idx[k] - P.begin) * (uint64_t)P.K;
+                g.bad[k] = 0;
+            }
+            g.orig = orig;
+            big_schedule<M, F64, NP>(g, mk, ops, xr, mem, lane_region, P, cap);
+#pragma unroll
+            for (int k = 0; k < NP; k++)
+                if (g.bad[k]) mk[k] = kInfeasible;
+        }
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            if (write_all) {
+                if (valid[k]) P.g_makespan[off[k]] = mk[k];
+            } else if (valid[k] && lex_less(mk[k], idx[k], best_mk, best_i)) {
+                best_mk = mk[k];
+                best_i = idx[k];
+            }
         }
         tile = write_all ? tile + (uint64_t)gridDim.x * wpb : claim();
     }
     if (write_all) return;
     grid_argmin(P, best_mk, best_i, red_mk, red_i, is_last);
 }
-
 template <int M, int GEN, bool F64>
 int launch_search_big(const KParams &p, int grid, int threads, int smem, void *stream) {
     search_big_kernel<M, GEN, F64><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
