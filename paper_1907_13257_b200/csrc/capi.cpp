@@ -225,8 +225,8 @@ static void fill(const pp_dfg *g, const Choice &best, uint64_t begin, uint64_t e
 // depends on the choice (every variant is bit-exact), only the speed.
 // The per-candidate (write-all) kernels are built for NP = 2 only.
 // The global-state tier (pp_dfg::big): search_big_kernel with
-// 256-thread CTAs, one placement per lane, and a warp region of
-// (W + 1 + M) slots × 256 B in the DFG's global scratch.  The kernel uses no
+// 256-thread CTAs, big_np(M) placements per lane, and a warp region of
+// (W + 1 + M) slots × 256 B × big_np(M) in the DFG's global scratch.  The kernel uses no
 // shared memory beyond its argmin scratch, so the L1 carve-out is maximal.
 // Resident warps: the occupancy limit, unless the live state of all warps
 // would exceed PP_BIG_STATE_MB (default 4096) of scratch.
@@ -253,7 +253,7 @@ static int setup_big(const pp_dfg *g, int M, int gen, bool write_all, uint64_t b
     grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, kMaxGrid));
     const size_t need = (size_t)grid * (kThreads / 32) * region;
     pp_dfg *mg = const_cast<pp_dfg *>(g);
-    if (need > mg->state_bytes) {   // stream-ordered like every other per-DFG buffer
+    if (need > mg->state_bytes) {   // grown on demand; cudaFree synchronises the device first
         if (mg->d_state) cudaFree(mg->d_state);
         mg->d_state = nullptr;
         mg->state_bytes = 0;

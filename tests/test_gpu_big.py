@@ -171,3 +171,19 @@ def test_u64_time_range_runs_global_tier(M):
         assert np.array_equal(got, _cands(od, M, ogen, 11, 64, base, range(3, 303))), gen
         r = pp.u64(g.search_range(M, gen, 12, 64, base, 0, 5000))
         assert (int(r[0]), int(r[1])) == od.round(M, ogen, 12, 64, base, 0, 5000)
+
+
+def test_forced_global_tier_other_entry_points(monkeypatch):
+    """The exact search (its in-order incumbent runs on the global tier), the
+    EFT seed and the GPipe search of a DFG loaded on the global tier equal the
+    oracle's."""
+    monkeypatch.setenv("PP_TIER", "global")
+    spec = synth.toy12()
+    g, od = pp.Dfg(spec), O.Dfg.from_spec(spec)
+    assert g.tier == pp.TIER_GLOBAL
+    for M, end in ((2, 600), (3, 400)):
+        ex = g.search_exact(M, pp.GEN_GRAY, 0, 0, None, 0, end)
+        assert ex[:2] == od.round_exact(M, O.GEN_GRAY, 0, 0, None, 0, end), M
+        assert np.array_equal(g.eft_place(M), od.eft(M))
+        pr = g.pipeline_search(M, [1, 2, 4])
+        assert (pr["makespan_ps"], pr["index"]) == od.pipeline_search(M, [1, 2, 4])
