@@ -648,9 +648,20 @@ __device__ __forceinline__ uint32_t cut_bit(uint32_t a, uint32_t b) {   // 1 iff
     return (M == 2) ? ((a ^ b) & 1u) : (uint32_t)(((a ^ b) & 7u) != 0);
 }
 // v + [tag(v) ≠ dev]·c for a tagged slot value
+// 1.0 iff devices a and b differ, else 0.0.  M = 2: (a ⊕ b) & 1 times the
+// high word of 1.0 (LOP3 + IMAD); M ≥ 3: a select on the 3-bit compare
+// (LOP3 with a predicate + SEL; PP_CUT_SEL=0 keeps the 0/1 multiply, A/B)
+#ifndef PP_CUT_SEL
+#define PP_CUT_SEL 1
+#endif
+template <int M>
+__device__ __forceinline__ double cut_one(uint32_t a, uint32_t b, uint32_t khi) {
+    if (M == 2 || !PP_CUT_SEL) return one_if(cut_bit<M>(a, b), khi);
+    return __hiloint2double((int)((((a ^ b) & 7u) != 0) ? khi : 0u), 0);
+}
 template <int M>
 __device__ __forceinline__ double cut_add_f64(double v, uint32_t dev, double c, uint32_t khi) {
-    return __fma_rn(c, one_if(cut_bit<M>((uint32_t)__double2loint(v), dev), khi), v);
+    return __fma_rn(c, cut_one<M>((uint32_t)__double2loint(v), dev, khi), v);
 }
 
 // Hardware graph (HW): a record's cost field is the image offset of its cost
@@ -705,7 +716,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], typen
             for (int k = 0; k < KN; k++) {
                 // free[dev] matters only across a cut (else it is prev, and
                 // cut·free = 0 ≤ prev): s = max(prev + cut·c0, cut·free[dev])
-                const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
+                const double cut = cut_one<M>(pdev[k], dev[k], khi);
                 const double t = HW ? __dadd_rn(prev[k], hwc(a.z, pdev[k], dev[k])) : __fma_rn(c0, cut, prev[k]);
                 double f;
                 if (SM) {
@@ -727,7 +738,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], typen
 #pragma unroll
                 for (int k = 0; k < KN; k++)
                     r[k] = HW ? __dadd_rn(prev[k], hwc(a.z, pdev[k], dev[k]))
-                              : __fma_rn(c0, one_if(cut_bit<M>(pdev[k], dev[k]), khi), prev[k]);
+                              : __fma_rn(c0, cut_one<M>(pdev[k], dev[k], khi), prev[k]);
             } else {
 #pragma unroll
                 for (int k = 0; k < KN; k++) {
@@ -752,7 +763,7 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], typen
 #pragma unroll
             for (int k = 0; k < KN; k++) {
                 // free[dev] = cut ? other : prev, exact on the FP64 pipe
-                const double cut = one_if(cut_bit<M>(pdev[k], dev[k]), khi);
+                const double cut = cut_one<M>(pdev[k], dev[k], khi);
                 double f;
                 if (SM) {
                     f = __fma_rn(cut, __dadd_rn(S::ldd(fslot(k, dev[k])), -prev[k]), prev[k]);
