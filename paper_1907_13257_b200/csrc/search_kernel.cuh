@@ -365,6 +365,11 @@ struct SmemSpace {
     static __device__ __forceinline__ void st(Addr a, uint64_t v) { sts64(a, v); }
     static __device__ __forceinline__ double ldd(Addr a) { return __longlong_as_double((long long)lds64(a)); }
     static __device__ __forceinline__ void std(Addr a, double v) { sts64(a, (uint64_t)__double_as_longlong(v)); }
+    static __device__ __forceinline__ uint32_t ld32(Addr a) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+        return v;
+    }
 };
 struct GmemSpace {
     typedef uint64_t Addr;
@@ -373,7 +378,16 @@ struct GmemSpace {
     static __device__ __forceinline__ void st(Addr a, uint64_t v) { *reinterpret_cast<uint64_t *>(a) = v; }
     static __device__ __forceinline__ double ldd(Addr a) { return *reinterpret_cast<const double *>(a); }
     static __device__ __forceinline__ void std(Addr a, double v) { *reinterpret_cast<double *>(a) = v; }
+    static __device__ __forceinline__ uint32_t ld32(Addr a) { return __ldg(reinterpret_cast<const uint32_t *>(a)); }
 };
+// An extra input's record by one LDS.128 (default) or by two loads, its cost
+// as an aligned double (LDS.64) and its slot offset (LDS.32), which saves the
+// two register moves into an aligned pair (PP_EXTRA_SPLIT=1).  A/B
+// (profiles/r02_ab_extra.txt): M = 2 ±0.3%, GNMT M = 4 +0.25%, Inception
+// M = 4 −1.0%, so not adopted.
+#ifndef PP_EXTRA_SPLIT
+#define PP_EXTRA_SPLIT 0
+#endif
 
 // ---------------------------------------------------------- arithmetic
 // Two exact representations of a tagged finish time (internal.h):
@@ -750,13 +764,23 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], typen
             const uint32_t nx = b.z & 0xFFFFu;
 #pragma unroll 1
             for (uint32_t q = 0; q < nx; q++) {   // further inputs (uniform trip count)
-                const uint4 e = S::rec(x);
+                double ce;
+                uint32_t ex, ez;
+                if (PP_EXTRA_SPLIT && !HW) {
+                    ce = S::ldd(x);
+                    ez = S::ld32(x + 8);
+                    ex = 0;
+                } else {
+                    const uint4 e = S::rec(x);
+                    ce = __hiloint2double((int)e.y, (int)e.x);
+                    ex = e.x;
+                    ez = e.z;
+                }
                 x += sizeof(ExtraRec);
-                const double ce = __hiloint2double((int)e.y, (int)e.x);
 #pragma unroll
                 for (int k = 0; k < KN; k++) {
-                    const double v = S::ldd(lane + e.z * NP + k * 256);
-                    r[k] = dmax(r[k], HW ? __dadd_rn(v, hwc(e.x, (uint32_t)__double2loint(v) & 7u, dev[k]))
+                    const double v = S::ldd(lane + ez * NP + k * 256);
+                    r[k] = dmax(r[k], HW ? __dadd_rn(v, hwc(ex, (uint32_t)__double2loint(v) & 7u, dev[k]))
                                          : cut_add_f64<M>(v, dev[k], ce, khi));
                 }
             }
@@ -1026,12 +1050,20 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
             const uint32_t nx = b.z & 0xFFFFu;
 #pragma unroll 1
             for (uint32_t q = 0; q < nx; q++) {   // further inputs (uniform trip count)
-                const uint4 e = lds128(x);
+                double ce;
+                uint32_t ez;
+                if (PP_EXTRA_SPLIT) {
+                    ce = ldd(x);
+                    ez = lds32(x + 8);
+                } else {
+                    const uint4 e = lds128(x);
+                    ce = __hiloint2double((int)e.y, (int)e.x);
+                    ez = e.z;
+                }
                 x += sizeof(ExtraRec);
-                const double ce = __hiloint2double((int)e.y, (int)e.x);
 #pragma unroll
                 for (int k = 0; k < NP; k++)
-                    r[k] = dmax(r[k], cut_add_f64<2>(ldd(lane + e.z * NP + k * 256), dw[k] >> (8 * c + 7), ce, khi));
+                    r[k] = dmax(r[k], cut_add_f64<2>(ldd(lane + ez * NP + k * 256), dw[k] >> (8 * c + 7), ce, khi));
             }
 #pragma unroll
             for (int k = 0; k < NP; k++) {
@@ -1201,12 +1233,20 @@ __device__ __forceinline__ void schedule_mpw(uint64_t A, uint64_t B, uint64_t dA
             const uint32_t nx = b.z & 0xFFFFu;
 #pragma unroll 1
             for (uint32_t q = 0; q < nx; q++) {   // further inputs (uniform trip count)
-                const uint4 e = lds128(x);
+                double ce;
+                uint32_t ez;
+                if (PP_EXTRA_SPLIT) {
+                    ce = ldd(x);
+                    ez = lds32(x + 8);
+                } else {
+                    const uint4 e = lds128(x);
+                    ce = __hiloint2double((int)e.y, (int)e.x);
+                    ez = e.z;
+                }
                 x += sizeof(ExtraRec);
-                const double ce = __hiloint2double((int)e.y, (int)e.x);
 #pragma unroll
                 for (int k = 0; k < NP; k++)
-                    r[k] = dmax(r[k], cut_add_f64<M>(ldd(lane + e.z * NP + k * 256), dc[k], ce, khi));
+                    r[k] = dmax(r[k], cut_add_f64<M>(ldd(lane + ez * NP + k * 256), dc[k], ce, khi));
             }
 #pragma unroll
             for (int k = 0; k < NP; k++) {
