@@ -613,6 +613,9 @@ __device__ __forceinline__ void schedule_gen(Gen &gen, uint64_t (&mk)[NP], typen
     }
 }
 
+#ifndef PP_BIG_REC_PREFETCH
+#define PP_BIG_REC_PREFETCH 1   // global tier: next record loaded one step ahead (A/B: profiles/r02_big_bench_prefetch.txt)
+#endif
 // ------------------------------------------------ tagged-f64 specialisation
 // State per placement: prev = finish time of the previous step as an exact
 // integer double (UNTAGGED), pdev = its device, and the other devices' free
@@ -715,10 +718,29 @@ __device__ __forceinline__ void schedule_f64(Gen &gen, uint64_t (&mk)[NP], typen
     };
     Addr x = xr;
 
+    // global tier (GmemSpace): records are consumed strictly in address order
+    // (forward π, then the backward records), so the next step's
+    // record is loaded when a step starts, off the L1 latency of the next one.
+    // With two placements per lane (M ≤ 2) only: at NP = 1 (M ≥ 3) the extra
+    // registers spill (A/B: profiles/r02_big_bench_prefetch.txt)
+    constexpr bool kRecPrefetch = std::is_same<S, GmemSpace>::value && PP_BIG_REC_PREFETCH && NP >= 2;
+    uint4 na = {0, 0, 0, 0}, nb = {0, 0, 0, 0};
+    if constexpr (kRecPrefetch) {
+        na = S::rec(ops);
+        nb = S::rec(ops + 16);
+    }
     auto step = [&](auto KNc, Addr rec, uint32_t p, uint32_t c, bool fwd) {
         constexpr int KN = decltype(KNc)::value;   // placements 0..KN−1 (KN < NP: the shared prefix)
-        const uint4 a = S::rec(rec);
-        const uint4 b = S::rec(rec + 16);
+        uint4 a, b;
+        if constexpr (kRecPrefetch) {
+            a = na;
+            b = nb;
+            na = S::rec(rec + sizeof(OpRec));        // past the last record: the extras (unused)
+            nb = S::rec(rec + sizeof(OpRec) + 16);
+        } else {
+            a = S::rec(rec);
+            b = S::rec(rec + 16);
+        }
         const double cost = __hiloint2double((int)a.y, (int)a.x);
         const double c0 = __hiloint2double((int)a.w, (int)a.z);
         uint32_t dev[NP];
