@@ -37,7 +37,8 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     KernelInfo kernel_for_m##m(int gen, bool mem, bool wa, bool f64, int np, bool hw); \
     UpdateFn update_for_m##m(int gen);                                                 \
     XKernelInfo exact_for_m##m(int gen);                                              \
-    KernelInfo big_for_m##m(int gen, bool f64);
+    KernelInfo big_for_m##m(int gen, bool f64);                                      \
+    KernelInfo rp_kernel_for_m##m(bool mem, int np);
 PP_DECL_M(1) PP_DECL_M(2) PP_DECL_M(3) PP_DECL_M(4) PP_DECL_M(5) PP_DECL_M(6) PP_DECL_M(7) PP_DECL_M(8)
 
 KernelInfo kernel_for(int M, int gen, bool mem, bool wa, bool f64, int np, bool hw) {
@@ -63,6 +64,9 @@ KernelInfo big_kernel_for(int M, int gen, bool f64) {
         case 7: return big_for_m7(gen, f64);
         default: return big_for_m8(gen, f64);
     }
+}
+static KernelInfo rp_kernel_for(int M, bool mem, int np) {
+    return M == 4 ? rp_kernel_for_m4(mem, np) : rp_kernel_for_m8(mem, np);
 }
 UpdateFn update_for(int M, int gen) {
     switch (M) {
@@ -138,9 +142,9 @@ struct Choice {
     uint32_t region = 0, slots_off = 0;
 };
 
-static int choose(const pp_dfg *g, int M, int gen, bool write_all, int np, Choice &c) {
+static int choose(const pp_dfg *g, int M, int gen, bool write_all, int np, Choice &c, bool rp = false) {
     const bool mem = g->cap > 0;
-    c.k = kernel_for(M, gen, mem, write_all, g->f64, np, g->hw);
+    c.k = rp ? rp_kernel_for(M, mem, np) : kernel_for(M, gen, mem, write_all, g->f64, np, g->hw);
     c.np = write_all ? 2 : np;
     const uint32_t nslot = (uint32_t)g->W + 1;                  // live + zero
     c.region = (nslot + (M > 2 ? (uint32_t)M : 0u)) * kSlotUnit * c.np;
@@ -366,7 +370,17 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
         cudaEventDestroy(e1);
         g->tuned[key] = cands[pick].np;
     }
-    const Choice &best = cands[pick];
+    Choice best = cands[pick];
+    // the device-word schedule with the next step's record prefetched (RP) when
+    // few warps are resident (< 20 per SM, e.g. GNMT's 22 live values): GNMT
+    // M = 4 +2.5%, while 24-warp configurations lose 0.4–1.4% to its extra
+    // registers (profiles/r02_ab_rec_prefetch.txt).  PP_RP=0/1 overrides.
+    if (gen == GEN_PERTURB && (M == 4 || M == 8) && g->f64 && !g->hw && !write_all) {
+        const char *rv = getenv("PP_RP");
+        const bool want = rv ? atoi(rv) != 0 : best.ctas * best.threads / 32 < 20;
+        Choice c2;
+        if (want && choose(g, M, gen, write_all, best.np, c2, true) == PP_OK) best = c2;
+    }
     if (getenv("PP_VERBOSE")) {
         cudaFuncAttributes fa;
         cudaFuncGetAttributes(&fa, best.k.func);

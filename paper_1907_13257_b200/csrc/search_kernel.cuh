@@ -1162,7 +1162,7 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
 // arithmetic is schedule_f64's for M ≥ 3, operation for operation; only the
 // devices and cut flags are derived differently, so the results are identical
 // (the parity suite runs both).
-template <int M, int NP, bool MEM>
+template <int M, int NP, bool MEM, bool RP = false>
 __device__ __forceinline__ void schedule_mpw(uint64_t A, uint64_t B, uint64_t dA, uint32_t hk0, uint64_t (&mk)[NP],
                                              uint32_t ops, uint32_t xr, const uint64_t *__restrict__ mem, uint32_t lane,
                                              uint32_t free_off, uint32_t K8, uint64_t cap, uint32_t khi, uint32_t tau,
@@ -1212,6 +1212,16 @@ __device__ __forceinline__ void schedule_mpw(uint64_t A, uint64_t B, uint64_t dA
             dprev[k] = dw[k];
         }
     };
+    // records are read in address order (forward, then backward): with RP the
+    // next step's record is loaded when a step starts (+10 registers; used when
+    // few warps are resident, e.g. GNMT: profiles/r02_ab_rec_prefetch.txt)
+    double rcost = 0.0, rc0 = 0.0;
+    uint4 rb = {0, 0, 0, 0};
+    if constexpr (RP) {
+        rcost = ldd(ops);
+        rc0 = ldd(ops + 8);
+        rb = lds128(ops + 16);
+    }
     // free[dev] of the next step of the half-group, loaded at the end of the
     // current step (after its write-back of free[pdev]), so the shared-memory
     // latency is off the step's dependency chain.  If the next step stays on
@@ -1221,9 +1231,20 @@ __device__ __forceinline__ void schedule_mpw(uint64_t A, uint64_t B, uint64_t dA
     auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
         const bool pre_in = PP_MPW_PREFETCH && (fwd ? c != 0 : c != 3);    // compile-time (unrolled c)
         const bool pre_out = PP_MPW_PREFETCH && (fwd ? c != 3 : c != 0);
-        const double cost = ldd(rec);
-        const double c0 = ldd(rec + 8);
-        const uint4 b = lds128(rec + 16);
+        double cost, c0;
+        uint4 b;
+        if constexpr (RP) {   // this step's record was loaded when the previous step started
+            cost = rcost;
+            c0 = rc0;
+            b = rb;
+            rcost = ldd(rec + sizeof(OpRec));
+            rc0 = ldd(rec + sizeof(OpRec) + 8);
+            rb = lds128(rec + sizeof(OpRec) + 16);
+        } else {
+            cost = ldd(rec);
+            c0 = ldd(rec + 8);
+            b = lds128(rec + 16);
+        }
         double cut[NP];
         uint32_t dc[NP], a[NP];
 #pragma unroll
@@ -1410,7 +1431,7 @@ __device__ __forceinline__ void grid_argmin(const KParams &P, uint64_t best_mk, 
 }
 
 // ------------------------------------------------------------------ kernel
-template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64, int NP, bool HW>
+template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64, int NP, bool HW, bool RP = false>
 __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(const KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t mbar;
@@ -1548,7 +1569,7 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
             const uint64_t Wd = (P.K + 7) / 8;
             const uint64_t A = (P.seed ^ 0xD1B54A32D192ED03ull) + kGamma * (i0 * Wd + 1);
             const uint64_t B = (P.seed ^ 0x8CB92BA72F3D8DD7ull) + kGamma * (i0 * Wd + 1);
-            schedule_mpw<M, NP, MEM>(A, B, kGamma * 32ull * Wd, i0 == 0 ? 0u : 0x80808080u, mk, ops, xr, mem,
+            schedule_mpw<M, NP, MEM, RP>(A, B, kGamma * 32ull * Wd, i0 == 0 ? 0u : 0x80808080u, mk, ops, xr, mem,
                                      lane_region, P.free_off, P.K8, P.cap, P.one_hi, P.tau, smem_base + P.off_hgw);
         } else if (GEN == GEN_PERTURB) {
             PerturbGen<M, NP> g;
@@ -1764,9 +1785,9 @@ __global__ void __launch_bounds__(256) round_update_kernel(const UParams U) {
     }
 }
 
-template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64, int NP, bool HW>
+template <int M, int GEN, bool MEM, bool WRITE_ALL, bool F64, int NP, bool HW, bool RP = false>
 int launch_search(const KParams &p, int grid, int threads, int smem, void *stream) {
-    search_kernel<M, GEN, MEM, WRITE_ALL, F64, NP, HW><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
+    search_kernel<M, GEN, MEM, WRITE_ALL, F64, NP, HW, RP><<<grid, threads, smem, (cudaStream_t)stream>>>(p);
     return (int)cudaGetLastError();
 }
 

@@ -1,0 +1,8 @@
+set -u
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -m gpu -q 2>&1 | tail -2 > gpurun_out/gpu_tests41.txt
+for w in gnmt inception_v3 biglstm; do for M in 4 8; do for rp in 0 1; do
+  r=$(PP_RP=$rp PP_VERBOSE=1 timeout 600 python bench.py --workload $w --M $M --parity off --no-cpu-baseline --steps 3 --warmup 3 2> gpurun_out/rp41_err.txt | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(round(d['value']/1e9,4), round(d['roofline']['frac'],4))")
+  echo "$w M=$M PP_RP=$rp $r $(grep -m1 'pp: M=' gpurun_out/rp41_err.txt)"
+done; done; done > gpurun_out/rp_ab41.txt 2>&1
+timeout 1200 bash tools/bench_matrix.sh > gpurun_out/matrix41.txt 2>&1
