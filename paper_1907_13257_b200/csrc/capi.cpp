@@ -66,7 +66,7 @@ KernelInfo big_kernel_for(int M, int gen, bool f64) {
     }
 }
 static KernelInfo rp_kernel_for(int M, bool mem, int np) {
-    return M == 4 ? rp_kernel_for_m4(mem, np) : rp_kernel_for_m8(mem, np);
+    return M == 2 ? rp_kernel_for_m2(mem, np) : M == 4 ? rp_kernel_for_m4(mem, np) : rp_kernel_for_m8(mem, np);
 }
 UpdateFn update_for(int M, int gen) {
     switch (M) {
@@ -371,11 +371,11 @@ static int setup(const pp_dfg *g, int M, int gen, bool write_all, uint64_t begin
         g->tuned[key] = cands[pick].np;
     }
     Choice best = cands[pick];
-    // the device-word schedule with the next step's record prefetched (RP) when
+    // the PERTURB schedules with the next step's record prefetched (RP) when
     // few warps are resident (< 20 per SM, e.g. GNMT's 22 live values): GNMT
-    // M = 4 +2.5%, while 24-warp configurations lose 0.4–1.4% to its extra
+    // M = 4 +2.6%, while 24-warp configurations lose 0.3–1.4% to its extra
     // registers (profiles/r02_ab_rec_prefetch.txt).  PP_RP=0/1 overrides.
-    if (gen == GEN_PERTURB && (M == 4 || M == 8) && g->f64 && !g->hw && !write_all) {
+    if (gen == GEN_PERTURB && (M == 2 || M == 4 || M == 8) && g->f64 && !g->hw && !write_all) {
         const char *rv = getenv("PP_RP");
         const bool want = rv ? atoi(rv) != 0 : best.ctas * best.threads / 32 < 20;
         Choice c2;

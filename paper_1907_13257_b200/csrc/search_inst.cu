@@ -66,15 +66,15 @@ static KernelInfo info_sym(bool, int np) {
     return info_sym_np<MEM, true>(np);
 }
 
-// the record-prefetch variants of the device-word schedule (PERTURB argmin,
-// M = 4, 8; schedule_mpw RP)
+// the record-prefetch variants of the PERTURB argmin kernels (M = 2: the
+// cut-word schedule, M = 4, 8: the device-word schedule; RP)
 template <bool MEM, int NP>
 static KernelInfo info_rp() {
     return KernelInfo{&launch_search<PP_M, GEN_PERTURB, MEM, false, true, NP, false, true>,
                       reinterpret_cast<const void *>(&search_kernel<PP_M, GEN_PERTURB, MEM, false, true, NP, false, true>)};
 }
 KernelInfo PP_CAT(rp_kernel_for_m, PP_M)(bool mem, int np) {
-    if constexpr (PP_M == 4 || PP_M == 8) {
+    if constexpr (PP_M == 2 || PP_M == 4 || PP_M == 8) {
         if (np >= 4) return mem ? info_rp<true, 4>() : info_rp<false, 4>();
         if (np == 2) return mem ? info_rp<true, 2>() : info_rp<false, 2>();
         return mem ? info_rp<true, 1>() : info_rp<false, 1>();

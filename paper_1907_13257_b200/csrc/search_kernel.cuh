@@ -982,7 +982,7 @@ __device__ __forceinline__ double dsel(uint32_t m, double a, double b) {
 // i_0 + 32k: word g of placement i is mix64(key(i) + γ·g) with key(i) =
 // (seed ⊕ C1) + γ·(i·Wd + 1), i.e. mix64(A_g + k·Δ) with A_g = key(i_0) + γ·g
 // (one running 64-bit value per lane) and Δ = γ·32·Wd (uniform).
-template <int NP, bool MEM>
+template <int NP, bool MEM, bool RP = false>
 __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t hk0, uint64_t (&mk)[NP], uint32_t ops,
                                              uint32_t xr, const uint64_t *__restrict__ mem, uint32_t lane, uint32_t K8,
                                              uint64_t cap, uint32_t khi, uint32_t tau) {
@@ -1027,10 +1027,27 @@ __device__ __forceinline__ void schedule_m2p(uint64_t A, uint64_t dA, uint32_t h
         }
     };
 
+    // records are read in address order: with RP the next step's record is
+    // loaded when a step starts (used when few warps are resident; as
+    // schedule_mpw, profiles/r02_ab_rec_prefetch.txt)
+    double rcost = 0.0, rc0 = 0.0;
+    uint4 rb = {0, 0, 0, 0};
+    if constexpr (RP) {
+        rcost = ldd(ops);
+        rc0 = ldd(ops + 8);
+        rb = lds128(ops + 16);
+    }
     auto step = [&](uint32_t rec, uint32_t p, uint32_t c, bool fwd) {
         uint4 a, b;
         double cost, c0;
-        if (PP_M2P_LDS64) {
+        if constexpr (RP) {
+            cost = rcost;
+            c0 = rc0;
+            b = rb;
+            rcost = ldd(rec + sizeof(OpRec));
+            rc0 = ldd(rec + sizeof(OpRec) + 8);
+            rb = lds128(rec + sizeof(OpRec) + 16);
+        } else if (PP_M2P_LDS64) {
             cost = ldd(rec);
             c0 = ldd(rec + 8);
             b = lds128(rec + 16);
@@ -1563,7 +1580,7 @@ __global__ void __launch_bounds__(PP_CTA_THREADS, PP_MIN_CTAS) search_kernel(con
         } else if constexpr (GEN == GEN_PERTURB && kM2P) {
             const uint64_t Wd = (P.K + 7) / 8;
             const uint64_t A = (P.seed ^ 0xD1B54A32D192ED03ull) + kGamma * (i0 * Wd + 1);
-            schedule_m2p<NP, MEM>(A, kGamma * 32ull * Wd, i0 == 0 ? 0u : 0x80808080u, mk, ops, xr, mem, lane_region,
+            schedule_m2p<NP, MEM, RP>(A, kGamma * 32ull * Wd, i0 == 0 ? 0u : 0x80808080u, mk, ops, xr, mem, lane_region,
                                   P.K8, P.cap, P.one_hi, P.tau);
         } else if constexpr (GEN == GEN_PERTURB && kMPW) {
             const uint64_t Wd = (P.K + 7) / 8;
