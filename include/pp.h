@@ -123,6 +123,11 @@ int  pp_load_dfg(const pp_dfg_desc *desc, const pp_link_desc *link, int cuda_dev
  * PP_E_TOO_LARGE when the rows do not fit in the 96 KB image.              */
 int  pp_load_dfg_hw(const pp_dfg_desc *desc, const pp_hw_desc *hw, int cuda_device, pp_dfg **out);
 void pp_free_dfg(pp_dfg *dfg);
+/* Host only (no CUDA device needed): what pp_load_dfg would build for this
+ * DFG — validation with the same errors, π, the slot allocation (num_slots =
+ * W), the image size, T_1, Σ param_bytes — and the state tier it would run on
+ * (*tier = PP_TIER_SHARED / PP_TIER_GLOBAL, pp_dfg_get_tier).  Host ptrs.   */
+int  pp_plan_dfg(const pp_dfg_desc *desc, const pp_link_desc *link, pp_dfg_info *info, int32_t *tier);
 int  pp_dfg_get_info(const pp_dfg *dfg, pp_dfg_info *out);
 /* The state tier the DFG runs on, decided at load time:
  *   PP_TIER_SHARED  image and lane state in shared memory (every kernel);

@@ -31,7 +31,8 @@ static uint64_t g_timing_n = 0;
 void set_error(const std::string &msg) { g_err = msg; }
 void note_launch() { g_launches++; }
 
-int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *hw, int cuda_device, pp_dfg **out);
+int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *hw, int cuda_device, pp_dfg **out,
+             pp_dfg_info *plan = nullptr, int32_t *plan_tier = nullptr);
 
 #define PP_DECL_M(m)                                                                   \
     KernelInfo kernel_for_m##m(int gen, bool mem, bool wa, bool f64, int np, bool hw); \
@@ -649,6 +650,11 @@ void pp_set_kernel_timing(int enable) {
 void pp_get_kernel_timing(double *total_ms, uint64_t *n) {
     if (total_ms) *total_ms = g_timing_ms;
     if (n) *n = g_timing_n;
+}
+
+int pp_plan_dfg(const pp_dfg_desc *desc, const pp_link_desc *link, pp_dfg_info *info, int32_t *tier) {
+    if (!info) { set_error("info is NULL"); return PP_E_INVALID; }
+    return load_dfg(desc, link, nullptr, 0, nullptr, info, tier);
 }
 
 int pp_load_dfg(const pp_dfg_desc *desc, const pp_link_desc *link, int cuda_device, pp_dfg **out) {

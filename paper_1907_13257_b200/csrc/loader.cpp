@@ -99,10 +99,14 @@ static void route_costs(const pp_hw_desc *hw, uint64_t bytes, int src, std::vect
     }
 }
 
+// plan / plan_tier non-null: a dry run (pp_plan_dfg) — validation, π, the
+// slot allocation and the tier, reported without touching a device.
 int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *hw, int cuda_device,
-             pp_dfg **out) {
-    if (!out) return fail(PP_E_INVALID, "out is NULL");
-    *out = nullptr;
+             pp_dfg **out, pp_dfg_info *plan, int32_t *plan_tier) {
+    const bool dry = plan != nullptr;
+    if (!out && !dry) return fail(PP_E_INVALID, "out is NULL");
+    if (out) *out = nullptr;
+    if (dry && !plan_tier) return fail(PP_E_INVALID, "tier is NULL");
     if (!d || (!link && !hw)) return fail(PP_E_INVALID, "desc or link is NULL");
     if (hw) {
         if (hw->num_devices < 1 || hw->num_devices > 8 || hw->num_routers < 0 || hw->num_links < 0 ||
@@ -383,6 +387,19 @@ int load_dfg(const pp_dfg_desc *d, const pp_link_desc *link, const pp_hw_desc *h
     }
     if (!big && bytes > (size_t)kMaxImageBytes) return fail(PP_E_TOO_LARGE, "DFG image exceeds 96 KB of shared memory");
     if (bytes >= (size_t)1 << 31) return fail(PP_E_TOO_LARGE, "DFG image exceeds 2 GB");
+    if (dry) {
+        plan->num_ops = K;
+        plan->num_edges = E;
+        plan->num_slots = W;
+        plan->image_bytes = (int32_t)bytes;
+        plan->t1_ps = (uint64_t)t1;
+        uint64_t gb = 0;
+        if (d->param_bytes)
+            for (int k = 0; k < K; k++) gb += d->param_bytes[k];
+        plan->grad_bytes = gb;
+        *plan_tier = big ? PP_TIER_GLOBAL : PP_TIER_SHARED;
+        return PP_OK;
+    }
 
     pp_dfg *g = new pp_dfg();
     g->device = cuda_device;

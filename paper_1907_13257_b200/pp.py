@@ -102,6 +102,7 @@ SIGNATURES = {
     "pp_dfg_get_info": ([C.c_void_p, P(DfgInfo)], C.c_int),
     "pp_dfg_get_pi": ([C.c_void_p, P(C.c_int32)], C.c_int),
     "pp_dfg_get_tier": ([C.c_void_p], C.c_int),
+    "pp_plan_dfg": ([P(DfgDesc), P(LinkDesc), P(DfgInfo), P(C.c_int32)], C.c_int),
     "pp_eval_placements": ([C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
     "pp_eval_generated": ([C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint64,
                            C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
@@ -402,6 +403,28 @@ class Dfg:
                                     _stream(stream), C.byref(res)))
         return SearchResult(int(res.best_makespan_ps), int(res.best_index), int(res.best_round),
                             int(res.t1_ps), int(res.evaluated), pl)
+
+
+def plan(spec: dict) -> dict:
+    """Host-only dry run of pp_load_dfg (pp_plan_dfg): K, E, the live slots W,
+    the image bytes, T_1, Σ param_bytes and the state tier, with no device."""
+    K = len(spec["fwd_ps"])
+    fwd, bwd = _u64(spec["fwd_ps"]), _u64(spec["bwd_ps"])
+    src = np.ascontiguousarray(np.asarray(spec["edge_src"], dtype=np.int32))
+    dst = np.ascontiguousarray(np.asarray(spec["edge_dst"], dtype=np.int32))
+    bf = _u64(spec["edge_fwd_bytes"])
+    bb = _u64(spec["edge_bwd_bytes"]) if spec.get("edge_bwd_bytes") is not None else None
+    ids = np.ascontiguousarray(np.asarray(spec["op_id"], dtype=np.int64)) if spec.get("op_id") is not None else None
+    mem = _u64(spec["mem_bytes"]) if spec.get("mem_bytes") is not None else None
+    par = _u64(spec["param_bytes"]) if spec.get("param_bytes") is not None else None
+    desc = DfgDesc(K, len(src), _ptr(ids, C.c_int64), _ptr(fwd, C.c_uint64), _ptr(bwd, C.c_uint64),
+                   _ptr(mem, C.c_uint64), _ptr(par, C.c_uint64), _ptr(src, C.c_int32), _ptr(dst, C.c_int32),
+                   _ptr(bf, C.c_uint64), _ptr(bb, C.c_uint64))
+    link = LinkDesc(int(spec["link_bw_Bps"]), int(spec["link_lat_ps"]), int(spec.get("dev_mem_cap_bytes") or 0))
+    info, tier = DfgInfo(), C.c_int32()
+    _check(lib().pp_plan_dfg(C.byref(desc), C.byref(link), C.byref(info), C.byref(tier)))
+    return {"K": info.num_ops, "E": info.num_edges, "W": info.num_slots, "image_bytes": info.image_bytes,
+            "t1": int(info.t1_ps), "grad_bytes": int(info.grad_bytes), "tier": tier.value}
 
 
 # ------------------------------------------------------------ multi-GPU
